@@ -1,0 +1,158 @@
+/* bl_b200.h — C ABI of the B200-native batched joint CTC/attention decoder.
+ *
+ * Drop-in boundary for the reference decoding path (beamlattice,
+ * /root/reference/proj). Plain pointers and sizes only; every entry point
+ * names the reference interface it replaces. The C++ drop-in headers
+ * (include/beamlattice/b200.hpp) and the Python mirror
+ * (paper_2101_05600_b200/) are thin layers over these calls.
+ *
+ * Status codes map to the reference's exception types:
+ *   BL_INVALID_ARGUMENT -> std::invalid_argument
+ *   BL_RUNTIME_ERROR    -> std::runtime_error
+ *   BL_LOGIC_ERROR      -> std::logic_error
+ *   BL_CUDA_ERROR       -> (new) CUDA failure; no CPU fallback exists.
+ * The message of the last failure on the calling thread is bl_last_error().
+ */
+#ifndef BL_B200_H
+#define BL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BL_OK 0
+#define BL_INVALID_ARGUMENT 1
+#define BL_RUNTIME_ERROR 2
+#define BL_LOGIC_ERROR 3
+#define BL_CUDA_ERROR 4
+
+/* kNoMargin (ctc_prefix.hpp:12) */
+#define BL_NO_MARGIN (1 << 29)
+
+/* EosMode / EosTrigger (beam_search.hpp:14-15) */
+#define BL_EOS_BASELINE 0
+#define BL_EOS_CTC 1
+#define BL_EOS_BOTH 2
+#define BL_TRIGGER_BASELINE 0
+#define BL_TRIGGER_CTC 1
+#define BL_TRIGGER_MAX_LEN 2
+
+/* DecoderConfig (beam_search.hpp:21-33), same fields, same defaults via
+ * bl_config_default. */
+typedef struct bl_config {
+  int beam_width;         /* B, default 3 */
+  double ctc_weight;      /* lambda, default 0.3 */
+  int eos_m;              /* default 3 */
+  double eos_dend;        /* nats, default -10 */
+  int eos_c;              /* default 2 */
+  int margin_m1;          /* default 5 */
+  int margin_m2;          /* default BL_NO_MARGIN */
+  int eos_mode;           /* default BL_EOS_BOTH */
+  double max_steps_ratio; /* default 1.0 */
+} bl_config;
+
+/* Utterance (grid.hpp:50-54) with its PosteriorGrid (grid.hpp:24-43):
+ * num_frames x vocab float32 natural-log posteriors, row-major, blank last.
+ * `logp` is a host pointer, or a device pointer when the decode call says so
+ * (device grids must be 16-byte aligned). */
+typedef struct bl_utt {
+  const char* id;
+  uint32_t num_frames;
+  uint32_t vocab;
+  uint32_t frame_shift_ms;
+  const float* logp;
+} bl_utt;
+
+typedef struct bl_scorer bl_scorer;
+typedef struct bl_decoder bl_decoder;
+typedef struct bl_results bl_results;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* bl_last_error(void);
+
+/* ---- configuration ------------------------------------------------------ */
+void bl_config_default(bl_config* cfg);
+/* DecoderConfig::validate (beam_search.cpp:36-46), same messages. */
+int bl_config_validate(const bl_config* cfg);
+
+/* ---- host-side path pieces (integer-exact, no GPU needed) ---------------- */
+/* hard_segments (segmentation.hpp:64-65, segmentation.cpp:121-133):
+ * writes up to `cap` half-open [start,end) pairs, *n_out = segment count. */
+int bl_hard_segments(int num_frames, int min_len, int max_len, int* starts,
+                     int* ends, int cap, int* n_out);
+/* make_batches (batched.hpp:20-21, batched.cpp:12-30): stable ascending
+ * sort by true_frames; order[n] receives the sorted input indices, batches
+ * are consecutive chunks of batch_size. */
+int bl_make_batches(int n, const uint32_t* true_frames, int batch_size,
+                    int* order, int* n_batches);
+
+/* ---- scorers: the "model load" hook (make_scorer, scorer.hpp:84) --------- */
+/* spec: "uniform" | "table:PATH" | "loop:TOKEN:P" (scorer.cpp:117-135). */
+int bl_scorer_create(const char* spec, int num_tokens, bl_scorer** out);
+/* In-memory TableScorer (scorer.hpp:38-55): n_entries contexts of length
+ * ctx_len[k] <= order-1 packed in ctx[k*max(order-1,1) ...], each with a
+ * normalized (|C|+1)-vector logp[k*(num_tokens+1) ...] (checked like
+ * TableScorer::add_entry, scorer.cpp:46-51). Later duplicates replace
+ * earlier ones, as std::map assignment does. */
+int bl_scorer_create_table(int num_tokens, int order, int n_entries,
+                           const int* ctx_len, const int* ctx,
+                           const double* logp, bl_scorer** out);
+int bl_scorer_create_loop(int num_tokens, int loop_token, double p_loop,
+                          bl_scorer** out);
+int bl_scorer_num_tokens(const bl_scorer* s);
+/* The attention vector the scorer returns for a prefix (Scorer::score,
+ * scorer.hpp:20-21), computed host-side; out has num_tokens+1 entries. */
+int bl_scorer_score(const bl_scorer* s, const int* prefix, int n, double* out);
+void bl_scorer_destroy(bl_scorer* s);
+
+/* ---- decoder: one handle per GPU, one CUDA stream per handle ------------ */
+int bl_decoder_create(int device, const bl_config* cfg, const bl_scorer* scorer,
+                      bl_decoder** out);
+/* nbest: finished hypotheses kept per utterance in the results (>= 1).
+ * exact: 1 = every candidate scored by the fp64 reference-order recursion
+ *        (fp64-decision mode); 0 = fp32 factorised bulk with certified fp64
+ *        refinement of every candidate near the top-B boundary (default).
+ * slack: half-width multiplier of the certified interval (default 1.0). */
+int bl_decoder_set_options(bl_decoder* d, int nbest, int exact, double slack);
+/* Use an external CUDA stream (cudaStream_t as void*); NULL = own stream. */
+int bl_decoder_set_stream(bl_decoder* d, void* stream);
+void bl_decoder_destroy(bl_decoder* d);
+
+/* batched_beam_search (batched.hpp:34-38): decodes the utterances of ONE
+ * batch (or any number of batches back to back — results are independent
+ * of grouping) and returns results in the given order. grids_on_device=1
+ * means utts[i].logp are device pointers on the decoder's GPU; 0 means host
+ * memory (copied through pinned staging inside the call). Blocks until the
+ * results are in host memory. */
+int bl_decode(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
+              bl_results** out);
+
+/* ---- results (DecodeResult, beam_search.hpp:35-42) ---------------------- */
+int bl_results_count(const bl_results* r);
+int bl_results_get(const bl_results* r, int i, const char** id,
+                   const int** tokens, int* n_tokens, double* joint_logp,
+                   const int** label_times, int* steps, int* eos_trigger);
+/* n-best (new): k-th best finished hypothesis of utterance i, best first;
+ * returns BL_INVALID_ARGUMENT past the available count (bl_results_nbest_count). */
+int bl_results_nbest_count(const bl_results* r, int i);
+int bl_results_nbest(const bl_results* r, int i, int k, const int** tokens,
+                     int* n_tokens, double* joint_logp, const int** label_times);
+/* DecodeCounters (beam_search.hpp:68-79) summed over the call. */
+int bl_results_counters(const bl_results* r, uint64_t* steps,
+                        uint64_t* scorer_queries, uint64_t* ctc_frames_evaluated);
+/* Instrumentation: device time of the decode kernel(s) on the decoder's
+ * stream (CUDA events), algorithmic prefix-score bytes, kernel
+ * launches, and the count of utterance-steps that took the exact fallback. */
+int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1_bytes,
+                     int* launches, uint64_t* fallback_steps,
+                     uint64_t* contenders);
+void bl_results_destroy(bl_results* r);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,531 @@
+"""Python mirror of the beamlattice decoder API over the B200 C ABI.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/beamlattice/*.hpp), so code and tests written
+against the reference read the same here. Every call goes through
+``libbl_b200.so`` (include/bl_b200.h); decoding runs only on the GPU and the
+module raises if the CUDA library is missing — there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+import os
+import struct
+from dataclasses import dataclass, field
+from typing import Dict, Iterable, List, Optional, Sequence, Tuple
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libbl_b200.so")
+
+NO_MARGIN = 1 << 29  # kNoMargin, ctc_prefix.hpp:12
+K_LOG_ZERO = -1e30   # logmath.hpp:11
+
+BL_OK, BL_INVALID_ARGUMENT, BL_RUNTIME_ERROR, BL_LOGIC_ERROR, BL_CUDA_ERROR = range(5)
+EOS_MODES = ("baseline", "ctc", "both")
+TRIGGERS = ("baseline", "ctc", "max_len")
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error."""
+
+
+class CudaError(RuntimeError):
+    """CUDA failure in the device decoder (no CPU fallback exists)."""
+
+
+class _Config(C.Structure):
+    _fields_ = [("beam_width", C.c_int), ("ctc_weight", C.c_double),
+                ("eos_m", C.c_int), ("eos_dend", C.c_double), ("eos_c", C.c_int),
+                ("margin_m1", C.c_int), ("margin_m2", C.c_int),
+                ("eos_mode", C.c_int), ("max_steps_ratio", C.c_double)]
+
+
+class _Utt(C.Structure):
+    _fields_ = [("id", C.c_char_p), ("num_frames", C.c_uint32),
+                ("vocab", C.c_uint32), ("frame_shift_ms", C.c_uint32),
+                ("logp", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libbl_b200.so (built by __graft_entry__.build()); fail loudly."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build the sm_100a extension with "
+            "`python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    vp, ip, dp = C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_double)
+    L.bl_last_error.restype = C.c_char_p
+    L.bl_config_default.argtypes = [C.POINTER(_Config)]
+    L.bl_config_validate.argtypes = [C.POINTER(_Config)]
+    L.bl_hard_segments.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip, C.c_int, ip]
+    L.bl_make_batches.argtypes = [C.c_int, C.POINTER(C.c_uint32), C.c_int, ip, ip]
+    L.bl_scorer_create.argtypes = [C.c_char_p, C.c_int, C.POINTER(vp)]
+    L.bl_scorer_create_table.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip, dp,
+                                         C.POINTER(vp)]
+    L.bl_scorer_create_loop.argtypes = [C.c_int, C.c_int, C.c_double, C.POINTER(vp)]
+    L.bl_scorer_num_tokens.argtypes = [vp]
+    L.bl_scorer_score.argtypes = [vp, ip, C.c_int, dp]
+    L.bl_scorer_destroy.argtypes = [vp]
+    L.bl_decoder_create.argtypes = [C.c_int, C.POINTER(_Config), vp, C.POINTER(vp)]
+    L.bl_decoder_set_options.argtypes = [vp, C.c_int, C.c_int, C.c_double]
+    L.bl_decoder_set_stream.argtypes = [vp, vp]
+    L.bl_decoder_destroy.argtypes = [vp]
+    L.bl_decode.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.c_int, C.POINTER(vp)]
+    L.bl_results_count.argtypes = [vp]
+    L.bl_results_get.argtypes = [vp, C.c_int, C.POINTER(C.c_char_p), C.POINTER(ip),
+                                 ip, dp, C.POINTER(ip), ip, ip]
+    L.bl_results_nbest_count.argtypes = [vp, C.c_int]
+    L.bl_results_nbest.argtypes = [vp, C.c_int, C.c_int, C.POINTER(ip), ip, dp,
+                                   C.POINTER(ip)]
+    u64p = C.POINTER(C.c_uint64)
+    L.bl_results_counters.argtypes = [vp, u64p, u64p, u64p]
+    L.bl_results_stats.argtypes = [vp, dp, u64p, ip, u64p, u64p]
+    L.bl_results_destroy.argtypes = [vp]
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc == BL_OK:
+        return
+    msg = lib().bl_last_error().decode()
+    if rc == BL_INVALID_ARGUMENT:
+        raise InvalidArgument(msg)
+    if rc == BL_LOGIC_ERROR:
+        raise LogicError(msg)
+    if rc == BL_CUDA_ERROR:
+        raise CudaError(msg)
+    raise RuntimeError(msg)
+
+
+# ------------------------------------------------------------------ config
+@dataclass
+class DecoderConfig:
+    """beam_search.hpp:21-33 (same defaults)."""
+    beam_width: int = 3
+    ctc_weight: float = 0.3
+    eos_m: int = 3
+    eos_dend: float = -10.0
+    eos_c: int = 2
+    margin_m1: int = 5
+    margin_m2: int = NO_MARGIN
+    eos_mode: str = "both"
+    max_steps_ratio: float = 1.0
+
+    def _c(self) -> _Config:
+        if self.eos_mode not in EOS_MODES:
+            raise InvalidArgument("unknown eos mode: " + str(self.eos_mode))
+        return _Config(self.beam_width, self.ctc_weight, self.eos_m, self.eos_dend,
+                       self.eos_c, self.margin_m1, self.margin_m2,
+                       EOS_MODES.index(self.eos_mode), self.max_steps_ratio)
+
+    def validate(self) -> None:
+        """DecoderConfig::validate (beam_search.cpp:36-46)."""
+        c = self._c()
+        _check(lib().bl_config_validate(C.byref(c)))
+
+
+def eos_mode_from_string(s: str) -> str:
+    """beam_search.cpp:29-34."""
+    if s not in EOS_MODES:
+        raise InvalidArgument("unknown eos mode: " + s)
+    return s
+
+
+# -------------------------------------------------------------- data model
+@dataclass
+class PosteriorGrid:
+    """grid.hpp:24-43: T x (|C|+1) float32 log-posteriors, blank last."""
+    logp: np.ndarray
+    frame_shift_ms: int = 10
+
+    def __post_init__(self):
+        self.logp = np.ascontiguousarray(self.logp, dtype=np.float32)
+        if self.logp.ndim != 2:
+            raise InvalidArgument("grid must be 2-D [T, vocab]")
+
+    @property
+    def num_frames(self) -> int:
+        return int(self.logp.shape[0])
+
+    @property
+    def vocab(self) -> int:
+        return int(self.logp.shape[1])
+
+    def num_tokens(self) -> int:
+        return self.vocab - 1
+
+    def blank_id(self) -> int:
+        return self.vocab - 1
+
+    def at(self, frame: int, symbol: int) -> float:
+        """1-based frame, promoted to double (grid.hpp:36-38)."""
+        return float(self.logp[frame - 1, symbol])
+
+    def audio_seconds(self) -> float:
+        return self.num_frames * self.frame_shift_ms / 1000.0
+
+
+@dataclass
+class Utterance:
+    """grid.hpp:50-54."""
+    id: str
+    grid: PosteriorGrid
+    true_frames: int = 0
+
+    def __post_init__(self):
+        if not self.true_frames:
+            self.true_frames = self.grid.num_frames
+
+
+@dataclass
+class Batch:
+    """batched.hpp:13-16."""
+    utterances: List[Utterance]
+    padded_frames: int = 0
+
+
+@dataclass
+class DecodeResult:
+    """beam_search.hpp:35-42, plus the n-best list (new)."""
+    id: str
+    tokens: List[int]
+    joint_logp: float
+    label_times: List[int]
+    steps_taken: int
+    eos_trigger: str
+    nbest: List[Tuple[List[int], float, List[int]]] = field(default_factory=list)
+
+
+@dataclass
+class DecodeCounters:
+    """beam_search.hpp:68-79."""
+    steps: int = 0
+    scorer_queries: int = 0
+    ctc_frames_evaluated: int = 0
+
+    def __iadd__(self, o: "DecodeCounters") -> "DecodeCounters":
+        self.steps += o.steps
+        self.scorer_queries += o.scorer_queries
+        self.ctc_frames_evaluated += o.ctc_frames_evaluated
+        return self
+
+
+@dataclass
+class Segment:
+    """segmentation.hpp:45-50."""
+    utterance_id: str
+    start: int
+    end: int
+    source: str = "hard"
+
+
+# -------------------------------------------------------- host path pieces
+def make_batches(utterances: Sequence[Utterance], batch_size: int) -> List[Batch]:
+    """batched.cpp:12-30 (stable length sort, then chunk)."""
+    n = len(utterances)
+    frames = (C.c_uint32 * max(n, 1))(*[u.true_frames for u in utterances])
+    order = (C.c_int * max(n, 1))()
+    nb = C.c_int()
+    _check(lib().bl_make_batches(n, frames, batch_size, order, C.byref(nb)))
+    out = []
+    for k in range(0, n, batch_size):
+        us = [utterances[order[i]] for i in range(k, min(n, k + batch_size))]
+        out.append(Batch(us, max(u.true_frames for u in us)))
+    return out
+
+
+def hard_segments(num_frames: int, min_len: int, max_len: int,
+                  utterance_id: str = "") -> List[Segment]:
+    """segmentation.cpp:121-133 (integer-exact)."""
+    cap = max(1, num_frames // max(1, max_len) + 2)
+    s = (C.c_int * cap)()
+    e = (C.c_int * cap)()
+    n = C.c_int()
+    _check(lib().bl_hard_segments(num_frames, min_len, max_len, s, e, cap,
+                                  C.byref(n)))
+    return [Segment(utterance_id, s[k], e[k], "hard") for k in range(n.value)]
+
+
+# ------------------------------------------------------------------ scorers
+class Scorer:
+    """Scorer contract (scorer.hpp:16-22), realised as a device scorer."""
+
+    _h: Optional[C.c_void_p] = None
+
+    def num_tokens(self) -> int:
+        return lib().bl_scorer_num_tokens(self._h)
+
+    def score(self, utterance_id: str, prefix: Sequence[int]) -> List[float]:
+        n = len(prefix)
+        arr = (C.c_int * max(n, 1))(*prefix)
+        out = (C.c_double * (self.num_tokens() + 1))()
+        _check(lib().bl_scorer_score(self._h, arr, n, out))
+        return list(out)
+
+    def _key(self):
+        return id(self)
+
+    def __del__(self):
+        if self._h is not None and _lib is not None:
+            _lib.bl_scorer_destroy(self._h)
+            self._h = None
+
+
+class UniformScorer(Scorer):
+    def __init__(self, num_tokens: int):
+        h = C.c_void_p()
+        _check(lib().bl_scorer_create(b"uniform", num_tokens, C.byref(h)))
+        self._h = h
+
+
+class LoopScorer(Scorer):
+    def __init__(self, num_tokens: int, loop_token: int, p_loop: float):
+        h = C.c_void_p()
+        _check(lib().bl_scorer_create_loop(num_tokens, loop_token, p_loop, C.byref(h)))
+        self._h = h
+
+
+class TableScorer(Scorer):
+    """n-gram table keyed by the last order-1 tokens (scorer.hpp:38-55)."""
+
+    def __init__(self, num_tokens: int, order: int):
+        self._n, self._order = num_tokens, order
+        self._entries: Dict[Tuple[int, ...], List[float]] = {}
+        self._rebuild()
+
+    def order(self) -> int:
+        return self._order
+
+    def add_entry(self, context: Sequence[int], logp: Sequence[float]) -> None:
+        new = dict(self._entries)
+        new[tuple(int(x) for x in context)] = [float(v) for v in logp]
+        old = self._entries
+        self._entries = new
+        try:
+            self._rebuild()
+        except Exception:
+            self._entries = old
+            raise
+
+    def entries(self):
+        return dict(self._entries)
+
+    def _rebuild(self):
+        ents = list(self._entries.items())
+        w = max(self._order - 1, 1)
+        n = len(ents)
+        V = self._n + 1
+        clen = (C.c_int * max(n, 1))()
+        ctx = (C.c_int * max(n * w, 1))()
+        lp = (C.c_double * max(n * V, 1))()
+        for k, (c, v) in enumerate(ents):
+            clen[k] = len(c)
+            for i, t in enumerate(c[:w]):
+                ctx[k * w + i] = t
+            if len(v) != V:
+                raise RuntimeError("TableScorer entry: wrong vector size")
+            for i, x in enumerate(v):
+                lp[k * V + i] = x
+        h = C.c_void_p()
+        _check(lib().bl_scorer_create_table(self._n, self._order, n, clen, ctx, lp,
+                                            C.byref(h)))
+        if self._h is not None:
+            lib().bl_scorer_destroy(self._h)
+        self._h = h
+
+
+class _SpecScorer(Scorer):
+    def __init__(self, spec: str, num_tokens: int):
+        h = C.c_void_p()
+        _check(lib().bl_scorer_create(spec.encode(), num_tokens, C.byref(h)))
+        self._h = h
+
+
+def make_scorer(spec: str, num_tokens: int) -> Scorer:
+    """scorer.cpp:117-135: "uniform" | "table:PATH" | "loop:TOKEN:P"."""
+    return _SpecScorer(spec, num_tokens)
+
+
+def save_table_scorer(path: str, scorer: TableScorer) -> None:
+    """scorer.cpp:105-115 file schema."""
+    j = {"order": scorer.order(), "num_tokens": scorer._n,
+         "entries": [{"ctx": list(c), "logp": v}
+                     for c, v in sorted(scorer.entries().items())]}
+    with open(path, "w") as f:
+        f.write(json.dumps(j) + "\n")
+
+
+# ------------------------------------------------------------------ decoder
+class Decoder:
+    """One device decoder (one GPU, one CUDA stream)."""
+
+    def __init__(self, scorer: Scorer, cfg: Optional[DecoderConfig] = None,
+                 device: int = 0, nbest: int = 1, exact: bool = False,
+                 slack: float = 1.0):
+        self.cfg = cfg or DecoderConfig()
+        self.scorer = scorer
+        self.device = device
+        c = self.cfg._c()
+        h = C.c_void_p()
+        _check(lib().bl_decoder_create(device, C.byref(c), scorer._h, C.byref(h)))
+        self._h = h
+        _check(lib().bl_decoder_set_options(h, nbest, 1 if exact else 0, slack))
+        self.last_stats: Dict[str, float] = {}
+
+    def set_stream(self, stream_ptr: int) -> None:
+        lib().bl_decoder_set_stream(self._h, C.c_void_p(stream_ptr or None))
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and _lib is not None:
+            _lib.bl_decoder_destroy(self._h)
+            self._h = None
+
+    def decode_raw(self, descs: Sequence[Tuple[str, int, int, int]],
+                   on_device: bool, counters: Optional[DecodeCounters] = None,
+                   frame_shift_ms: int = 10) -> List[DecodeResult]:
+        """descs: (id, num_frames, vocab, data pointer)."""
+        n = len(descs)
+        arr = (_Utt * max(n, 1))()
+        keep = []
+        for i, (uid, T, V, ptr) in enumerate(descs):
+            b = uid.encode()
+            keep.append(b)
+            arr[i] = _Utt(b, T, V, frame_shift_ms, C.c_void_p(ptr))
+        h = C.c_void_p()
+        _check(lib().bl_decode(self._h, n, arr, 1 if on_device else 0, C.byref(h)))
+        try:
+            return self._collect(h, counters)
+        finally:
+            lib().bl_results_destroy(h)
+
+    def decode(self, utterances: Sequence[Utterance],
+               counters: Optional[DecodeCounters] = None) -> List[DecodeResult]:
+        keep = [u.grid.logp for u in utterances]
+        return self.decode_raw([(u.id, u.grid.num_frames, u.grid.vocab,
+                                 g.ctypes.data) for u, g in zip(utterances, keep)],
+                               on_device=False, counters=counters)
+
+    def _collect(self, h, counters) -> List[DecodeResult]:
+        L = lib()
+        out = []
+        ip = C.POINTER(C.c_int)
+        for i in range(L.bl_results_count(h)):
+            uid = C.c_char_p()
+            tok, lt = ip(), ip()
+            nt, st, tr = C.c_int(), C.c_int(), C.c_int()
+            jt = C.c_double()
+            _check(L.bl_results_get(h, i, C.byref(uid), C.byref(tok), C.byref(nt),
+                                    C.byref(jt), C.byref(lt), C.byref(st),
+                                    C.byref(tr)))
+            n = nt.value
+            r = DecodeResult(uid.value.decode(), [tok[k] for k in range(n)], jt.value,
+                             [lt[k] for k in range(n)], st.value, TRIGGERS[tr.value])
+            for k in range(L.bl_results_nbest_count(h, i)):
+                _check(L.bl_results_nbest(h, i, k, C.byref(tok), C.byref(nt),
+                                          C.byref(jt), C.byref(lt)))
+                m = nt.value
+                r.nbest.append(([tok[q] for q in range(m)], jt.value,
+                                [lt[q] for q in range(m)]))
+            out.append(r)
+        s, q, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        L.bl_results_counters(h, C.byref(s), C.byref(q), C.byref(f))
+        if counters is not None:
+            counters += DecodeCounters(s.value, q.value, f.value)
+        ms, k1, fb, nc = C.c_double(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        nl = C.c_int()
+        L.bl_results_stats(h, C.byref(ms), C.byref(k1), C.byref(nl), C.byref(fb),
+                           C.byref(nc))
+        self.last_stats = {"kernel_ms": ms.value, "k1_bytes": k1.value,
+                           "launches": nl.value, "fallback_steps": fb.value,
+                           "contenders": nc.value, "steps": s.value,
+                           "scorer_queries": q.value, "ctc_frames_evaluated": f.value}
+        return out
+
+
+_decoders: Dict[tuple, Decoder] = {}
+
+
+def _decoder_for(scorer: Scorer, cfg: DecoderConfig, device: int = 0) -> Decoder:
+    key = (scorer._key(), tuple(vars(cfg).values()), device)
+    d = _decoders.get(key)
+    if d is None or d.scorer is not scorer:
+        d = Decoder(scorer, cfg, device)
+        _decoders[key] = d
+    return d
+
+
+def batched_beam_search(batch: Batch, scorer: Scorer, cfg: DecoderConfig,
+                        counters: Optional[DecodeCounters] = None,
+                        device: int = 0) -> List[DecodeResult]:
+    """batched.hpp:34-38: results in batch order."""
+    cfg.validate()
+    if not batch.utterances:
+        return []
+    return _decoder_for(scorer, cfg, device).decode(batch.utterances, counters)
+
+
+def beam_search(utt: Utterance, scorer: Scorer, cfg: DecoderConfig,
+                counters: Optional[DecodeCounters] = None,
+                device: int = 0) -> DecodeResult:
+    """beam_search.hpp:109-111 (a one-utterance batch is exactly Alg. 1)."""
+    return batched_beam_search(Batch([utt], utt.true_frames), scorer, cfg,
+                               counters, device)[0]
+
+
+# ---------------------------------------------------------------------- I/O
+def write_grid(path: str, grid: PosteriorGrid) -> None:
+    """CTCG v1 (grid.cpp:94-106)."""
+    with open(path, "wb") as f:
+        f.write(b"CTCG" + struct.pack("<IIII", 1, grid.num_frames, grid.vocab,
+                                      grid.frame_shift_ms))
+        f.write(grid.logp.astype("<f4").tobytes())
+
+
+def read_grid(path: str) -> PosteriorGrid:
+    """CTCG v1 (grid.cpp:108-127), same error messages."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise RuntimeError("cannot open grid file: " + path)
+    with f:
+        magic = f.read(4)
+        if magic != b"CTCG":
+            raise RuntimeError("bad magic in grid file: " + path)
+        hdr = f.read(16)
+        if len(hdr) < 4 or struct.unpack("<I", hdr[:4])[0] != 1:
+            raise RuntimeError("unsupported grid version in " + path)
+        _, T, V, fs = struct.unpack("<IIII", hdr)
+        data = f.read(4 * T * V)
+        if len(data) != 4 * T * V:
+            raise RuntimeError("truncated grid file: " + path)
+    return PosteriorGrid(np.frombuffer(data, "<f4").reshape(T, V).copy(), fs)
+
+
+def result_json(r: DecodeResult) -> str:
+    """io.cpp:81-92 line; keys sorted as nlohmann::json emits them."""
+    d = {"eos_trigger": r.eos_trigger, "id": r.id, "joint_logp": r.joint_logp,
+         "label_times": r.label_times, "steps": r.steps_taken, "tokens": r.tokens}
+    if r.nbest and len(r.nbest) > 1:
+        d["nbest"] = [{"joint_logp": j, "label_times": lt, "tokens": t}
+                      for t, j, lt in r.nbest]
+    return json.dumps(d, separators=(",", ":"), sort_keys=True)
+
+
+def write_results(fp, results: Iterable[DecodeResult]) -> None:
+    for r in results:
+        fp.write(result_json(r) + "\n")

@@ -1,0 +1,728 @@
+// capi.cu — C ABI of the B200 decoder (include/bl_b200.h): host planner,
+// device workspace, scorer loading, result assembly. Host logic mirrors the
+// reference semantics cited per function; all decoding runs on the GPU —
+// there is no CPU fallback.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <json.hpp>
+
+#include "../../include/bl_b200.h"
+#include "decode.cuh"
+
+namespace bl {
+cudaError_t launch_decode(const KParams& p, cudaStream_t st);
+size_t decode_smem_bytes(const KParams& p);
+int bmax_for(int B);
+}  // namespace bl
+
+namespace {
+
+thread_local std::string g_err;
+
+struct BlError {
+  int code;
+  std::string msg;
+};
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                             \
+  do {                                                                       \
+    cudaError_t _e = (call);                                                 \
+    if (_e != cudaSuccess)                                                   \
+      throw BlError{BL_CUDA_ERROR, std::string(#call) + ": " +               \
+                                       cudaGetErrorString(_e)};              \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    g_err.clear();
+    return f();
+  } catch (const BlError& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return BL_INVALID_ARGUMENT;
+  } catch (const std::logic_error& e) {
+    g_err = e.what();
+    return BL_LOGIC_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return BL_RUNTIME_ERROR;
+  }
+}
+
+// ------------------------------------------------------------ scorers
+// check_normalized, scorer.cpp:14-28
+void check_normalized(const std::vector<double>& v, size_t expected,
+                      const std::string& what) {
+  if (v.size() != expected) throw std::runtime_error(what + ": wrong vector size");
+  double m = -HUGE_VAL;
+  for (double x : v) m = std::max(m, x);
+  double s = 0.0;
+  for (double x : v) s += std::exp(x - m);
+  double lse = m + std::log(s);
+  if (!(std::abs(lse) <= 1e-6)) {
+    std::ostringstream os;
+    os << what << ": vector not normalized (logsumexp=" << lse << ")";
+    throw std::runtime_error(os.str());
+  }
+}
+
+}  // namespace
+
+struct bl_scorer {
+  int kind = 0;  // 0 uniform, 1 table, 2 loop
+  int num_tokens = 0;
+  int order = 1;
+  std::map<std::vector<int>, std::vector<double>> table;
+  int loop_token = 0;
+  double p_loop = 0.0;
+
+  std::vector<double> uniform_row() const {  // scorer.cpp:34-38
+    return std::vector<double>(num_tokens + 1,
+                               -std::log(static_cast<double>(num_tokens + 1)));
+  }
+  std::vector<double> loop_row() const {  // scorer.cpp:73-80
+    double rest = std::log((1.0 - p_loop) / num_tokens);
+    std::vector<double> v(num_tokens + 1, rest);
+    v[loop_token] = std::log(p_loop);
+    return v;
+  }
+  std::vector<double> score(const std::vector<int>& prefix) const {
+    if (kind == 2) return loop_row();
+    if (kind == 1) {  // scorer.cpp:53-62
+      size_t n = std::min<size_t>(prefix.size(), order - 1);
+      std::vector<int> ctx(prefix.end() - n, prefix.end());
+      auto it = table.find(ctx);
+      if (it != table.end()) return it->second;
+    }
+    return uniform_row();
+  }
+};
+
+namespace {
+
+bl_scorer* make_table(int num_tokens, int order) {  // scorer.cpp:40-44
+  if (num_tokens < 1) throw std::invalid_argument("TableScorer: |C| < 1");
+  if (order < 1) throw std::invalid_argument("TableScorer: order < 1");
+  auto* s = new bl_scorer;
+  s->kind = 1;
+  s->num_tokens = num_tokens;
+  s->order = order;
+  return s;
+}
+
+bl_scorer* make_loop(int num_tokens, int loop_token, double p) {  // scorer.cpp:64-71
+  if (num_tokens < 1) throw std::invalid_argument("LoopScorer: |C| < 1");
+  if (loop_token < 0 || loop_token >= num_tokens)
+    throw std::invalid_argument("LoopScorer: loop token out of range");
+  if (!(p > 0.5 && p < 1.0))
+    throw std::invalid_argument("LoopScorer: p_loop must be in (0.5, 1)");
+  auto* s = new bl_scorer;
+  s->kind = 2;
+  s->num_tokens = num_tokens;
+  s->loop_token = loop_token;
+  s->p_loop = p;
+  return s;
+}
+
+// load_table_scorer, scorer.cpp:82-103
+bl_scorer* load_table(const std::string& path) {
+  std::ifstream is(path);
+  if (!is) throw std::runtime_error("cannot open scorer file: " + path);
+  nlohmann::json j;
+  try {
+    is >> j;
+  } catch (const nlohmann::json::exception& e) {
+    throw std::runtime_error("malformed scorer file " + path + ": " + e.what());
+  }
+  if (!j.contains("order") || !j.contains("num_tokens") || !j.contains("entries"))
+    throw std::runtime_error("malformed scorer file " + path + ": missing field");
+  std::unique_ptr<bl_scorer> s(make_table(j["num_tokens"].get<int>(), j["order"].get<int>()));
+  for (const auto& e : j["entries"]) {
+    auto lp = e["logp"].get<std::vector<double>>();
+    check_normalized(lp, static_cast<size_t>(s->num_tokens) + 1, "TableScorer entry");
+    s->table[e["ctx"].get<std::vector<int>>()] = std::move(lp);
+  }
+  return s.release();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------ decoder
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    CK(cudaMalloc(&p, bytes));
+    n = bytes;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct HostBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  void ensure(size_t bytes) {
+    if (bytes <= n) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    n = 0;
+    CK(cudaMallocHost(&p, bytes));
+    n = bytes;
+  }
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+struct bl_decoder {
+  int device = 0;
+  bl_config cfg{};
+  int num_tokens = 0;
+  int nbest = 1;
+  int exact = 0;
+  double slack = 1.0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // device scorer
+  int sc_order = 1, sc_nent = 0, sc_w = 1;
+  DevBuf sc_ctx_len, sc_ctx, sc_row, sc_rows;
+  // workspace
+  DevBuf grid, utts, gam, Ftab, Gtab, keys, xs, taken, hist, fin, res, cnt;
+  HostBuf h_grid, h_utts, h_res, h_cnt;
+};
+
+struct bl_results {
+  struct One {
+    std::string id;
+    std::vector<int> tokens, label_times;
+    double joint = 0.0;
+    int steps = 0, trigger = 2;
+    std::vector<std::vector<int>> nb_tokens, nb_times;
+    std::vector<double> nb_joint;
+  };
+  std::vector<One> r;
+  uint64_t steps = 0, queries = 0, frames = 0, k1 = 0, fallback = 0, contenders = 0;
+  double kernel_ms = 0.0;
+  int launches = 0;
+};
+
+namespace {
+
+void upload_scorer(bl_decoder* d, const bl_scorer* s) {
+  // rows: 0 = uniform fallback, then one row per entry
+  const int V = s->num_tokens + 1;
+  std::vector<double> rows = s->uniform_row();
+  std::vector<std::pair<std::vector<int>, int>> ents;
+  if (s->kind == 2) {
+    auto lr = s->loop_row();
+    rows.insert(rows.end(), lr.begin(), lr.end());
+    ents.push_back({{}, 1});
+    d->sc_order = 1;
+  } else if (s->kind == 1) {
+    int r = 1;
+    for (const auto& kv : s->table) {
+      // only contexts a prefix can produce (len <= order-1) are reachable
+      if ((int)kv.first.size() > s->order - 1) continue;
+      rows.insert(rows.end(), kv.second.begin(), kv.second.end());
+      ents.push_back({kv.first, r++});
+    }
+    d->sc_order = s->order;
+  } else {
+    d->sc_order = 1;
+  }
+  if (d->sc_order - 1 > 8)
+    throw std::invalid_argument("device table scorer supports order <= 9");
+  std::sort(ents.begin(), ents.end(), [](const auto& a, const auto& b) {
+    if (a.first.size() != b.first.size()) return a.first.size() < b.first.size();
+    return a.first < b.first;
+  });
+  d->sc_nent = (int)ents.size();
+  d->sc_w = std::max(d->sc_order - 1, 1);
+  std::vector<int> clen(std::max<size_t>(ents.size(), 1), 0),
+      ctx(std::max<size_t>(ents.size() * d->sc_w, 1), 0),
+      row(std::max<size_t>(ents.size(), 1), 0);
+  for (size_t k = 0; k < ents.size(); ++k) {
+    clen[k] = (int)ents[k].first.size();
+    for (size_t i = 0; i < ents[k].first.size(); ++i) ctx[k * d->sc_w + i] = ents[k].first[i];
+    row[k] = ents[k].second;
+  }
+  (void)V;
+  d->sc_ctx_len.ensure(clen.size() * sizeof(int));
+  d->sc_ctx.ensure(ctx.size() * sizeof(int));
+  d->sc_row.ensure(row.size() * sizeof(int));
+  d->sc_rows.ensure(rows.size() * sizeof(double));
+  CK(cudaMemcpy(d->sc_ctx_len.p, clen.data(), clen.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d->sc_ctx.p, ctx.data(), ctx.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d->sc_row.p, row.data(), row.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d->sc_rows.p, rows.data(), rows.size() * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+// DecoderConfig::validate (beam_search.cpp:36-46)
+void validate_cfg(const bl_config& c) {
+  if (c.beam_width < 1) throw std::invalid_argument("beam width must be >= 1");
+  if (c.ctc_weight < 0.0 || c.ctc_weight > 1.0)
+    throw std::invalid_argument("ctc weight must be in [0, 1]");
+  if (c.eos_m < 1) throw std::invalid_argument("eos M must be >= 1");
+  if (c.eos_c < 0) throw std::invalid_argument("eos C must be >= 0");
+  if (c.margin_m1 < 0 || c.margin_m2 < 0)
+    throw std::invalid_argument("margins must be >= 0");
+  if (!(c.max_steps_ratio > 0.0 && c.max_steps_ratio <= 1.0))
+    throw std::invalid_argument("max steps ratio must be in (0, 1]");
+  if (c.eos_mode < 0 || c.eos_mode > 2) throw std::invalid_argument("unknown eos mode");
+}
+
+float guard_float() {
+  // largest float f with (double)f <= -1e29 (is_log_zero on promoted grids)
+  float f = static_cast<float>(-1e29);
+  while (static_cast<double>(f) > -1e29) f = std::nextafter(f, -INFINITY);
+  while (static_cast<double>(std::nextafter(f, INFINITY)) <= -1e29)
+    f = std::nextafter(f, INFINITY);
+  return f;
+}
+
+int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
+                bl_results** out) {
+  validate_cfg(d->cfg);  // batched.cpp:97
+  auto res = std::make_unique<bl_results>();
+  if (n == 0) {  // batched.cpp:99
+    *out = res.release();
+    return BL_OK;
+  }
+  const int C = d->num_tokens, V = C + 1, B = d->cfg.beam_width;
+  for (int i = 0; i < n; ++i) {  // batched.cpp:105-111
+    const std::string id = utts[i].id ? utts[i].id : "";
+    if (utts[i].num_frames < 1)
+      throw std::invalid_argument("empty grid in utterance " + id);
+    if ((int)utts[i].vocab - 1 != C)
+      throw std::invalid_argument("scorer vocabulary mismatch in utterance " + id);
+  }
+  if (bl::bmax_for(B) == 0)
+    throw std::invalid_argument("beam width > 32 is not supported by the device decoder");
+  CK(cudaSetDevice(d->device));
+
+  int Tmax = 0, S = 0;
+  std::vector<bl::UttDesc> desc(n);
+  std::vector<size_t> goff(n);
+  size_t gtotal = 0;
+  for (int i = 0; i < n; ++i) {
+    const int T = (int)utts[i].num_frames;
+    Tmax = std::max(Tmax, T);
+    desc[i].T = T;
+    desc[i].max_steps = static_cast<int>(std::ceil(d->cfg.max_steps_ratio * T));
+    S = std::max(S, desc[i].max_steps);
+    desc[i].need_tail = d->cfg.margin_m2 < T ? 1 : 0;
+    goff[i] = gtotal;
+    gtotal += ((size_t)T * V + 31) & ~(size_t)31;  // 128-B aligned starts
+  }
+  const int Tp = (Tmax + 2) & ~1;
+  const int caps = std::min(2 * B + 16, bl::kNT);
+  const int nbest = std::max(1, d->nbest);
+  const int rs = bl::res_stride(S, nbest);
+  const int U = n;
+
+  bool tail = false;
+  for (auto& x : desc) tail |= x.need_tail != 0;
+
+  // workspace
+  d->gam.ensure(sizeof(double) * (size_t)U * 2 * caps * 2 * Tp);
+  d->Gtab.ensure(sizeof(double) * (size_t)U * Tp);
+  d->Ftab.ensure(tail ? sizeof(double) * (size_t)U * Tp * C : 8);
+  d->keys.ensure(sizeof(float2) * (size_t)U * B * C);
+  d->xs.ensure(sizeof(double) * (size_t)U * B * (C + 1));
+  d->taken.ensure((size_t)U * B * (C + 1));
+  d->hist.ensure(sizeof(bl::HistRec) * (size_t)U * (S + 1) * B);
+  d->fin.ensure(sizeof(bl::FinEntry) * (size_t)U * B * S);
+  d->res.ensure(sizeof(int) * (size_t)U * rs);
+  d->cnt.ensure(sizeof(unsigned long long) * (size_t)U * 8);
+  d->utts.ensure(sizeof(bl::UttDesc) * U);
+  d->h_utts.ensure(sizeof(bl::UttDesc) * U);
+  d->h_res.ensure(sizeof(int) * (size_t)U * rs);
+  d->h_cnt.ensure(sizeof(unsigned long long) * (size_t)U * 8);
+
+  cudaStream_t st = d->stream;
+  if (!on_device) {
+    d->grid.ensure(sizeof(float) * gtotal);
+    d->h_grid.ensure(sizeof(float) * gtotal);
+    float* hg = static_cast<float*>(d->h_grid.p);
+    for (int i = 0; i < n; ++i)
+      std::memcpy(hg + goff[i], utts[i].logp, sizeof(float) * (size_t)desc[i].T * V);
+  }
+
+  bl::KParams p{};
+  p.U = U;
+  p.V = V;
+  p.C = C;
+  p.B = B;
+  p.Tmax = Tmax;
+  p.Tp = Tp;
+  p.S = S;
+  p.caps = caps;
+  p.lambda = d->cfg.ctc_weight;
+  p.eos_dend = d->cfg.eos_dend;
+  p.eos_m = d->cfg.eos_m;
+  p.eos_c = d->cfg.eos_c;
+  p.m1 = d->cfg.margin_m1;
+  p.m2 = d->cfg.margin_m2;
+  p.eos_mode = d->cfg.eos_mode;
+  p.guard_f = guard_float();
+  p.exact = d->exact;
+  p.nbest = nbest;
+  p.dpsi0 = 5e-4 * d->slack;
+  p.dpsi1 = 1e-6 * d->slack;
+  p.sc_order = d->sc_order;
+  p.sc_nent = d->sc_nent;
+  p.sc_w = d->sc_w;
+  p.sc_ctx_len = static_cast<const int*>(d->sc_ctx_len.p);
+  p.sc_ctx = static_cast<const int*>(d->sc_ctx.p);
+  p.sc_row = static_cast<const int*>(d->sc_row.p);
+  p.sc_rows = static_cast<const double*>(d->sc_rows.p);
+  p.gam = static_cast<double*>(d->gam.p);
+  p.Ftab = static_cast<double*>(d->Ftab.p);
+  p.Gtab = static_cast<double*>(d->Gtab.p);
+  p.keys = static_cast<float2*>(d->keys.p);
+  p.xs = static_cast<double*>(d->xs.p);
+  p.taken = static_cast<unsigned char*>(d->taken.p);
+  p.hist = static_cast<bl::HistRec*>(d->hist.p);
+  p.fin = static_cast<bl::FinEntry*>(d->fin.p);
+  p.res = static_cast<int*>(d->res.p);
+  p.res_stride = rs;
+  p.cnt = static_cast<unsigned long long*>(d->cnt.p);
+  p.utts = static_cast<const bl::UttDesc*>(d->utts.p);
+
+  for (int i = 0; i < n; ++i)
+    desc[i].grid = on_device ? utts[i].logp
+                             : static_cast<const float*>(d->grid.p) + goff[i];
+  std::memcpy(d->h_utts.p, desc.data(), sizeof(bl::UttDesc) * U);
+  if (bl::decode_smem_bytes(p) > 227 * 1024)
+    throw std::invalid_argument("utterance too long for the device decoder's shared memory plan");
+
+  if (!on_device)
+    CK(cudaMemcpyAsync(d->grid.p, d->h_grid.p, sizeof(float) * gtotal,
+                       cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d->utts.p, d->h_utts.p, sizeof(bl::UttDesc) * U,
+                     cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(d->ev0, st));
+  CK(bl::launch_decode(p, st));
+  CK(cudaEventRecord(d->ev1, st));
+  CK(cudaMemcpyAsync(d->h_res.p, d->res.p, sizeof(int) * (size_t)U * rs,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(d->h_cnt.p, d->cnt.p, sizeof(unsigned long long) * (size_t)U * 8,
+                     cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
+  res->kernel_ms = ms;
+  res->launches = 1;
+
+  const int* hr = static_cast<const int*>(d->h_res.p);
+  const unsigned long long* hc = static_cast<const unsigned long long*>(d->h_cnt.p);
+  res->r.resize(n);
+  for (int i = 0; i < n; ++i) {
+    const int* r = hr + (size_t)i * rs;
+    auto& o = res->r[i];
+    o.id = utts[i].id ? utts[i].id : "";
+    const int nt = r[0];
+    o.steps = r[1];
+    o.trigger = r[2];
+    std::memcpy(&o.joint, r + 4, sizeof(double));
+    o.tokens.assign(r + bl::kResHdr, r + bl::kResHdr + nt);
+    o.label_times.assign(r + bl::kResHdr + S, r + bl::kResHdr + S + nt);
+    const int nn = r[3];
+    for (int k = 0; k < nn; ++k) {
+      const int* q = r + bl::kResHdr + 2 * S + k * (4 + 2 * S);
+      double jv;
+      std::memcpy(&jv, q + 2, sizeof(double));
+      o.nb_joint.push_back(jv);
+      o.nb_tokens.emplace_back(q + 4, q + 4 + q[0]);
+      o.nb_times.emplace_back(q + 4 + S, q + 4 + S + q[0]);
+    }
+    const unsigned long long* c = hc + (size_t)i * 8;
+    res->steps += c[0];
+    res->queries += c[1];
+    res->frames += c[2];
+    res->k1 += c[3];
+    res->fallback += c[4];
+    res->contenders += c[5];
+  }
+  *out = res.release();
+  return BL_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C ABI
+extern "C" {
+
+const char* bl_last_error(void) { return g_err.c_str(); }
+
+void bl_config_default(bl_config* c) {  // beam_search.hpp:21-33
+  c->beam_width = 3;
+  c->ctc_weight = 0.3;
+  c->eos_m = 3;
+  c->eos_dend = -10.0;
+  c->eos_c = 2;
+  c->margin_m1 = 5;
+  c->margin_m2 = BL_NO_MARGIN;
+  c->eos_mode = BL_EOS_BOTH;
+  c->max_steps_ratio = 1.0;
+}
+
+int bl_config_validate(const bl_config* c) {
+  return guarded([&] {
+    validate_cfg(*c);
+    return BL_OK;
+  });
+}
+
+// hard_segments / split_uniform (segmentation.cpp:65-75, 121-133)
+int bl_hard_segments(int T, int min_len, int max_len, int* starts, int* ends,
+                     int cap, int* n_out) {
+  return guarded([&] {
+    if (T < 1) throw std::invalid_argument("hard_segments: T < 1");
+    if (!(min_len > 0 && min_len <= max_len))
+      throw std::invalid_argument("hard_segments: need 0 < min_len <= max_len");
+    int n = 0;
+    auto emit = [&](int s, int e) {
+      if (n < cap) {
+        starts[n] = s;
+        ends[n] = e;
+      }
+      ++n;
+    };
+    if (T < min_len) {
+      emit(0, T);
+    } else {
+      const int len = T;
+      const int pieces = (len + max_len - 1) / max_len;
+      int offset = 0;
+      for (int k = 0; k < pieces; ++k) {
+        const int piece = len / pieces + (k < len % pieces ? 1 : 0);
+        emit(offset, offset + piece);
+        offset += piece;
+      }
+    }
+    *n_out = n;
+    return BL_OK;
+  });
+}
+
+// make_batches (batched.cpp:12-30)
+int bl_make_batches(int n, const uint32_t* frames, int batch_size, int* order,
+                    int* n_batches) {
+  return guarded([&] {
+    if (batch_size < 1) throw std::invalid_argument("batch size must be >= 1");
+    std::vector<int> idx(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    std::stable_sort(idx.begin(), idx.end(),
+                     [&](int a, int b) { return frames[a] < frames[b]; });
+    for (int i = 0; i < n; ++i) order[i] = idx[i];
+    *n_batches = (n + batch_size - 1) / batch_size;
+    return BL_OK;
+  });
+}
+
+// make_scorer (scorer.cpp:117-135)
+int bl_scorer_create(const char* spec_c, int num_tokens, bl_scorer** out) {
+  return guarded([&] {
+    const std::string spec(spec_c ? spec_c : "");
+    if (spec == "uniform") {
+      if (num_tokens < 1) throw std::invalid_argument("UniformScorer: |C| < 1");
+      auto* s = new bl_scorer;
+      s->num_tokens = num_tokens;
+      *out = s;
+      return BL_OK;
+    }
+    if (spec.rfind("table:", 0) == 0) {
+      std::unique_ptr<bl_scorer> s(load_table(spec.substr(6)));
+      if (s->num_tokens != num_tokens)
+        throw std::runtime_error("table scorer vocabulary does not match grids");
+      *out = s.release();
+      return BL_OK;
+    }
+    if (spec.rfind("loop:", 0) == 0) {
+      std::string rest = spec.substr(5);
+      auto colon = rest.find(':');
+      if (colon == std::string::npos)
+        throw std::runtime_error("loop scorer spec must be loop:TOKEN:P");
+      int token = std::stoi(rest.substr(0, colon));
+      double p = std::stod(rest.substr(colon + 1));
+      *out = make_loop(num_tokens, token, p);
+      return BL_OK;
+    }
+    throw std::runtime_error("unknown scorer spec: " + spec);
+  });
+}
+
+int bl_scorer_create_table(int num_tokens, int order, int n_entries,
+                           const int* ctx_len, const int* ctx, const double* logp,
+                           bl_scorer** out) {
+  return guarded([&] {
+    std::unique_ptr<bl_scorer> s(make_table(num_tokens, order));
+    const int w = std::max(order - 1, 1);
+    for (int k = 0; k < n_entries; ++k) {  // TableScorer::add_entry
+      std::vector<double> lp(logp + (size_t)k * (num_tokens + 1),
+                             logp + (size_t)(k + 1) * (num_tokens + 1));
+      check_normalized(lp, static_cast<size_t>(num_tokens) + 1, "TableScorer entry");
+      s->table[std::vector<int>(ctx + (size_t)k * w, ctx + (size_t)k * w + ctx_len[k])] =
+          std::move(lp);
+    }
+    *out = s.release();
+    return BL_OK;
+  });
+}
+
+int bl_scorer_create_loop(int num_tokens, int loop_token, double p, bl_scorer** out) {
+  return guarded([&] {
+    *out = make_loop(num_tokens, loop_token, p);
+    return BL_OK;
+  });
+}
+
+int bl_scorer_num_tokens(const bl_scorer* s) { return s ? s->num_tokens : -1; }
+
+int bl_scorer_score(const bl_scorer* s, const int* prefix, int n, double* out) {
+  return guarded([&] {
+    auto v = s->score(std::vector<int>(prefix, prefix + n));
+    std::copy(v.begin(), v.end(), out);
+    return BL_OK;
+  });
+}
+
+void bl_scorer_destroy(bl_scorer* s) { delete s; }
+
+int bl_decoder_create(int device, const bl_config* cfg, const bl_scorer* scorer,
+                      bl_decoder** out) {
+  return guarded([&] {
+    validate_cfg(*cfg);
+    if (!scorer) throw std::invalid_argument("scorer is required");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+      throw BlError{BL_CUDA_ERROR, "no CUDA device " + std::to_string(device)};
+    CK(cudaSetDevice(device));
+    std::unique_ptr<bl_decoder> d(new bl_decoder);
+    d->device = device;
+    d->cfg = *cfg;
+    d->num_tokens = scorer->num_tokens;
+    CK(cudaStreamCreateWithFlags(&d->own, cudaStreamNonBlocking));
+    d->stream = d->own;
+    CK(cudaEventCreate(&d->ev0));
+    CK(cudaEventCreate(&d->ev1));
+    upload_scorer(d.get(), scorer);
+    *out = d.release();
+    return BL_OK;
+  });
+}
+
+int bl_decoder_set_options(bl_decoder* d, int nbest, int exact, double slack) {
+  return guarded([&] {
+    if (nbest < 1) throw std::invalid_argument("nbest must be >= 1");
+    if (!(slack >= 1.0)) throw std::invalid_argument("slack must be >= 1");
+    d->nbest = nbest;
+    d->exact = exact ? 1 : 0;
+    d->slack = slack;
+    return BL_OK;
+  });
+}
+
+int bl_decoder_set_stream(bl_decoder* d, void* stream) {
+  d->stream = stream ? static_cast<cudaStream_t>(stream) : d->own;
+  return BL_OK;
+}
+
+void bl_decoder_destroy(bl_decoder* d) {
+  if (!d) return;
+  cudaSetDevice(d->device);
+  cudaStreamSynchronize(d->stream);
+  if (d->ev0) cudaEventDestroy(d->ev0);
+  if (d->ev1) cudaEventDestroy(d->ev1);
+  if (d->own) cudaStreamDestroy(d->own);
+  delete d;
+}
+
+int bl_decode(bl_decoder* d, int n, const bl_utt* utts, int on_device,
+              bl_results** out) {
+  return guarded([&] { return decode_impl(d, n, utts, on_device, out); });
+}
+
+int bl_results_count(const bl_results* r) { return (int)r->r.size(); }
+
+int bl_results_get(const bl_results* r, int i, const char** id, const int** tokens,
+                   int* n_tokens, double* joint, const int** label_times, int* steps,
+                   int* trigger) {
+  if (i < 0 || i >= (int)r->r.size()) return fail(BL_INVALID_ARGUMENT, "result index out of range");
+  const auto& o = r->r[i];
+  if (id) *id = o.id.c_str();
+  if (tokens) *tokens = o.tokens.data();
+  if (n_tokens) *n_tokens = (int)o.tokens.size();
+  if (joint) *joint = o.joint;
+  if (label_times) *label_times = o.label_times.data();
+  if (steps) *steps = o.steps;
+  if (trigger) *trigger = o.trigger;
+  return BL_OK;
+}
+
+int bl_results_nbest_count(const bl_results* r, int i) {
+  if (i < 0 || i >= (int)r->r.size()) return 0;
+  return (int)r->r[i].nb_joint.size();
+}
+
+int bl_results_nbest(const bl_results* r, int i, int k, const int** tokens,
+                     int* n_tokens, double* joint, const int** label_times) {
+  if (i < 0 || i >= (int)r->r.size() || k < 0 || k >= (int)r->r[i].nb_joint.size())
+    return fail(BL_INVALID_ARGUMENT, "n-best index out of range");
+  const auto& o = r->r[i];
+  if (tokens) *tokens = o.nb_tokens[k].data();
+  if (n_tokens) *n_tokens = (int)o.nb_tokens[k].size();
+  if (joint) *joint = o.nb_joint[k];
+  if (label_times) *label_times = o.nb_times[k].data();
+  return BL_OK;
+}
+
+int bl_results_counters(const bl_results* r, uint64_t* steps, uint64_t* q, uint64_t* f) {
+  if (steps) *steps = r->steps;
+  if (q) *q = r->queries;
+  if (f) *f = r->frames;
+  return BL_OK;
+}
+
+int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1,
+                     int* launches, uint64_t* fallback, uint64_t* contenders) {
+  if (kernel_ms) *kernel_ms = r->kernel_ms;
+  if (k1) *k1 = r->k1;
+  if (launches) *launches = r->launches;
+  if (fallback) *fallback = r->fallback;
+  if (contenders) *contenders = r->contenders;
+  return BL_OK;
+}
+
+void bl_results_destroy(bl_results* r) { delete r; }
+
+}  // extern "C"

@@ -1,0 +1,1000 @@
+// decode_kernel.cu — persistent sm_100a decoder: one CTA per utterance runs
+// the whole label-synchronous joint CTC/attention beam search (Alg. 2 of
+// arXiv 2101.05600 as implemented by beamlattice batched_beam_search,
+// /root/reference/proj/src/batched.cpp:94-237) with every step on device:
+//
+//   P1  windows + per-utterance envelope       ctc_prefix.cpp:106-125, batched.cpp:129-135
+//       eos candidates (exact fp64)            ctc_prefix.cpp:88-104 via precomputed tail tables
+//   P2  phi_j[t] = gb[t-1] (+) gn[t-1]  (fp64)  ctc_prefix.cpp:50-51
+//   P3  K1 bulk prefix score, all (j, c):       ctc_prefix.cpp:47-59 (psi term)
+//       psi ~= M_j + m_c + log sum_t exp(phi_j-M_j) exp(L[t,c]-m_c)  (fp32 FMA,
+//       certified half-width) -> joint keys     beam_search.cpp:60-66, logmath.hpp:34-39
+//   P4  B-th largest certified lower bound (theta)
+//   P5  contenders = candidates whose upper bound reaches theta (+ repeats)
+//   P6  contenders re-scored by the reference-order fp64 recursion, which
+//       also yields their child state (gamma_n', gamma_b', tau, tau~)
+//   P7  exact total order (score desc, parent asc, token asc) incl. eos
+//                                               batched.cpp:172-186
+//   P8  walk: finished entries / children       batched.cpp:188-212
+//   P9  end detection                           batched.cpp:215-228
+//   fin finalize + n-best                       batched.cpp:70-90
+//
+// If the contender set overflows (degenerate ties) or exact mode is on, the
+// step falls back to fp64 scores for every candidate and an exact block
+// arg-max selection — slower, same results.
+#include <cfloat>
+#include <climits>
+
+#include "decode.cuh"
+
+namespace bl {
+
+// ---------------------------------------------------------------- logmath
+__device__ __forceinline__ bool is_zero(double x) { return x <= kLogZeroGuard; }
+
+// logmath.hpp:19-23
+__device__ __forceinline__ double log_add(double a, double b) {
+  if (a < b) {
+    double t = a;
+    a = b;
+    b = t;
+  }
+  if (is_zero(b)) return is_zero(a) ? kLogZero : a;
+  return a + log1p(exp(b - a));
+}
+
+// logmath.hpp:26-29
+__device__ __forceinline__ double log_mul(double a, double b) {
+  if (is_zero(a) || is_zero(b)) return kLogZero;
+  return __dadd_rn(a, b);
+}
+
+// logmath.hpp:34-39 (no FMA contraction: same rounding as the host)
+__device__ __forceinline__ double mix_joint(double lam, double ctc, double att) {
+  if (lam <= 0.0) return att;
+  if (lam >= 1.0) return ctc;
+  if (is_zero(ctc) || is_zero(att)) return kLogZero;
+  return __dadd_rn(__dmul_rn(lam, ctc), __dmul_rn(__dsub_rn(1.0, lam), att));
+}
+
+// candidate order, batched.cpp:181-186 (eos carries token id |C|)
+__device__ __forceinline__ bool before(double sa, int pa, int ta, double sb,
+                                       int pb, int tb) {
+  if (sa != sb) return sa > sb;
+  if (pa != pb) return pa < pb;
+  return ta < tb;
+}
+
+// window_for, ctc_prefix.cpp:106-114
+__device__ __forceinline__ void window_for(int tau, int taut, int m1, int m2,
+                                           int step, int T, int* s, int* e) {
+  long long ss = (long long)tau - m1;
+  if ((long long)step > ss) ss = step;
+  if (ss < 1) ss = 1;
+  long long ee = (long long)taut + m2;
+  if ((long long)T < ee) ee = T;
+  if (ss > ee) ss = ee;
+  *s = (int)ss;
+  *e = (int)ee;
+}
+
+__device__ __forceinline__ double gread(const double* a, int i, int vlo, int cov) {
+  return (i < vlo || i > cov) ? kLogZero : a[i];
+}
+
+__device__ __forceinline__ double warp_max_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max_f(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+struct SelE {
+  double score;
+  int parent, token, slot, tau, taut, pad;
+};
+
+struct Cand {
+  double score;
+  int parent, token, tau, taut;
+};
+
+template <int BMAX>
+struct Shared {
+  int b_area[2][BMAX], b_slot[2][BMAX], b_vlo[2][BMAX], b_cov[2][BMAX];
+  int b_tau[2][BMAX], b_taut[2][BMAX], b_last[2][BMAX], b_row[2][BMAX];
+  double b_att[2][BMAX], b_joint[2][BMAX];
+  double M[BMAX];
+  double eosj[BMAX];
+  float wl[kNWarp][BMAX];
+  SelE sel[2 * BMAX + 2];
+  double red_s[kNWarp];
+  int red_p[kNWarp], red_t[kNWarp];
+  int s, e, W, nb, n_cont, nsel, nchild, n_fin, n_fin_new, count_long, best_fin;
+  int done, trigger, steps, fallback;
+  double best_all, best_fin_val, off;
+  float theta;
+  unsigned long long c_queries, c_frames, c_k1, c_fallback, c_cont, c_steps;
+};
+
+__device__ __forceinline__ double* gam_ptr(const KParams& P, int u, int area,
+                                           int slot, int which) {
+  return P.gam + ((((size_t)u * 2 + area) * P.caps + slot) * 2 + which) * (size_t)P.Tp;
+}
+
+// TableScorer::score context lookup (scorer.cpp:53-62): the last
+// min(len, order-1) tokens of the prefix; entries are sorted by
+// (length, tokens) on the host. Row 0 is the uniform fallback.
+__device__ int lookup_row(const KParams& P, const HistRec* hist_u, int len,
+                          int parent_step, int parent_slot, int c) {
+  if (P.sc_nent == 0) return 0;
+  int n = len < P.sc_order - 1 ? len : P.sc_order - 1;
+  int ctx[8];
+  if (n > 0) {
+    ctx[n - 1] = c;
+    int k = parent_slot;
+    for (int i = n - 2, st = parent_step; i >= 0; --i, --st) {
+      HistRec h = hist_u[(size_t)st * P.B + k];
+      ctx[i] = h.token;
+      k = h.parent;
+    }
+  }
+  int lo = 0, hi = P.sc_nent - 1;
+  while (lo <= hi) {
+    int mid = (lo + hi) >> 1;
+    int ml = P.sc_ctx_len[mid];
+    int cmp = 0;
+    if (ml != n) {
+      cmp = ml < n ? -1 : 1;
+    } else {
+      const int* mc = P.sc_ctx + (size_t)mid * P.sc_w;
+      for (int i = 0; i < n; ++i)
+        if (mc[i] != ctx[i]) {
+          cmp = mc[i] < ctx[i] ? -1 : 1;
+          break;
+        }
+    }
+    if (cmp == 0) return P.sc_row[mid];
+    if (cmp < 0) lo = mid + 1;
+    else hi = mid - 1;
+  }
+  return 0;
+}
+
+// Reference-order child recursion (ctc_prefix.cpp:47-77) for parent j,
+// token c over [s, e]; writes the child's gamma arrays (entries inside
+// [s, e]) and returns psi, tau, tau~.
+template <int BMAX>
+__device__ double child_recursion(const KParams& P, const Shared<BMAX>& sh,
+                                  int u, int cur, int j, int c, int s, int e,
+                                  const float* __restrict__ grid,
+                                  const double* phi, double* gnc, double* gbc,
+                                  int* tau_out, int* taut_out, bool write) {
+  const int V = P.V, blank = P.V - 1;
+  const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
+  const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
+  const bool repeat = sh.b_last[cur][j] == c;
+  const int lo = sh.b_tau[cur][j] > 1 ? sh.b_tau[cur][j] : 1;
+  int best_n = lo, best_b = lo;
+  double val_n = kLogZero, val_b = kLogZero;
+  double gn_prev = kLogZero, gb_prev = kLogZero, psi = kLogZero;
+  for (int t = s; t <= e; ++t) {
+    const double ph = repeat ? gread(gbp, t - 1, vlo, cov) : phi[t - s];
+    const float* row = grid + (size_t)(t - 1) * V;
+    const double pc = (double)row[c];
+    const double pbl = (double)row[blank];
+    const double gn = log_mul(log_add(gn_prev, ph), pc);
+    const double gb = log_mul(log_add(gb_prev, gn_prev), pbl);
+    psi = log_add(psi, log_mul(ph, pc));
+    if (write) {
+      gnc[t] = gn;
+      gbc[t] = gb;
+    }
+    if (t >= lo) {
+      if (gn > val_n) {
+        val_n = gn;
+        best_n = t;
+      }
+      if (gb > val_b) {
+        val_b = gb;
+        best_b = t;
+      }
+    }
+    gn_prev = gn;
+    gb_prev = gb;
+  }
+  *tau_out = best_n;
+  *taut_out = best_b;
+  return psi;
+}
+
+// psi only (fallback path), same order as the reference.
+template <int BMAX>
+__device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
+                           int cur, int j, int c, int s, int e,
+                           const float* __restrict__ grid, const double* phi) {
+  const int V = P.V;
+  const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
+  const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
+  const bool repeat = sh.b_last[cur][j] == c;
+  double psi = kLogZero;
+  for (int t = s; t <= e; ++t) {
+    const double ph = repeat ? gread(gbp, t - 1, vlo, cov) : phi[t - s];
+    psi = log_add(psi, log_mul(ph, (double)grid[(size_t)(t - 1) * V + c]));
+  }
+  return psi;
+}
+
+template <int BMAX>
+__global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  __shared__ Shared<BMAX> sh;
+
+  const int u = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const UttDesc ud = P.utts[u];
+  const float* __restrict__ grid = ud.grid;
+  const int T = ud.T, V = P.V, C = P.C, B = P.B, blank = P.V - 1;
+  const double lam = P.lambda;
+
+  // dynamic smem carve-up
+  double* phi = reinterpret_cast<double*>(dsm);                      // [BMAX][Tmax]
+  float* PhiF = reinterpret_cast<float*>(phi + (size_t)BMAX * P.Tmax); // [Tmax][BMAX]
+  Cand* cand = reinterpret_cast<Cand*>(PhiF + (size_t)P.Tmax * BMAX);  // [kNT]
+  double* best_by_len = reinterpret_cast<double*>(cand + kNT);         // [S+2]
+
+  const HistRec* hist_c = P.hist + (size_t)u * (P.S + 1) * B;
+  HistRec* hist_u = P.hist + (size_t)u * (P.S + 1) * B;
+  FinEntry* fin_u = P.fin + (size_t)u * B * P.S;
+  float2* keys_u = P.keys + (size_t)u * B * C;
+  double* Ft = P.Ftab + (size_t)u * P.Tp * C;
+  double* Gt = P.Gtab + (size_t)u * P.Tp;
+
+  // ---------------------------------------------------------------- init
+  for (int i = tid; i <= P.S + 1; i += kNT) best_by_len[i] = -HUGE_VAL;
+  {
+    double* gn0 = gam_ptr(P, u, 0, 0, 0);
+    for (int t = tid; t <= T; t += kNT) gn0[t] = kLogZero;
+  }
+  if (tid == 0) {
+    // init_state, ctc_prefix.cpp:10-26 (sequential: exact reference order)
+    double* gb0 = gam_ptr(P, u, 0, 0, 1);
+    double acc = 0.0;
+    gb0[0] = acc;
+    for (int t = 1; t <= T; ++t) {
+      acc = log_mul(acc, (double)grid[(size_t)(t - 1) * V + blank]);
+      gb0[t] = acc;
+    }
+    if (ud.need_tail) {  // G[k] = blank mass of frames k+1..T
+      double g = 0.0;
+      Gt[T] = g;
+      for (int k = T - 1; k >= 0; --k) {
+        g = log_mul((double)grid[(size_t)k * V + blank], g);
+        Gt[k] = g;
+      }
+    }
+    sh.nb = 1;
+    sh.b_area[0][0] = 0;
+    sh.b_slot[0][0] = 0;
+    sh.b_vlo[0][0] = 0;
+    sh.b_cov[0][0] = T;
+    sh.b_tau[0][0] = 1;
+    sh.b_taut[0][0] = 1;
+    sh.b_last[0][0] = -1;
+    sh.b_att[0][0] = 0.0;
+    sh.b_joint[0][0] = 0.0;
+    sh.n_fin = 0;
+    sh.count_long = 0;
+    sh.best_fin = -1;
+    sh.best_fin_val = 0.0;
+    sh.best_all = -HUGE_VAL;
+    sh.done = 0;
+    sh.trigger = 2;
+    sh.steps = 0;
+    sh.c_queries = sh.c_frames = sh.c_k1 = sh.c_fallback = sh.c_cont = sh.c_steps = 0;
+    sh.b_row[0][0] = lookup_row(P, hist_c, 0, 0, 0, 0);
+  }
+  __syncthreads();
+  if (ud.need_tail) {
+    // F[k][c]: label c held from frame k to some k' then blank to T
+    // (the eos tail of ctc_prefix.cpp:88-104 in closed form).
+    for (int c = tid; c < C; c += kNT) {
+      double f = 0.0;
+      Ft[(size_t)T * C + c] = f;
+      for (int k = T - 1; k >= 0; --k) {
+        f = log_add(log_mul((double)grid[(size_t)k * V + c], f), Gt[k]);
+        Ft[(size_t)k * C + c] = f;
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---------------------------------------------------------- step loop
+  for (int l = 1;; ++l) {
+    const int cur = (l - 1) & 1, nxt = l & 1;
+    if (l > ud.max_steps) break;  // batched.cpp:125-128
+    const int nb = sh.nb;
+
+    // ---- P1: windows, eos candidates, offsets (warp 0) ----
+    if (warp == 0) {
+      const int j = lane;
+      int ws = INT_MAX, we = INT_MIN;
+      double jm = -HUGE_VAL;
+      unsigned long long tail = 0;
+      if (j < nb) {
+        window_for(sh.b_tau[cur][j], sh.b_taut[cur][j], P.m1, P.m2, l, T, &ws, &we);
+        const int cov = sh.b_cov[cur][j];
+        const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
+        const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
+        double ee;
+        if (cov >= T) {
+          ee = log_add(gnp[T], gbp[T]);
+        } else {
+          const int last = sh.b_last[cur][j];
+          const double fl = last >= 0 ? Ft[(size_t)cov * C + last] : Gt[cov];
+          ee = log_add(log_mul(gnp[cov], fl), log_mul(gbp[cov], Gt[cov]));
+          tail = (unsigned long long)(T - cov);
+        }
+        const double* row = P.sc_rows + (size_t)sh.b_row[cur][j] * V;
+        sh.eosj[j] = mix_joint(lam, ee, __dadd_rn(sh.b_att[cur][j], row[C]));
+        jm = sh.b_joint[cur][j];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        ws = min(ws, __shfl_xor_sync(0xffffffffu, ws, o));
+        we = max(we, __shfl_xor_sync(0xffffffffu, we, o));
+        tail += __shfl_xor_sync(0xffffffffu, tail, o);
+      }
+      jm = warp_max_d(jm);
+      if (lane == 0) {
+        sh.s = ws;
+        sh.e = we;
+        const int W = we - ws + 1;
+        sh.W = W;
+        sh.off = is_zero(jm) ? 0.0 : jm;
+        sh.c_queries += nb;
+        sh.c_frames += (unsigned long long)nb * C * W + tail;
+        sh.c_k1 += 4ull * V * W + 16ull * nb * (W + 1) + 4ull * nb * V;
+        sh.n_cont = 0;
+        sh.fallback = P.exact;
+      }
+    }
+    __syncthreads();
+    const int s = sh.s, e = sh.e, W = sh.W;
+
+    // ---- P2: phi_j[t] (fp64, reference log_add) and the fp32 factors ----
+    for (int idx = tid; idx < nb * W; idx += kNT) {
+      const int j = idx / W, i = idx - j * W, t = s + i;
+      const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
+      const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
+      const double* gbp = gnp + P.Tp;
+      phi[(size_t)j * P.Tmax + i] =
+          log_add(gread(gbp, t - 1, vlo, cov), gread(gnp, t - 1, vlo, cov));
+    }
+    __syncthreads();
+
+    if (!P.exact) {
+      for (int j = warp; j < nb; j += kNWarp) {
+        double m = -HUGE_VAL;
+        for (int i = lane; i < W; i += 32) {
+          const double v = phi[(size_t)j * P.Tmax + i];
+          if (!is_zero(v) && v > m) m = v;
+        }
+        m = warp_max_d(m);
+        if (lane == 0) sh.M[j] = (m == -HUGE_VAL) ? kLogZero : m;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < W * BMAX; idx += kNT) {
+        const int i = idx / BMAX, j = idx - i * BMAX;
+        float v = 0.f;
+        if (j < nb) {
+          const double Mj = sh.M[j];
+          const double p = phi[(size_t)j * P.Tmax + i];
+          if (!is_zero(Mj) && !is_zero(p)) v = __expf((float)(p - Mj));
+        }
+        PhiF[(size_t)i * BMAX + j] = v;
+      }
+      __syncthreads();
+
+      // ---- P3: K1 bulk prefix score + certified joint keys ----
+      float list[BMAX];
+#pragma unroll
+      for (int q = 0; q < BMAX; ++q) list[q] = -INFINITY;
+      const double dpsi = P.dpsi0 + W * P.dpsi1;
+      const double off = sh.off;
+      const float gf = P.guard_f;
+      for (int c = tid; c < C; c += kNT) {
+        float S[BMAX];
+#pragma unroll
+        for (int q = 0; q < BMAX; ++q) S[q] = 0.f;
+        float m = -INFINITY;
+        const float* col = grid + (size_t)(s - 1) * V + c;
+        int i = 0;
+        for (; i + 4 <= W; i += 4) {
+          float xv[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) xv[k] = __ldg(col + (size_t)(i + k) * V);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float x = xv[k];
+            if (x > gf) {
+              if (x > m + 8.f) {
+                const float r = __expf(m - x);
+#pragma unroll
+                for (int q = 0; q < BMAX; ++q) S[q] *= r;
+                m = x;
+              }
+              const float p = __expf(x - m);
+              const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)(i + k) * BMAX);
+#pragma unroll
+              for (int q = 0; q < BMAX / 4; ++q) {
+                const float4 f = ph[q];
+                S[4 * q + 0] = fmaf(f.x, p, S[4 * q + 0]);
+                S[4 * q + 1] = fmaf(f.y, p, S[4 * q + 1]);
+                S[4 * q + 2] = fmaf(f.z, p, S[4 * q + 2]);
+                S[4 * q + 3] = fmaf(f.w, p, S[4 * q + 3]);
+              }
+            }
+          }
+        }
+        for (; i < W; ++i) {
+          const float x = __ldg(col + (size_t)i * V);
+          if (x > gf) {
+            if (x > m + 8.f) {
+              const float r = __expf(m - x);
+#pragma unroll
+              for (int q = 0; q < BMAX; ++q) S[q] *= r;
+              m = x;
+            }
+            const float p = __expf(x - m);
+            const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)i * BMAX);
+#pragma unroll
+            for (int q = 0; q < BMAX / 4; ++q) {
+              const float4 f = ph[q];
+              S[4 * q + 0] = fmaf(f.x, p, S[4 * q + 0]);
+              S[4 * q + 1] = fmaf(f.y, p, S[4 * q + 1]);
+              S[4 * q + 2] = fmaf(f.z, p, S[4 * q + 2]);
+              S[4 * q + 3] = fmaf(f.w, p, S[4 * q + 3]);
+            }
+          }
+        }
+        // certified (lo, ub) of joint(j, c) relative to `off`
+#pragma unroll
+        for (int q = 0; q < BMAX; ++q) {
+          if (q >= nb) break;
+          float klo = -INFINITY, kub = -INFINITY;
+          if (c != sh.b_last[cur][q]) {
+            const double att = __dadd_rn(sh.b_att[cur][q],
+                                         P.sc_rows[(size_t)sh.b_row[cur][q] * V + c]);
+            double lo, ub;
+            if (lam <= 0.0) {
+              lo = ub = att;
+            } else {
+              double plo, pub;
+              const double Mj = sh.M[q];
+              if (is_zero(Mj) || m == -INFINITY) {
+                plo = pub = kLogZero;  // exact: no admissible term
+              } else if (S[q] >= 7.888609052210118e-31f) {  // 2^-100
+                const double ps = Mj + (double)m + (double)logf(S[q]);
+                plo = ps - dpsi;
+                pub = ps + dpsi;
+              } else {  // underflow: certified upper bound only
+                plo = -HUGE_VAL;
+                pub = Mj + (double)m - 68.62157411784526;  // log 2^-99
+              }
+              if (lam >= 1.0) {
+                lo = plo;
+                ub = pub;
+              } else if (is_zero(att)) {
+                lo = ub = kLogZero;
+              } else {
+                lo = (plo == -HUGE_VAL) ? -HUGE_VAL : mix_joint(lam, plo, att);
+                ub = mix_joint(lam, pub, att);
+              }
+            }
+            klo = (lo == -HUGE_VAL) ? -INFINITY : __double2float_rd(lo - off);
+            kub = __double2float_ru(ub - off);
+            // insert klo into the sorted top list
+            float v = klo;
+#pragma unroll
+            for (int r = 0; r < BMAX; ++r) {
+              if (v > list[r]) {
+                const float t2 = list[r];
+                list[r] = v;
+                v = t2;
+              }
+            }
+          }
+          keys_u[(size_t)q * C + c] = make_float2(klo, kub);
+        }
+      }
+
+      // ---- P4: theta = B-th largest certified lower bound ----
+      for (int r = 0; r < B; ++r) {
+        const float h = list[0];
+        const float mx = warp_max_f(h);
+        const unsigned who = __ballot_sync(0xffffffffu, h == mx);
+        if (lane == __ffs(who) - 1) {
+#pragma unroll
+          for (int q = 0; q < BMAX - 1; ++q) list[q] = list[q + 1];
+          list[BMAX - 1] = -INFINITY;
+        }
+        if (lane == 0) sh.wl[warp][r] = mx;
+      }
+      __syncthreads();
+      if (warp == 0) {
+#pragma unroll
+        for (int q = 0; q < BMAX; ++q)
+          list[q] = (lane < kNWarp && q < B) ? sh.wl[lane][q] : -INFINITY;
+        float th = -INFINITY;
+        for (int r = 0; r < B; ++r) {
+          const float h = list[0];
+          const float mx = warp_max_f(h);
+          const unsigned who = __ballot_sync(0xffffffffu, h == mx);
+          if (lane == __ffs(who) - 1) {
+#pragma unroll
+            for (int q = 0; q < BMAX - 1; ++q) list[q] = list[q + 1];
+            list[BMAX - 1] = -INFINITY;
+          }
+          th = mx;
+        }
+        if (lane == 0) sh.theta = th;
+      }
+      __syncthreads();
+
+      // ---- P5: contenders ----
+      const float theta = sh.theta;
+      for (int c = tid; c < C; c += kNT) {
+        for (int q = 0; q < nb; ++q) {
+          if (c == sh.b_last[cur][q]) continue;
+          const float2 k = keys_u[(size_t)q * C + c];
+          if (k.y >= theta) {
+            const int idx = atomicAdd(&sh.n_cont, 1);
+            if (idx < kNT) {
+              cand[idx].parent = q;
+              cand[idx].token = c;
+            }
+          }
+        }
+      }
+      if (warp == 0 && lane < nb && sh.b_last[cur][lane] >= 0) {
+        const int idx = atomicAdd(&sh.n_cont, 1);  // repeat column: always exact
+        if (idx < kNT) {
+          cand[idx].parent = lane;
+          cand[idx].token = sh.b_last[cur][lane];
+        }
+      }
+      __syncthreads();
+      if (tid == 0) {
+        sh.c_cont += sh.n_cont;
+        if (sh.n_cont > P.caps || sh.n_cont + nb > kNT) sh.fallback = 1;
+      }
+      __syncthreads();
+    }
+
+    if (!sh.fallback) {
+      // ---- P6: exact re-scoring of contenders, with their child states ----
+      const int nc = sh.n_cont;
+      if (tid < nc) {
+        const int j = cand[tid].parent, c = cand[tid].token;
+        double* gnc = gam_ptr(P, u, nxt, tid, 0);
+        double* gbc = gnc + P.Tp;
+        int tau, taut;
+        const double psi = child_recursion<BMAX>(P, sh, u, cur, j, c, s, e, grid,
+                                                 phi + (size_t)j * P.Tmax, gnc, gbc,
+                                                 &tau, &taut, true);
+        const double att = __dadd_rn(sh.b_att[cur][j],
+                                     P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+        cand[tid].score = mix_joint(lam, psi, att);
+        cand[tid].tau = tau;
+        cand[tid].taut = taut;
+      }
+      __syncthreads();
+      // ---- P7: exact order over contenders + eos (rank sort) ----
+      const int ni = nc + nb;
+      if (tid < ni) {
+        double ms;
+        int mp, mt;
+        if (tid < nc) {
+          ms = cand[tid].score;
+          mp = cand[tid].parent;
+          mt = cand[tid].token;
+        } else {
+          ms = sh.eosj[tid - nc];
+          mp = tid - nc;
+          mt = C;
+        }
+        int rank = 0;
+        for (int q = 0; q < ni; ++q) {
+          double qs;
+          int qp, qt;
+          if (q < nc) {
+            qs = cand[q].score;
+            qp = cand[q].parent;
+            qt = cand[q].token;
+          } else {
+            qs = sh.eosj[q - nc];
+            qp = q - nc;
+            qt = C;
+          }
+          rank += before(qs, qp, qt, ms, mp, mt) ? 1 : 0;
+        }
+        if (rank < B + nb) {
+          SelE x;
+          x.score = ms;
+          x.parent = mp;
+          x.token = mt;
+          x.slot = tid < nc ? tid : -1;
+          x.tau = tid < nc ? cand[tid].tau : 0;
+          x.taut = tid < nc ? cand[tid].taut : 0;
+          sh.sel[rank] = x;
+        }
+      }
+      if (tid == 0) sh.nsel = min(ni, B + nb);
+      __syncthreads();
+    } else {
+      // ---- fallback: fp64 scores for every candidate + exact selection ----
+      double* xs = P.xs + (size_t)u * B * (C + 1);
+      unsigned char* taken = P.taken + (size_t)u * B * (C + 1);
+      const int total = nb * (C + 1);
+      for (int idx = tid; idx < total; idx += kNT) {
+        const int j = idx / (C + 1), c = idx - j * (C + 1);
+        double sc;
+        if (c == C) {
+          sc = sh.eosj[j];
+        } else {
+          const double att = __dadd_rn(sh.b_att[cur][j],
+                                       P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+          const double psi = lam <= 0.0 ? kLogZero
+                                        : psi_only<BMAX>(P, sh, u, cur, j, c, s, e, grid,
+                                                         phi + (size_t)j * P.Tmax);
+          sc = mix_joint(lam, psi, att);
+        }
+        xs[idx] = sc;
+        taken[idx] = 0;
+      }
+      if (tid == 0) {
+        sh.nsel = 0;
+        sh.c_fallback += 1;
+      }
+      __syncthreads();
+      int non_eos = 0;
+      for (int r = 0; r < total && non_eos < B; ++r) {
+        double bs = 0.0;
+        int bp = INT_MAX, bt = INT_MAX;
+        for (int idx = tid; idx < total; idx += kNT) {
+          if (taken[idx]) continue;
+          const int j = idx / (C + 1), c = idx - j * (C + 1);
+          if (bp == INT_MAX || before(xs[idx], j, c, bs, bp, bt)) {
+            bs = xs[idx];
+            bp = j;
+            bt = c;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+          const int op = __shfl_xor_sync(0xffffffffu, bp, o);
+          const int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+          if (op != INT_MAX && (bp == INT_MAX || before(os, op, ot, bs, bp, bt))) {
+            bs = os;
+            bp = op;
+            bt = ot;
+          }
+        }
+        if (lane == 0) {
+          sh.red_s[warp] = bs;
+          sh.red_p[warp] = bp;
+          sh.red_t[warp] = bt;
+        }
+        __syncthreads();
+        if (tid == 0) {
+          double ws2 = sh.red_s[0];
+          int wp = sh.red_p[0], wt = sh.red_t[0];
+          for (int w = 1; w < kNWarp; ++w)
+            if (sh.red_p[w] != INT_MAX &&
+                (wp == INT_MAX || before(sh.red_s[w], sh.red_p[w], sh.red_t[w], ws2, wp, wt))) {
+              ws2 = sh.red_s[w];
+              wp = sh.red_p[w];
+              wt = sh.red_t[w];
+            }
+          SelE x;
+          x.score = ws2;
+          x.parent = wp;
+          x.token = wt;
+          x.slot = -1;
+          x.tau = x.taut = 0;
+          sh.sel[sh.nsel++] = x;
+          taken[(size_t)wp * (C + 1) + wt] = 1;
+        }
+        __syncthreads();
+        non_eos += (sh.sel[sh.nsel - 1].token < C) ? 1 : 0;
+      }
+    }
+
+    // ---- P8: walk (parallel): finished entries and children ----
+    const int nsel = sh.nsel;
+    if (tid < nsel) {
+      const SelE x = sh.sel[tid];
+      int non_eos_before = 0, eos_before = 0;
+      for (int q = 0; q < tid; ++q) {
+        if (sh.sel[q].token < C) ++non_eos_before;
+        else ++eos_before;
+      }
+      if (non_eos_before < B) {
+        const int j = x.parent;
+        if (x.token == C) {
+          FinEntry f;
+          f.joint = x.score;
+          f.tau_last = sh.b_tau[cur][j];
+          f.length = l;
+          f.bp_step = l - 1;
+          f.bp_slot = j;
+          fin_u[sh.n_fin + eos_before] = f;
+        } else {
+          const int k = non_eos_before;
+          const int c = x.token;
+          sh.b_area[nxt][k] = nxt;
+          sh.b_slot[nxt][k] = x.slot >= 0 ? x.slot : k;
+          sh.b_vlo[nxt][k] = s;
+          sh.b_cov[nxt][k] = e;
+          sh.b_tau[nxt][k] = x.tau;
+          sh.b_taut[nxt][k] = x.taut;
+          sh.b_last[nxt][k] = c;
+          sh.b_att[nxt][k] = __dadd_rn(sh.b_att[cur][j],
+                                       P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+          sh.b_joint[nxt][k] = x.score;
+          sh.b_row[nxt][k] = lookup_row(P, hist_c, l, l - 1, j, c);
+          HistRec h;
+          h.token = c;
+          h.parent = j;
+          h.tau = x.tau;
+          h.pad = 0;
+          hist_u[(size_t)l * B + k] = h;
+        }
+      }
+    }
+    if (tid == 0) {
+      int ne = 0, ee2 = 0;
+      for (int q = 0; q < nsel; ++q) {
+        if (ne >= B) break;
+        if (sh.sel[q].token < C) ++ne;
+        else ++ee2;
+      }
+      sh.nchild = ne;
+      sh.n_fin_new = ee2;
+    }
+    __syncthreads();
+    if (sh.fallback && tid < sh.nchild) {
+      // children states for the fallback path (slot k of area nxt)
+      int k = tid, cnt = 0, q = 0;
+      for (; q < nsel; ++q) {
+        if (sh.sel[q].token < C) {
+          if (cnt == k) break;
+          ++cnt;
+        }
+      }
+      const SelE x = sh.sel[q];
+      double* gnc = gam_ptr(P, u, nxt, k, 0);
+      double* gbc = gnc + P.Tp;
+      int tau, taut;
+      child_recursion<BMAX>(P, sh, u, cur, x.parent, x.token, s, e, grid,
+                            phi + (size_t)x.parent * P.Tmax, gnc, gbc, &tau, &taut,
+                            true);
+      sh.b_tau[nxt][k] = tau;
+      sh.b_taut[nxt][k] = taut;
+      hist_u[(size_t)l * B + k].tau = tau;
+    }
+
+    // ---- P9: end detection (batched.cpp:215-228) ----
+    if (tid == 0) {
+      const int n0 = sh.n_fin, nn = sh.n_fin_new;
+      for (int q = n0; q < n0 + nn; ++q) {
+        const FinEntry f = fin_u[q];
+        if (f.joint > best_by_len[l]) best_by_len[l] = f.joint;
+        if (f.joint > sh.best_all) sh.best_all = f.joint;
+        if (f.tau_last == T) ++sh.count_long;
+        if (sh.best_fin < 0 || f.joint > sh.best_fin_val) {
+          sh.best_fin = q;
+          sh.best_fin_val = f.joint;
+        }
+      }
+      sh.n_fin = n0 + nn;
+      sh.steps = l;
+      sh.c_steps += 1;
+      bool stop = false;
+      if (P.eos_mode != 1 && sh.n_fin > 0) {  // end_detect_baseline
+        bool ok = true;
+        for (int m = 0; m < P.eos_m; ++m) {
+          const int len = l - m;
+          const double lb = len >= 1 ? best_by_len[len] : -HUGE_VAL;
+          if (lb == -HUGE_VAL || !(lb - sh.best_all < P.eos_dend)) {
+            ok = false;
+            break;
+          }
+        }
+        if (ok) {
+          sh.trigger = 0;
+          stop = true;
+        }
+      }
+      if (!stop && P.eos_mode != 0 && sh.count_long > P.eos_c) {
+        sh.trigger = 1;
+        stop = true;
+      }
+      if (sh.nchild == 0) stop = true;
+      sh.nb = sh.nchild;
+      sh.done = stop ? 1 : 0;
+    }
+    __syncthreads();
+    if (sh.done) break;
+  }
+
+  // ------------------------------------------------------------ finalize
+  // batched.cpp:70-90: first max (strict >) over finished entries in
+  // insertion order, else over the live beam with trigger = max_len.
+  const int fcur = sh.steps & 1;  // beam after the last processed step
+  int* res = P.res + (size_t)u * P.res_stride;
+  const int S = P.S;
+  if (tid == 0) {
+    int bp_step, bp_slot, trig = sh.trigger;
+    double joint;
+    if (sh.n_fin > 0) {
+      const FinEntry f = fin_u[sh.best_fin];
+      bp_step = f.bp_step;
+      bp_slot = f.bp_slot;
+      joint = f.joint;
+    } else {
+      int best = 0;
+      for (int k = 1; k < sh.nb; ++k)
+        if (sh.b_joint[fcur][k] > sh.b_joint[fcur][best]) best = k;
+      bp_step = sh.steps;
+      bp_slot = best;
+      joint = sh.b_joint[fcur][best];
+      trig = 2;
+    }
+    res[0] = bp_step;
+    res[1] = sh.steps;
+    res[2] = trig;
+    res[3] = 0;
+    reinterpret_cast<double*>(res + 4)[0] = joint;
+    res[6] = sh.n_fin;
+    res[7] = 0;
+    int k = bp_slot;
+    for (int st = bp_step; st >= 1; --st) {
+      const HistRec h = hist_c[(size_t)st * B + k];
+      res[kResHdr + st - 1] = h.token;
+      res[kResHdr + S + st - 1] = h.tau;
+      k = h.parent;
+    }
+    unsigned long long* cn = P.cnt + (size_t)u * 8;
+    cn[0] = sh.c_steps;
+    cn[1] = sh.c_queries;
+    cn[2] = sh.c_frames;
+    cn[3] = sh.c_k1;
+    cn[4] = sh.c_fallback;
+    cn[5] = sh.c_cont;
+    cn[6] = 0;
+    cn[7] = 0;
+  }
+  // n-best over finished entries: (joint desc, insertion asc)
+  if (P.nbest > 0 && sh.n_fin > 0) {
+    unsigned char* taken = P.taken + (size_t)u * B * (C + 1);  // reuse (>= B*S? no)
+    (void)taken;
+    const int nf = sh.n_fin;
+    const int want = min(P.nbest, nf);
+    double last_s = HUGE_VAL;
+    int last_i = -1;
+    for (int r = 0; r < want; ++r) {
+      // next entry strictly after (last_s, last_i) in the order
+      double bs = -HUGE_VAL;
+      int bi = INT_MAX;
+      for (int q = tid; q < nf; q += kNT) {
+        const double js = fin_u[q].joint;
+        const bool after_last = (js < last_s) || (js == last_s && q > last_i);
+        if (!after_last) continue;
+        if (bi == INT_MAX || js > bs || (js == bs && q < bi)) {
+          bs = js;
+          bi = q;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_xor_sync(0xffffffffu, bs, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oi != INT_MAX && (bi == INT_MAX || os > bs || (os == bs && oi < bi))) {
+          bs = os;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        sh.red_s[warp] = bs;
+        sh.red_p[warp] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double ws2 = sh.red_s[0];
+        int wi = sh.red_p[0];
+        for (int w = 1; w < kNWarp; ++w) {
+          const int oi = sh.red_p[w];
+          const double os = sh.red_s[w];
+          if (oi != INT_MAX && (wi == INT_MAX || os > ws2 || (os == ws2 && oi < wi))) {
+            ws2 = os;
+            wi = oi;
+          }
+        }
+        const FinEntry f = fin_u[wi];
+        int* nb_rec = res + kResHdr + 2 * S + r * (4 + 2 * S);
+        nb_rec[0] = f.bp_step;
+        nb_rec[1] = wi;
+        reinterpret_cast<double*>(nb_rec + 2)[0] = f.joint;
+        int k = f.bp_slot;
+        for (int st = f.bp_step; st >= 1; --st) {
+          const HistRec h = hist_c[(size_t)st * B + k];
+          nb_rec[4 + st - 1] = h.token;
+          nb_rec[4 + S + st - 1] = h.tau;
+          k = h.parent;
+        }
+        res[3] = r + 1;
+        sh.red_s[0] = ws2;
+        sh.red_p[0] = wi;
+      }
+      __syncthreads();
+      last_s = sh.red_s[0];
+      last_i = sh.red_p[0];
+      __syncthreads();
+    }
+  }
+}
+
+// ------------------------------------------------------------ launchers
+template <int BMAX>
+static size_t smem_bytes(const KParams& p) {
+  return sizeof(double) * (size_t)BMAX * p.Tmax + sizeof(float) * (size_t)p.Tmax * BMAX +
+         sizeof(Cand) * kNT + sizeof(double) * (size_t)(p.S + 2);
+}
+
+template <int BMAX>
+static cudaError_t launch_t(const KParams& p, cudaStream_t st) {
+  const size_t sm = smem_bytes<BMAX>(p);
+  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+  if (err != cudaSuccess) return err;
+  decode_kernel<BMAX><<<p.U, kNT, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
+int bmax_for(int B) {
+  if (B <= 4) return 4;
+  if (B <= 8) return 8;
+  if (B <= 16) return 16;
+  if (B <= 32) return 32;
+  return 0;
+}
+
+size_t decode_smem_bytes(const KParams& p) {
+  switch (bmax_for(p.B)) {
+    case 4: return smem_bytes<4>(p);
+    case 8: return smem_bytes<8>(p);
+    case 16: return smem_bytes<16>(p);
+    case 32: return smem_bytes<32>(p);
+  }
+  return 0;
+}
+
+cudaError_t launch_decode(const KParams& p, cudaStream_t st) {
+  switch (bmax_for(p.B)) {
+    case 4: return launch_t<4>(p, st);
+    case 8: return launch_t<8>(p, st);
+    case 16: return launch_t<16>(p, st);
+    case 32: return launch_t<32>(p, st);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace bl
