@@ -94,6 +94,7 @@ def lib() -> C.CDLL:
     u64p = C.POINTER(C.c_uint64)
     L.bl_results_counters.argtypes = [vp, u64p, u64p, u64p]
     L.bl_results_stats.argtypes = [vp, dp, u64p, ip, u64p, u64p]
+    L.bl_results_profile.argtypes = [vp, dp]
     L.bl_results_destroy.argtypes = [vp]
     _lib = L
     return L
@@ -454,6 +455,10 @@ class Decoder:
                            "launches": nl.value, "fallback_steps": fb.value,
                            "contenders": nc.value, "steps": s.value,
                            "scorer_queries": q.value, "ctc_frames_evaluated": f.value}
+        if os.environ.get("BL_PROFILE"):
+            prof = (C.c_double * 16)()
+            L.bl_results_profile(h, prof)
+            self.last_stats["profile_cycles"] = [round(x) for x in prof]
         return out
 
 

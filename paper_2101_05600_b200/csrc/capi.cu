@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <map>
@@ -212,10 +213,11 @@ struct bl_decoder {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // device scorer
   int sc_order = 1, sc_nent = 0, sc_w = 1;
-  DevBuf sc_ctx_len, sc_ctx, sc_row, sc_rows;
+  DevBuf sc_ctx_len, sc_ctx, sc_row, sc_rows, sc_rowsf;
   // workspace
-  DevBuf grid, utts, gam, Ftab, Gtab, keys, xs, taken, hist, fin, res, cnt;
-  HostBuf h_grid, h_utts, h_res, h_cnt;
+  DevBuf grid, utts, gam, Ftab, Gtab, kubg, xs, taken, hist, fin, res, cnt, prof;
+  HostBuf h_grid, h_utts, h_res, h_cnt, h_prof;
+  bool profile = getenv("BL_PROFILE") != nullptr;
 };
 
 struct bl_results {
@@ -231,6 +233,7 @@ struct bl_results {
   uint64_t steps = 0, queries = 0, frames = 0, k1 = 0, fallback = 0, contenders = 0;
   double kernel_ms = 0.0;
   int launches = 0;
+  double prof[16] = {0};  // mean cycles per utterance per phase
 };
 
 namespace {
@@ -278,6 +281,16 @@ void upload_scorer(bl_decoder* d, const bl_scorer* s) {
   d->sc_ctx.ensure(ctx.size() * sizeof(int));
   d->sc_row.ensure(row.size() * sizeof(int));
   d->sc_rows.ensure(rows.size() * sizeof(double));
+  // (1 - lambda) * row in fp32 for the certified bulk keys; -inf marks a
+  // log-zero attention entry (mix_joint then returns kLogZero exactly).
+  const double lam = d->cfg.ctc_weight;
+  std::vector<float> rowsf(rows.size());
+  for (size_t i = 0; i < rows.size(); ++i)
+    rowsf[i] = lam >= 1.0 ? 0.f
+               : rows[i] <= -1e29 ? -INFINITY
+                                  : (float)((lam <= 0.0 ? 1.0 : 1.0 - lam) * rows[i]);
+  d->sc_rowsf.ensure(rowsf.size() * sizeof(float));
+  CK(cudaMemcpy(d->sc_rowsf.p, rowsf.data(), rowsf.size() * sizeof(float), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d->sc_ctx_len.p, clen.data(), clen.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d->sc_ctx.p, ctx.data(), ctx.size() * sizeof(int), cudaMemcpyHostToDevice));
   CK(cudaMemcpy(d->sc_row.p, row.data(), row.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -354,7 +367,9 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   d->gam.ensure(sizeof(double) * (size_t)U * 2 * caps * 2 * Tp);
   d->Gtab.ensure(sizeof(double) * (size_t)U * Tp);
   d->Ftab.ensure(tail ? sizeof(double) * (size_t)U * Tp * C : 8);
-  d->keys.ensure(sizeof(float2) * (size_t)U * B * C);
+  const int bmax = bl::bmax_for(B);
+  int kub_smem = bl::smem_plan(Tmax, B, bmax, C, caps, S, 1).total <= 100 * 1024 ? 1 : 0;
+  if (!kub_smem) d->kubg.ensure(sizeof(float) * (size_t)U * B * C);
   d->xs.ensure(sizeof(double) * (size_t)U * B * (C + 1));
   d->taken.ensure((size_t)U * B * (C + 1));
   d->hist.ensure(sizeof(bl::HistRec) * (size_t)U * (S + 1) * B);
@@ -406,7 +421,9 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.gam = static_cast<double*>(d->gam.p);
   p.Ftab = static_cast<double*>(d->Ftab.p);
   p.Gtab = static_cast<double*>(d->Gtab.p);
-  p.keys = static_cast<float2*>(d->keys.p);
+  p.kubg = static_cast<float*>(d->kubg.p);
+  p.kub_smem = kub_smem;
+  p.sc_rowsf = static_cast<const float*>(d->sc_rowsf.p);
   p.xs = static_cast<double*>(d->xs.p);
   p.taken = static_cast<unsigned char*>(d->taken.p);
   p.hist = static_cast<bl::HistRec*>(d->hist.p);
@@ -415,6 +432,13 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.res_stride = rs;
   p.cnt = static_cast<unsigned long long*>(d->cnt.p);
   p.utts = static_cast<const bl::UttDesc*>(d->utts.p);
+  p.prof = nullptr;
+  if (d->profile) {
+    d->prof.ensure(sizeof(long long) * (size_t)U * 16);
+    d->h_prof.ensure(sizeof(long long) * (size_t)U * 16);
+    CK(cudaMemsetAsync(d->prof.p, 0, sizeof(long long) * (size_t)U * 16, st));
+    p.prof = static_cast<long long*>(d->prof.p);
+  }
 
   for (int i = 0; i < n; ++i)
     desc[i].grid = on_device ? utts[i].logp
@@ -435,7 +459,15 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
                      cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(d->h_cnt.p, d->cnt.p, sizeof(unsigned long long) * (size_t)U * 8,
                      cudaMemcpyDeviceToHost, st));
+  if (d->profile)
+    CK(cudaMemcpyAsync(d->h_prof.p, d->prof.p, sizeof(long long) * (size_t)U * 16,
+                       cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  if (d->profile) {
+    const long long* hp = static_cast<const long long*>(d->h_prof.p);
+    for (int i = 0; i < U; ++i)
+      for (int k = 0; k < 16; ++k) res->prof[k] += (double)hp[(size_t)i * 16 + k] / U;
+  }
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
   res->kernel_ms = ms;
@@ -720,6 +752,11 @@ int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1,
   if (launches) *launches = r->launches;
   if (fallback) *fallback = r->fallback;
   if (contenders) *contenders = r->contenders;
+  return BL_OK;
+}
+
+int bl_results_profile(const bl_results* r, double* out16) {
+  for (int k = 0; k < 16; ++k) out16[k] = r->prof[k];
   return BL_OK;
 }
 

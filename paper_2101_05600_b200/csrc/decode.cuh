@@ -62,11 +62,13 @@ struct KParams {
   const int* sc_ctx;
   const int* sc_row;     // row of entry k
   const double* sc_rows; // [rows][V]; row 0 = uniform fallback
+  const float* sc_rowsf;  // [rows][V]: (float)((1-lambda)*row), -inf where row is log-zero
   // workspace (per-utterance slices)
   double* gam;     // [U][2][caps][2][Tp]
   double* Ftab;    // [U][Tp][C]   eos tail tables (need_tail only)
   double* Gtab;    // [U][Tp]
-  float2* keys;    // [U][B][C]    certified (lo, ub) joint keys
+  float* kubg;     // [U][B][C]    certified upper keys when they do not fit in smem
+  int kub_smem;    // 1: upper keys live in shared memory
   double* xs;      // [U][B][C+1]  exact joints (fallback path)
   unsigned char* taken;  // [U][B][C+1]
   HistRec* hist;   // [U][S+1][B]
@@ -74,7 +76,34 @@ struct KParams {
   int* res;        // [U][res_stride]
   int res_stride;
   unsigned long long* cnt;  // [U][8]
+  long long* prof;          // [U][16] phase cycles, or nullptr
 };
+
+// Dynamic shared-memory plan (identical on host and device).
+struct SmemPlan {
+  size_t phi, phir, region, items, bbl, total;
+  size_t phif, kub;  // P3 view of `region`
+  size_t stl, stb;   // P6 view of `region`
+};
+constexpr int kItemBytes = 24;  // score(double) + parent, token, tau, taut
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C,
+                                              int caps, int S, int kub_smem) {
+  SmemPlan p;
+  p.phi = 0;
+  p.phir = align16(p.phi + sizeof(double) * (size_t)B * Tmax);
+  p.region = align16(p.phir + sizeof(double) * (size_t)B * Tmax);
+  p.phif = 0;
+  p.kub = align16(sizeof(float) * (size_t)Tmax * bmax);
+  const size_t a = p.kub + (kub_smem ? sizeof(float) * (size_t)B * C : 0);
+  p.stl = 0;
+  p.stb = align16(sizeof(float) * (size_t)caps * Tmax);
+  const size_t b = p.stb + sizeof(float) * (size_t)Tmax;
+  p.items = align16(p.region + (a > b ? a : b));
+  p.bbl = align16(p.items + (size_t)kItemBytes * (kNT + bmax));
+  p.total = align16(p.bbl + sizeof(double) * (size_t)(S + 2));
+  return p;
+}
 
 // Result record layout (ints) per utterance.
 constexpr int kResHdr = 8;

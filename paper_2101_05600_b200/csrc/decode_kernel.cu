@@ -7,12 +7,13 @@
 //       eos candidates (exact fp64)            ctc_prefix.cpp:88-104 via precomputed tail tables
 //   P2  phi_j[t] = gb[t-1] (+) gn[t-1]  (fp64)  ctc_prefix.cpp:50-51
 //   P3  K1 bulk prefix score, all (j, c):       ctc_prefix.cpp:47-59 (psi term)
-//       psi ~= M_j + m_c + log sum_t exp(phi_j-M_j) exp(L[t,c]-m_c)  (fp32 FMA,
-//       certified half-width) -> joint keys     beam_search.cpp:60-66, logmath.hpp:34-39
-//   P4  B-th largest certified lower bound (theta)
+//       psi ~= M_j + m_c + log sum_t exp(phi_j-M_j) exp(L[t,c]-m_c)  (fp32 FMA)
+//       -> certified fp32 joint keys            beam_search.cpp:60-66, logmath.hpp:34-39
+//   P4  theta = B-th largest certified lower bound
 //   P5  contenders = candidates whose upper bound reaches theta (+ repeats)
-//   P6  contenders re-scored by the reference-order fp64 recursion, which
-//       also yields their child state (gamma_n', gamma_b', tau, tau~)
+//   P6  contenders re-scored by the reference-order fp64 recursion from
+//       shared-memory staged inputs; it also yields their child state
+//       (gamma_n', gamma_b', tau, tau~)
 //   P7  exact total order (score desc, parent asc, token asc) incl. eos
 //                                               batched.cpp:172-186
 //   P8  walk: finished entries / children       batched.cpp:188-212
@@ -26,21 +27,20 @@
 #include <climits>
 
 #include "decode.cuh"
+#include "softplus.cuh"
 
 namespace bl {
 
 // ---------------------------------------------------------------- logmath
 __device__ __forceinline__ bool is_zero(double x) { return x <= kLogZeroGuard; }
 
-// logmath.hpp:19-23
-__device__ __forceinline__ double log_add(double a, double b) {
-  if (a < b) {
-    double t = a;
-    a = b;
-    b = t;
-  }
-  if (is_zero(b)) return is_zero(a) ? kLogZero : a;
-  return a + log1p(exp(b - a));
+__constant__ SpTables c_sptab = {SP_THI_INIT, SP_TLO_INIT, SP_INV_INIT, SP_LH_INIT,
+                                 SP_LL_INIT};
+
+// logmath.hpp:19-23 — branch-free table-driven version (softplus.cuh); the
+// tables live in shared memory (`tb`).
+__device__ __forceinline__ double log_add(double a, double b, const SpTables& tb) {
+  return log_add_fast(a, b, tb);
 }
 
 // logmath.hpp:26-29
@@ -93,15 +93,18 @@ __device__ __forceinline__ float warp_max_f(float v) {
   return v;
 }
 
+constexpr float kZeroKey = -3.0e38f;  // key of a joint that is exactly kLogZero
+
 struct SelE {
   double score;
   int parent, token, slot, tau, taut, pad;
 };
 
-struct Cand {
+struct Item {  // contender or eos candidate (kItemBytes)
   double score;
   int parent, token, tau, taut;
 };
+static_assert(sizeof(Item) == kItemBytes, "Item layout");
 
 template <int BMAX>
 struct Shared {
@@ -109,7 +112,8 @@ struct Shared {
   int b_tau[2][BMAX], b_taut[2][BMAX], b_last[2][BMAX], b_row[2][BMAX];
   double b_att[2][BMAX], b_joint[2][BMAX];
   double M[BMAX];
-  double eosj[BMAX];
+  float kb[BMAX];
+  int mzero[BMAX];
   float wl[kNWarp][BMAX];
   SelE sel[2 * BMAX + 2];
   double red_s[kNWarp];
@@ -165,15 +169,54 @@ __device__ int lookup_row(const KParams& P, const HistRec* hist_u, int len,
   return 0;
 }
 
-// Reference-order child recursion (ctc_prefix.cpp:47-77) for parent j,
-// token c over [s, e]; writes the child's gamma arrays (entries inside
-// [s, e]) and returns psi, tau, tau~.
+// Reference-order child recursion (ctc_prefix.cpp:47-77) over [s, s+W-1]
+// from shared-memory inputs: ph[i] = phi(t = s+i), lc[i] = L[t, c],
+// lb[i] = L[t, blank]. Writes gamma_n'/gamma_b' for t in the window and
+// returns psi, tau, tau~ (tau scan from lo = max(1, tau_parent)).
+__device__ double child_recursion_smem(const double* ph, const float* lc,
+                                       const float* lb, int s, int W, int tau_p,
+                                       double* gnc, double* gbc, int* tau_out,
+                                       int* taut_out, const SpTables& tb) {
+  const int lo = tau_p > 1 ? tau_p : 1;
+  int best_n = lo, best_b = lo;
+  double val_n = kLogZero, val_b = kLogZero;
+  double gn_prev = kLogZero, gb_prev = kLogZero, psi = kLogZero;
+  for (int i = 0; i < W; ++i) {
+    const int t = s + i;
+    const double phv = ph[i];
+    const double pc = (double)lc[i];
+    const double pbl = (double)lb[i];
+    const double gn = log_mul(log_add(gn_prev, phv, tb), pc);
+    const double gb = log_mul(log_add(gb_prev, gn_prev, tb), pbl);
+    psi = log_add(psi, log_mul(phv, pc), tb);
+    gnc[t] = gn;
+    gbc[t] = gb;
+    if (t >= lo) {
+      if (gn > val_n) {
+        val_n = gn;
+        best_n = t;
+      }
+      if (gb > val_b) {
+        val_b = gb;
+        best_b = t;
+      }
+    }
+    gn_prev = gn;
+    gb_prev = gb;
+  }
+  *tau_out = best_n;
+  *taut_out = best_b;
+  return psi;
+}
+
+// Same recursion reading the grid and the parent from global memory
+// (fallback path).
 template <int BMAX>
-__device__ double child_recursion(const KParams& P, const Shared<BMAX>& sh,
-                                  int u, int cur, int j, int c, int s, int e,
-                                  const float* __restrict__ grid,
-                                  const double* phi, double* gnc, double* gbc,
-                                  int* tau_out, int* taut_out, bool write) {
+__device__ double child_recursion_global(const KParams& P, const Shared<BMAX>& sh,
+                                       int u, int cur, int j, int c, int s, int e,
+                                       const float* __restrict__ grid,
+                                       const double* phi, double* gnc, double* gbc,
+                                       int* tau_out, int* taut_out, const SpTables& tb) {
   const int V = P.V, blank = P.V - 1;
   const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
   const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
@@ -186,14 +229,11 @@ __device__ double child_recursion(const KParams& P, const Shared<BMAX>& sh,
     const double ph = repeat ? gread(gbp, t - 1, vlo, cov) : phi[t - s];
     const float* row = grid + (size_t)(t - 1) * V;
     const double pc = (double)row[c];
-    const double pbl = (double)row[blank];
-    const double gn = log_mul(log_add(gn_prev, ph), pc);
-    const double gb = log_mul(log_add(gb_prev, gn_prev), pbl);
-    psi = log_add(psi, log_mul(ph, pc));
-    if (write) {
-      gnc[t] = gn;
-      gbc[t] = gb;
-    }
+    const double gn = log_mul(log_add(gn_prev, ph, tb), pc);
+    const double gb = log_mul(log_add(gb_prev, gn_prev, tb), (double)row[blank]);
+    psi = log_add(psi, log_mul(ph, pc), tb);
+    gnc[t] = gn;
+    gbc[t] = gb;
     if (t >= lo) {
       if (gn > val_n) {
         val_n = gn;
@@ -216,7 +256,8 @@ __device__ double child_recursion(const KParams& P, const Shared<BMAX>& sh,
 template <int BMAX>
 __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
                            int cur, int j, int c, int s, int e,
-                           const float* __restrict__ grid, const double* phi) {
+                           const float* __restrict__ grid, const double* phi,
+                           const SpTables& tb) {
   const int V = P.V;
   const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
   const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
@@ -224,15 +265,25 @@ __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
   double psi = kLogZero;
   for (int t = s; t <= e; ++t) {
     const double ph = repeat ? gread(gbp, t - 1, vlo, cov) : phi[t - s];
-    psi = log_add(psi, log_mul(ph, (double)grid[(size_t)(t - 1) * V + c]));
+    psi = log_add(psi, log_mul(ph, (double)grid[(size_t)(t - 1) * V + c]), tb);
   }
   return psi;
 }
+
+// Optional per-phase cycle accounting (P.prof != nullptr): thread 0 reads
+// clock64 right after each block barrier, so each delta is a phase's span.
+#define PROF_MARK(k)                                   \
+  if (P.prof && tid == 0) {                            \
+    const long long _now = clock64();                  \
+    P.prof[(size_t)u * 16 + (k)] += _now - prof_t;     \
+    prof_t = _now;                                     \
+  }
 
 template <int BMAX>
 __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Shared<BMAX> sh;
+  __shared__ SpTables tb;
 
   const int u = blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -240,21 +291,31 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
   const float* __restrict__ grid = ud.grid;
   const int T = ud.T, V = P.V, C = P.C, B = P.B, blank = P.V - 1;
   const double lam = P.lambda;
+  const float lamf = (float)lam;
+  long long prof_t = clock64();
 
-  // dynamic smem carve-up
-  double* phi = reinterpret_cast<double*>(dsm);                      // [BMAX][Tmax]
-  float* PhiF = reinterpret_cast<float*>(phi + (size_t)BMAX * P.Tmax); // [Tmax][BMAX]
-  Cand* cand = reinterpret_cast<Cand*>(PhiF + (size_t)P.Tmax * BMAX);  // [kNT]
-  double* best_by_len = reinterpret_cast<double*>(cand + kNT);         // [S+2]
+  // dynamic smem carve-up (smem_plan, decode.cuh)
+  const SmemPlan pl = smem_plan(P.Tmax, B, BMAX, C, P.caps, P.S, P.kub_smem);
+  double* phi = reinterpret_cast<double*>(dsm + pl.phi);    // [B][Tmax]
+  double* phir = reinterpret_cast<double*>(dsm + pl.phir);  // [B][Tmax]
+  float* PhiF = reinterpret_cast<float*>(dsm + pl.region + pl.phif);  // [Tmax][BMAX]
+  float* kub = P.kub_smem ? reinterpret_cast<float*>(dsm + pl.region + pl.kub)
+                          : P.kubg + (size_t)u * B * C;           // [B][C]
+  // P6 staging (aliases the P3 region)
+  float* stL = reinterpret_cast<float*>(dsm + pl.region + pl.stl);  // [caps][Tmax]
+  float* stB = reinterpret_cast<float*>(dsm + pl.region + pl.stb);  // [Tmax]
+  Item* items = reinterpret_cast<Item*>(dsm + pl.items);            // [kNT + BMAX]
+  double* best_by_len = reinterpret_cast<double*>(dsm + pl.bbl);    // [S+2]
 
   const HistRec* hist_c = P.hist + (size_t)u * (P.S + 1) * B;
   HistRec* hist_u = P.hist + (size_t)u * (P.S + 1) * B;
   FinEntry* fin_u = P.fin + (size_t)u * B * P.S;
-  float2* keys_u = P.keys + (size_t)u * B * C;
   double* Ft = P.Ftab + (size_t)u * P.Tp * C;
   double* Gt = P.Gtab + (size_t)u * P.Tp;
 
   // ---------------------------------------------------------------- init
+  for (int i = tid; i < 320; i += kNT)
+    reinterpret_cast<double*>(&tb)[i] = reinterpret_cast<const double*>(&c_sptab)[i];
   for (int i = tid; i <= P.S + 1; i += kNT) best_by_len[i] = -HUGE_VAL;
   {
     double* gn0 = gam_ptr(P, u, 0, 0, 0);
@@ -306,12 +367,13 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       double f = 0.0;
       Ft[(size_t)T * C + c] = f;
       for (int k = T - 1; k >= 0; --k) {
-        f = log_add(log_mul((double)grid[(size_t)k * V + c], f), Gt[k]);
+        f = log_add(log_mul((double)grid[(size_t)k * V + c], f), Gt[k], tb);
         Ft[(size_t)k * C + c] = f;
       }
     }
   }
   __syncthreads();
+  PROF_MARK(0);
 
   // ---------------------------------------------------------- step loop
   for (int l = 1;; ++l) {
@@ -329,18 +391,23 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         window_for(sh.b_tau[cur][j], sh.b_taut[cur][j], P.m1, P.m2, l, T, &ws, &we);
         const int cov = sh.b_cov[cur][j];
         const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
-        const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
+        const double* gbp = gnp + P.Tp;
         double ee;
         if (cov >= T) {
-          ee = log_add(gnp[T], gbp[T]);
+          ee = log_add(gnp[T], gbp[T], tb);
         } else {
           const int last = sh.b_last[cur][j];
           const double fl = last >= 0 ? Ft[(size_t)cov * C + last] : Gt[cov];
-          ee = log_add(log_mul(gnp[cov], fl), log_mul(gbp[cov], Gt[cov]));
+          ee = log_add(log_mul(gnp[cov], fl), log_mul(gbp[cov], Gt[cov]), tb);
           tail = (unsigned long long)(T - cov);
         }
         const double* row = P.sc_rows + (size_t)sh.b_row[cur][j] * V;
-        sh.eosj[j] = mix_joint(lam, ee, __dadd_rn(sh.b_att[cur][j], row[C]));
+        Item it;
+        it.score = mix_joint(lam, ee, __dadd_rn(sh.b_att[cur][j], row[C]));
+        it.parent = j;
+        it.token = C;
+        it.tau = it.taut = 0;
+        items[kNT + j] = it;  // eos candidates live past the contender slots
         jm = sh.b_joint[cur][j];
       }
 #pragma unroll
@@ -364,6 +431,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       }
     }
     __syncthreads();
+    PROF_MARK(1);
     const int s = sh.s, e = sh.e, W = sh.W;
 
     // ---- P2: phi_j[t] (fp64, reference log_add) and the fp32 factors ----
@@ -372,8 +440,9 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
       const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
       const double* gbp = gnp + P.Tp;
-      phi[(size_t)j * P.Tmax + i] =
-          log_add(gread(gbp, t - 1, vlo, cov), gread(gnp, t - 1, vlo, cov));
+      const double gb = gread(gbp, t - 1, vlo, cov);
+      phi[(size_t)j * P.Tmax + i] = log_add(gb, gread(gnp, t - 1, vlo, cov), tb);
+      phir[(size_t)j * P.Tmax + i] = gb;  // repeat column: ctc_prefix.cpp:50
     }
     __syncthreads();
 
@@ -385,7 +454,16 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
           if (!is_zero(v) && v > m) m = v;
         }
         m = warp_max_d(m);
-        if (lane == 0) sh.M[j] = (m == -HUGE_VAL) ? kLogZero : m;
+        if (lane == 0) {
+          const double Mj = (m == -HUGE_VAL) ? kLogZero : m;
+          sh.M[j] = Mj;
+          sh.mzero[j] = is_zero(Mj) ? 1 : 0;
+          // per-parent float base of the joint key, relative to `off`
+          const double base = (lam >= 1.0)   ? Mj
+                              : (lam <= 0.0) ? sh.b_att[cur][j]
+                                             : lam * Mj + (1.0 - lam) * sh.b_att[cur][j];
+          sh.kb[j] = (float)(base - sh.off);
+        }
       }
       __syncthreads();
       for (int idx = tid; idx < W * BMAX; idx += kNT) {
@@ -399,13 +477,13 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         PhiF[(size_t)i * BMAX + j] = v;
       }
       __syncthreads();
+      PROF_MARK(2);
 
-      // ---- P3: K1 bulk prefix score + certified joint keys ----
+      // ---- P3: K1 bulk prefix score + certified fp32 joint keys ----
       float list[BMAX];
 #pragma unroll
       for (int q = 0; q < BMAX; ++q) list[q] = -INFINITY;
-      const double dpsi = P.dpsi0 + W * P.dpsi1;
-      const double off = sh.off;
+      const float hw = (float)(lam * (P.dpsi0 + W * P.dpsi1)) + 1e-4f;
       const float gf = P.guard_f;
       for (int c = tid; c < C; c += kNT) {
         float S[BMAX];
@@ -413,13 +491,13 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         for (int q = 0; q < BMAX; ++q) S[q] = 0.f;
         float m = -INFINITY;
         const float* col = grid + (size_t)(s - 1) * V + c;
-        int i = 0;
-        for (; i + 4 <= W; i += 4) {
-          float xv[4];
+        for (int i0 = 0; i0 < W; i0 += 8) {
+          float xv[8];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) xv[k] = __ldg(col + (size_t)(i + k) * V);
+          for (int k = 0; k < 8; ++k)
+            xv[k] = (i0 + k < W) ? __ldg(col + (size_t)(i0 + k) * V) : -INFINITY;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < 8; ++k) {
             const float x = xv[k];
             if (x > gf) {
               if (x > m + 8.f) {
@@ -429,7 +507,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
                 m = x;
               }
               const float p = __expf(x - m);
-              const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)(i + k) * BMAX);
+              const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)(i0 + k) * BMAX);
 #pragma unroll
               for (int q = 0; q < BMAX / 4; ++q) {
                 const float4 f = ph[q];
@@ -441,75 +519,45 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
             }
           }
         }
-        for (; i < W; ++i) {
-          const float x = __ldg(col + (size_t)i * V);
-          if (x > gf) {
-            if (x > m + 8.f) {
-              const float r = __expf(m - x);
-#pragma unroll
-              for (int q = 0; q < BMAX; ++q) S[q] *= r;
-              m = x;
-            }
-            const float p = __expf(x - m);
-            const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)i * BMAX);
-#pragma unroll
-            for (int q = 0; q < BMAX / 4; ++q) {
-              const float4 f = ph[q];
-              S[4 * q + 0] = fmaf(f.x, p, S[4 * q + 0]);
-              S[4 * q + 1] = fmaf(f.y, p, S[4 * q + 1]);
-              S[4 * q + 2] = fmaf(f.z, p, S[4 * q + 2]);
-              S[4 * q + 3] = fmaf(f.w, p, S[4 * q + 3]);
-            }
-          }
-        }
-        // certified (lo, ub) of joint(j, c) relative to `off`
+        // certified keys: [key - hw', key + hw'] contains joint(j, c) - off
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) {
           if (q >= nb) break;
-          float klo = -INFINITY, kub = -INFINITY;
+          float klo = -INFINITY, kub_v = -INFINITY;
           if (c != sh.b_last[cur][q]) {
-            const double att = __dadd_rn(sh.b_att[cur][q],
-                                         P.sc_rows[(size_t)sh.b_row[cur][q] * V + c]);
-            double lo, ub;
-            if (lam <= 0.0) {
-              lo = ub = att;
-            } else {
-              double plo, pub;
-              const double Mj = sh.M[q];
-              if (is_zero(Mj) || m == -INFINITY) {
-                plo = pub = kLogZero;  // exact: no admissible term
-              } else if (S[q] >= 7.888609052210118e-31f) {  // 2^-100
-                const double ps = Mj + (double)m + (double)logf(S[q]);
-                plo = ps - dpsi;
-                pub = ps + dpsi;
-              } else {  // underflow: certified upper bound only
-                plo = -HUGE_VAL;
-                pub = Mj + (double)m - 68.62157411784526;  // log 2^-99
-              }
-              if (lam >= 1.0) {
-                lo = plo;
-                ub = pub;
-              } else if (is_zero(att)) {
-                lo = ub = kLogZero;
-              } else {
-                lo = (plo == -HUGE_VAL) ? -HUGE_VAL : mix_joint(lam, plo, att);
-                ub = mix_joint(lam, pub, att);
-              }
+            const float r = P.sc_rowsf[(size_t)sh.b_row[cur][q] * V + c];
+            if (r == -INFINITY) {
+              klo = kub_v = kZeroKey;  // att is log-zero: joint exactly kLogZero
+            } else if (lam <= 0.0) {
+              const float key = sh.kb[q] + r;
+              const float h = hw + fabsf(key) * 2.4e-7f;
+              klo = key - h;
+              kub_v = key + h;
+            } else if (sh.mzero[q] || m == -INFINITY) {
+              klo = kub_v = kZeroKey;  // psi exactly kLogZero
+            } else if (S[q] >= 7.888609052210118e-31f) {  // 2^-100
+              const float key = sh.kb[q] + lamf * (m + logf(S[q])) + r;
+              const float h = hw + fabsf(key) * 2.4e-7f;
+              klo = key - h;
+              kub_v = key + h;
+            } else {  // fp32 underflow: certified upper bound only
+              const float key = sh.kb[q] + lamf * (m - 68.62157f) + r;
+              klo = -INFINITY;
+              kub_v = key + hw + fabsf(key) * 2.4e-7f;
             }
-            klo = (lo == -HUGE_VAL) ? -INFINITY : __double2float_rd(lo - off);
-            kub = __double2float_ru(ub - off);
-            // insert klo into the sorted top list
-            float v = klo;
+            if (klo > list[BMAX - 1]) {
+              float v = klo;
 #pragma unroll
-            for (int r = 0; r < BMAX; ++r) {
-              if (v > list[r]) {
-                const float t2 = list[r];
-                list[r] = v;
-                v = t2;
+              for (int rr = 0; rr < BMAX; ++rr) {
+                if (v > list[rr]) {
+                  const float t2 = list[rr];
+                  list[rr] = v;
+                  v = t2;
+                }
               }
             }
           }
-          keys_u[(size_t)q * C + c] = make_float2(klo, kub);
+          kub[(size_t)q * C + c] = kub_v;
         }
       }
 
@@ -526,6 +574,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         if (lane == 0) sh.wl[warp][r] = mx;
       }
       __syncthreads();
+      PROF_MARK(3);
       if (warp == 0) {
 #pragma unroll
         for (int q = 0; q < BMAX; ++q)
@@ -545,97 +594,104 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         if (lane == 0) sh.theta = th;
       }
       __syncthreads();
+      PROF_MARK(4);
 
-      // ---- P5: contenders ----
+      // ---- P5: contenders (warp-aggregated appends) ----
       const float theta = sh.theta;
-      for (int c = tid; c < C; c += kNT) {
+      for (int c0 = 0; c0 < C; c0 += kNT) {
+        const int c = c0 + tid;
         for (int q = 0; q < nb; ++q) {
-          if (c == sh.b_last[cur][q]) continue;
-          const float2 k = keys_u[(size_t)q * C + c];
-          if (k.y >= theta) {
-            const int idx = atomicAdd(&sh.n_cont, 1);
-            if (idx < kNT) {
-              cand[idx].parent = q;
-              cand[idx].token = c;
+          const bool hit = c < C && c != sh.b_last[cur][q] && kub[(size_t)q * C + c] >= theta;
+          const unsigned mask = __ballot_sync(0xffffffffu, hit);
+          if (mask) {
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&sh.n_cont, __popc(mask));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (hit) {
+              const int idx = base + __popc(mask & ((1u << lane) - 1));
+              if (idx < kNT) {
+                items[idx].parent = q;
+                items[idx].token = c;
+              }
             }
           }
         }
       }
+      __syncthreads();
       if (warp == 0 && lane < nb && sh.b_last[cur][lane] >= 0) {
         const int idx = atomicAdd(&sh.n_cont, 1);  // repeat column: always exact
         if (idx < kNT) {
-          cand[idx].parent = lane;
-          cand[idx].token = sh.b_last[cur][lane];
+          items[idx].parent = lane;
+          items[idx].token = sh.b_last[cur][lane];
         }
       }
       __syncthreads();
       if (tid == 0) {
         sh.c_cont += sh.n_cont;
-        if (sh.n_cont > P.caps || sh.n_cont + nb > kNT) sh.fallback = 1;
+        if (sh.n_cont > P.caps) sh.fallback = 1;
       }
       __syncthreads();
+      PROF_MARK(5);
     }
 
     if (!sh.fallback) {
-      // ---- P6: exact re-scoring of contenders, with their child states ----
       const int nc = sh.n_cont;
+      // ---- P6a: stage the contenders' grid columns and the blank column ----
+      for (int idx = tid; idx < (nc + 1) * W; idx += kNT) {
+        const int q = idx / W, i = idx - q * W;
+        const int c = q < nc ? items[q].token : blank;
+        const float v = grid[(size_t)(s - 1 + i) * V + c];
+        if (q < nc) stL[(size_t)q * P.Tmax + i] = v;
+        else stB[i] = v;
+      }
+      __syncthreads();
+      // ---- P6: exact re-scoring of contenders, with their child states ----
+      // (reference op order, ctc_prefix.cpp:47-77; one thread per contender)
       if (tid < nc) {
-        const int j = cand[tid].parent, c = cand[tid].token;
+        const int j = items[tid].parent, c = items[tid].token;
+        const bool repeat = sh.b_last[cur][j] == c;
         double* gnc = gam_ptr(P, u, nxt, tid, 0);
         double* gbc = gnc + P.Tp;
         int tau, taut;
-        const double psi = child_recursion<BMAX>(P, sh, u, cur, j, c, s, e, grid,
-                                                 phi + (size_t)j * P.Tmax, gnc, gbc,
-                                                 &tau, &taut, true);
+        const double psi = child_recursion_smem(
+            (repeat ? phir : phi) + (size_t)j * P.Tmax, stL + (size_t)tid * P.Tmax, stB,
+            s, W, sh.b_tau[cur][j], gnc, gbc, &tau, &taut, tb);
         const double att = __dadd_rn(sh.b_att[cur][j],
                                      P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
-        cand[tid].score = mix_joint(lam, psi, att);
-        cand[tid].tau = tau;
-        cand[tid].taut = taut;
+        items[tid].score = mix_joint(lam, psi, att);
+        items[tid].tau = tau;
+        items[tid].taut = taut;
       }
       __syncthreads();
-      // ---- P7: exact order over contenders + eos (rank sort) ----
+      PROF_MARK(6);
+      // ---- P7: exact order over contenders + eos (warp-ballot ranks) ----
       const int ni = nc + nb;
-      if (tid < ni) {
-        double ms;
-        int mp, mt;
-        if (tid < nc) {
-          ms = cand[tid].score;
-          mp = cand[tid].parent;
-          mt = cand[tid].token;
-        } else {
-          ms = sh.eosj[tid - nc];
-          mp = tid - nc;
-          mt = C;
-        }
+      for (int i = warp; i < ni; i += kNWarp) {
+        const Item me = items[i < nc ? i : kNT + (i - nc)];
         int rank = 0;
-        for (int q = 0; q < ni; ++q) {
-          double qs;
-          int qp, qt;
-          if (q < nc) {
-            qs = cand[q].score;
-            qp = cand[q].parent;
-            qt = cand[q].token;
-          } else {
-            qs = sh.eosj[q - nc];
-            qp = q - nc;
-            qt = C;
+        for (int q0 = 0; q0 < ni; q0 += 32) {
+          const int qq = q0 + lane;
+          bool b = false;
+          if (qq < ni) {
+            const Item o = items[qq < nc ? qq : kNT + (qq - nc)];
+            b = before(o.score, o.parent, o.token, me.score, me.parent, me.token);
           }
-          rank += before(qs, qp, qt, ms, mp, mt) ? 1 : 0;
+          rank += __popc(__ballot_sync(0xffffffffu, b));
         }
-        if (rank < B + nb) {
+        if (lane == 0 && rank < B + nb) {
           SelE x;
-          x.score = ms;
-          x.parent = mp;
-          x.token = mt;
-          x.slot = tid < nc ? tid : -1;
-          x.tau = tid < nc ? cand[tid].tau : 0;
-          x.taut = tid < nc ? cand[tid].taut : 0;
+          x.score = me.score;
+          x.parent = me.parent;
+          x.token = me.token;
+          x.slot = i < nc ? i : -1;
+          x.tau = me.tau;
+          x.taut = me.taut;
           sh.sel[rank] = x;
         }
       }
       if (tid == 0) sh.nsel = min(ni, B + nb);
       __syncthreads();
+      PROF_MARK(7);
     } else {
       // ---- fallback: fp64 scores for every candidate + exact selection ----
       double* xs = P.xs + (size_t)u * B * (C + 1);
@@ -645,13 +701,13 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         const int j = idx / (C + 1), c = idx - j * (C + 1);
         double sc;
         if (c == C) {
-          sc = sh.eosj[j];
+          sc = items[kNT + j].score;
         } else {
           const double att = __dadd_rn(sh.b_att[cur][j],
                                        P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
           const double psi = lam <= 0.0 ? kLogZero
                                         : psi_only<BMAX>(P, sh, u, cur, j, c, s, e, grid,
-                                                         phi + (size_t)j * P.Tmax);
+                                                         phi + (size_t)j * P.Tmax, tb);
           sc = mix_joint(lam, psi, att);
         }
         xs[idx] = sc;
@@ -714,6 +770,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         __syncthreads();
         non_eos += (sh.sel[sh.nsel - 1].token < C) ? 1 : 0;
       }
+      PROF_MARK(8);
     }
 
     // ---- P8: walk (parallel): finished entries and children ----
@@ -769,6 +826,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       sh.n_fin_new = ee2;
     }
     __syncthreads();
+    PROF_MARK(9);
     if (sh.fallback && tid < sh.nchild) {
       // children states for the fallback path (slot k of area nxt)
       int k = tid, cnt = 0, q = 0;
@@ -782,9 +840,9 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       double* gnc = gam_ptr(P, u, nxt, k, 0);
       double* gbc = gnc + P.Tp;
       int tau, taut;
-      child_recursion<BMAX>(P, sh, u, cur, x.parent, x.token, s, e, grid,
-                            phi + (size_t)x.parent * P.Tmax, gnc, gbc, &tau, &taut,
-                            true);
+      child_recursion_global<BMAX>(P, sh, u, cur, x.parent, x.token, s, e, grid,
+                                   phi + (size_t)x.parent * P.Tmax, gnc, gbc, &tau, &taut,
+                                   tb);
       sh.b_tau[nxt][k] = tau;
       sh.b_taut[nxt][k] = taut;
       hist_u[(size_t)l * B + k].tau = tau;
@@ -831,6 +889,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       sh.done = stop ? 1 : 0;
     }
     __syncthreads();
+    PROF_MARK(10);
     if (sh.done) break;
   }
 
@@ -883,8 +942,6 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
   }
   // n-best over finished entries: (joint desc, insertion asc)
   if (P.nbest > 0 && sh.n_fin > 0) {
-    unsigned char* taken = P.taken + (size_t)u * B * (C + 1);  // reuse (>= B*S? no)
-    (void)taken;
     const int nf = sh.n_fin;
     const int want = min(P.nbest, nf);
     double last_s = HUGE_VAL;
@@ -949,26 +1006,11 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       __syncthreads();
     }
   }
+  __syncthreads();
+  PROF_MARK(11);
 }
 
 // ------------------------------------------------------------ launchers
-template <int BMAX>
-static size_t smem_bytes(const KParams& p) {
-  return sizeof(double) * (size_t)BMAX * p.Tmax + sizeof(float) * (size_t)p.Tmax * BMAX +
-         sizeof(Cand) * kNT + sizeof(double) * (size_t)(p.S + 2);
-}
-
-template <int BMAX>
-static cudaError_t launch_t(const KParams& p, cudaStream_t st) {
-  const size_t sm = smem_bytes<BMAX>(p);
-  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
-  if (err != cudaSuccess) return err;
-  decode_kernel<BMAX><<<p.U, kNT, sm, st>>>(p);
-  return cudaGetLastError();
-}
-
 int bmax_for(int B) {
   if (B <= 4) return 4;
   if (B <= 8) return 8;
@@ -978,13 +1020,18 @@ int bmax_for(int B) {
 }
 
 size_t decode_smem_bytes(const KParams& p) {
-  switch (bmax_for(p.B)) {
-    case 4: return smem_bytes<4>(p);
-    case 8: return smem_bytes<8>(p);
-    case 16: return smem_bytes<16>(p);
-    case 32: return smem_bytes<32>(p);
-  }
-  return 0;
+  return smem_plan(p.Tmax, p.B, bmax_for(p.B), p.C, p.caps, p.S, p.kub_smem).total;
+}
+
+template <int BMAX>
+static cudaError_t launch_t(const KParams& p, cudaStream_t st) {
+  const size_t sm = decode_smem_bytes(p);
+  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+  if (err != cudaSuccess) return err;
+  decode_kernel<BMAX><<<p.U, kNT, sm, st>>>(p);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_decode(const KParams& p, cudaStream_t st) {
