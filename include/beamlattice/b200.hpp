@@ -1,0 +1,289 @@
+// beamlattice/b200.hpp — C++ drop-in for the reference decoding API
+// (/root/reference/proj/include/beamlattice/{grid,scorer,beam_search,batched,
+// segmentation}.hpp) implemented over the C ABI (include/bl_b200.h).
+//
+// Same names, types, argument meaning and exception types as the reference,
+// so a caller of beamlattice::batched_beam_search recompiles against this
+// header and links libbl_b200.so. Decoding runs on the GPU (device 0, or
+// $BL_DEVICE); there is no CPU fallback. Scorers are device scorers: the
+// reference's Uniform/Table/Loop scorers and make_scorer specs.
+#pragma once
+
+#include <cstdint>
+#include <algorithm>
+#include <cstdlib>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../bl_b200.h"
+
+namespace beamlattice {
+
+inline constexpr double kLogZero = -1e30;  // logmath.hpp:11
+inline constexpr int kNoMargin = BL_NO_MARGIN;  // ctc_prefix.hpp:12
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == BL_OK) return;
+  const std::string msg = bl_last_error();
+  if (rc == BL_INVALID_ARGUMENT) throw std::invalid_argument(msg);
+  if (rc == BL_LOGIC_ERROR) throw std::logic_error(msg);
+  throw std::runtime_error(msg);
+}
+inline int device() {
+  const char* d = std::getenv("BL_DEVICE");
+  return d ? std::atoi(d) : 0;
+}
+}  // namespace detail
+
+// grid.hpp:24-55
+struct PosteriorGrid {
+  uint32_t num_frames = 0;
+  uint32_t vocab = 0;
+  uint32_t frame_shift_ms = 10;
+  std::vector<float> logp;
+  int num_tokens() const { return static_cast<int>(vocab) - 1; }
+  int blank_id() const { return static_cast<int>(vocab) - 1; }
+  double at(int frame, int symbol) const {
+    return logp[static_cast<size_t>(frame - 1) * vocab + symbol];
+  }
+  double audio_seconds() const { return num_frames * frame_shift_ms / 1000.0; }
+};
+
+struct Utterance {
+  std::string id;
+  PosteriorGrid grid;
+  uint32_t true_frames = 0;
+};
+
+// beam_search.hpp:14-79
+enum class EosMode { kBaseline, kCtc, kBoth };
+enum class EosTrigger { kBaseline, kCtc, kMaxLen };
+
+inline const char* to_string(EosMode m) {
+  return m == EosMode::kBaseline ? "baseline" : m == EosMode::kCtc ? "ctc" : "both";
+}
+inline const char* to_string(EosTrigger t) {
+  return t == EosTrigger::kBaseline ? "baseline" : t == EosTrigger::kCtc ? "ctc" : "max_len";
+}
+inline EosMode eos_mode_from_string(const std::string& s) {
+  if (s == "baseline") return EosMode::kBaseline;
+  if (s == "ctc") return EosMode::kCtc;
+  if (s == "both") return EosMode::kBoth;
+  throw std::invalid_argument("unknown eos mode: " + s);
+}
+
+struct DecoderConfig {
+  int beam_width = 3;
+  double ctc_weight = 0.3;
+  int eos_m = 3;
+  double eos_dend = -10.0;
+  int eos_c = 2;
+  int margin_m1 = 5;
+  int margin_m2 = kNoMargin;
+  EosMode eos_mode = EosMode::kBoth;
+  double max_steps_ratio = 1.0;
+
+  bl_config c() const {
+    return bl_config{beam_width, ctc_weight, eos_m, eos_dend, eos_c, margin_m1, margin_m2,
+                     static_cast<int>(eos_mode), max_steps_ratio};
+  }
+  void validate() const {
+    const bl_config cc = c();
+    detail::check(bl_config_validate(&cc));
+  }
+};
+
+struct DecodeResult {
+  std::string id;
+  std::vector<int> tokens;
+  double joint_logp = 0.0;
+  std::vector<int> label_times;
+  int steps_taken = 0;
+  EosTrigger eos_trigger = EosTrigger::kMaxLen;
+};
+
+struct DecodeCounters {
+  uint64_t steps = 0;
+  uint64_t scorer_queries = 0;
+  uint64_t ctc_frames_evaluated = 0;
+  DecodeCounters& operator+=(const DecodeCounters& o) {
+    steps += o.steps;
+    scorer_queries += o.scorer_queries;
+    ctc_frames_evaluated += o.ctc_frames_evaluated;
+    return *this;
+  }
+};
+
+// scorer.hpp:11-84 — device scorers
+class Scorer {
+ public:
+  virtual ~Scorer() { bl_scorer_destroy(h_); }
+  int num_tokens() const { return bl_scorer_num_tokens(h_); }
+  std::vector<double> score(const std::string&, const std::vector<int>& prefix) const {
+    std::vector<double> out(num_tokens() + 1);
+    detail::check(bl_scorer_score(h_, prefix.data(), static_cast<int>(prefix.size()),
+                                  out.data()));
+    return out;
+  }
+  const bl_scorer* handle() const { return h_; }
+
+ protected:
+  bl_scorer* h_ = nullptr;
+};
+
+class UniformScorer : public Scorer {
+ public:
+  explicit UniformScorer(int num_tokens) {
+    detail::check(bl_scorer_create("uniform", num_tokens, &h_));
+  }
+};
+
+class LoopScorer : public Scorer {
+ public:
+  LoopScorer(int num_tokens, int loop_token, double p_loop) {
+    detail::check(bl_scorer_create_loop(num_tokens, loop_token, p_loop, &h_));
+  }
+};
+
+class TableScorer : public Scorer {
+ public:
+  TableScorer(int num_tokens, int order) : n_(num_tokens), order_(order) { rebuild(); }
+  int order() const { return order_; }
+  void add_entry(const std::vector<int>& context, std::vector<double> logp) {
+    auto old = table_;
+    table_[context] = std::move(logp);
+    try {
+      rebuild();
+    } catch (...) {
+      table_ = std::move(old);
+      throw;
+    }
+  }
+  const std::map<std::vector<int>, std::vector<double>>& entries() const { return table_; }
+
+ private:
+  void rebuild() {
+    const int w = order_ - 1 > 0 ? order_ - 1 : 1;
+    std::vector<int> len, ctx;
+    std::vector<double> lp;
+    for (const auto& [c, v] : table_) {
+      len.push_back(static_cast<int>(c.size()));
+      for (int i = 0; i < w; ++i) ctx.push_back(i < (int)c.size() ? c[i] : 0);
+      if (v.size() != static_cast<size_t>(n_) + 1)
+        throw std::runtime_error("TableScorer entry: wrong vector size");
+      lp.insert(lp.end(), v.begin(), v.end());
+    }
+    bl_scorer* h = nullptr;
+    detail::check(bl_scorer_create_table(n_, order_, static_cast<int>(len.size()), len.data(),
+                                         ctx.data(), lp.data(), &h));
+    bl_scorer_destroy(h_);
+    h_ = h;
+  }
+  int n_, order_;
+  std::map<std::vector<int>, std::vector<double>> table_;
+};
+
+namespace detail {
+class SpecScorer : public Scorer {
+ public:
+  SpecScorer(const std::string& spec, int n) {
+    detail::check(bl_scorer_create(spec.c_str(), n, &h_));
+  }
+};
+}  // namespace detail
+
+inline std::unique_ptr<Scorer> make_scorer(const std::string& spec, int num_tokens) {
+  return std::make_unique<detail::SpecScorer>(spec, num_tokens);
+}
+
+// segmentation.hpp:45-65
+struct Segment {
+  std::string utterance_id;
+  int start = 0;
+  int end = 0;
+  std::string source;
+};
+
+inline std::vector<Segment> hard_segments(int num_frames, int min_len, int max_len,
+                                          const std::string& utterance_id) {
+  const int cap = (max_len > 0 ? num_frames / max_len : 0) + 2;
+  std::vector<int> s(cap > 0 ? cap : 1), e(cap > 0 ? cap : 1);
+  int n = 0;
+  detail::check(bl_hard_segments(num_frames, min_len, max_len, s.data(), e.data(), cap, &n));
+  std::vector<Segment> out;
+  for (int k = 0; k < n; ++k) out.push_back({utterance_id, s[k], e[k], "hard"});
+  return out;
+}
+
+// batched.hpp:13-38
+struct Batch {
+  std::vector<Utterance> utterances;
+  uint32_t padded_frames = 0;
+};
+
+inline std::vector<Batch> make_batches(std::vector<Utterance> utterances, int batch_size) {
+  std::vector<uint32_t> fr;
+  for (const auto& u : utterances) fr.push_back(u.true_frames);
+  std::vector<int> order(utterances.size());
+  int nb = 0;
+  detail::check(bl_make_batches(static_cast<int>(fr.size()), fr.data(), batch_size,
+                                order.data(), &nb));
+  std::vector<Batch> out;
+  for (size_t i = 0; i < order.size(); i += batch_size) {
+    Batch b;
+    for (size_t k = i; k < order.size() && k < i + batch_size; ++k) {
+      b.utterances.push_back(std::move(utterances[order[k]]));
+      b.padded_frames = std::max(b.padded_frames, b.utterances.back().true_frames);
+    }
+    out.push_back(std::move(b));
+  }
+  return out;
+}
+
+inline std::vector<DecodeResult> batched_beam_search(const Batch& batch, const Scorer& scorer,
+                                                     const DecoderConfig& cfg,
+                                                     DecodeCounters* counters = nullptr) {
+  cfg.validate();
+  if (batch.utterances.empty()) return {};
+  const bl_config cc = cfg.c();
+  bl_decoder* d = nullptr;
+  detail::check(bl_decoder_create(detail::device(), &cc, scorer.handle(), &d));
+  std::unique_ptr<bl_decoder, void (*)(bl_decoder*)> guard(d, bl_decoder_destroy);
+  std::vector<bl_utt> in;
+  for (const auto& u : batch.utterances)
+    in.push_back({u.id.c_str(), u.grid.num_frames, u.grid.vocab, u.grid.frame_shift_ms,
+                  u.grid.logp.data()});
+  bl_results* r = nullptr;
+  detail::check(bl_decode(d, static_cast<int>(in.size()), in.data(), 0, &r));
+  std::unique_ptr<bl_results, void (*)(bl_results*)> rg(r, bl_results_destroy);
+  std::vector<DecodeResult> out;
+  for (int i = 0; i < bl_results_count(r); ++i) {
+    const char* id;
+    const int *tok, *lt;
+    int n, steps, trig;
+    double joint;
+    detail::check(bl_results_get(r, i, &id, &tok, &n, &joint, &lt, &steps, &trig));
+    out.push_back({id, std::vector<int>(tok, tok + n), joint, std::vector<int>(lt, lt + n),
+                   steps, static_cast<EosTrigger>(trig)});
+  }
+  if (counters) {
+    DecodeCounters c;
+    bl_results_counters(r, &c.steps, &c.scorer_queries, &c.ctc_frames_evaluated);
+    *counters += c;
+  }
+  return out;
+}
+
+inline DecodeResult beam_search(const Utterance& utt, const Scorer& scorer,
+                                const DecoderConfig& cfg, DecodeCounters* counters = nullptr) {
+  Batch b;
+  b.utterances = {utt};
+  b.padded_frames = utt.true_frames;
+  return batched_beam_search(b, scorer, cfg, counters).front();
+}
+
+}  // namespace beamlattice

@@ -149,6 +149,8 @@ int bl_results_counters(const bl_results* r, uint64_t* steps,
 int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1_bytes,
                      int* launches, uint64_t* fallback_steps,
                      uint64_t* contenders);
+/* Bytes moved host->device (grids) and device->host (result records). */
+int bl_results_transfer(const bl_results* r, uint64_t* h2d, uint64_t* d2h);
 /* Per-phase device cycle accounting, mean per utterance (16 slots), filled
  * only when the environment variable BL_PROFILE is set. */
 int bl_results_profile(const bl_results* r, double* out16);

@@ -95,6 +95,7 @@ def lib() -> C.CDLL:
     L.bl_results_counters.argtypes = [vp, u64p, u64p, u64p]
     L.bl_results_stats.argtypes = [vp, dp, u64p, ip, u64p, u64p]
     L.bl_results_profile.argtypes = [vp, dp]
+    L.bl_results_transfer.argtypes = [vp, u64p, u64p]
     L.bl_results_destroy.argtypes = [vp]
     _lib = L
     return L
@@ -455,6 +456,10 @@ class Decoder:
                            "launches": nl.value, "fallback_steps": fb.value,
                            "contenders": nc.value, "steps": s.value,
                            "scorer_queries": q.value, "ctc_frames_evaluated": f.value}
+        h2d, d2h = C.c_uint64(), C.c_uint64()
+        L.bl_results_transfer(h, C.byref(h2d), C.byref(d2h))
+        self.last_stats["h2d_bytes"] = h2d.value
+        self.last_stats["d2h_bytes"] = d2h.value
         if os.environ.get("BL_PROFILE"):
             prof = (C.c_double * 16)()
             L.bl_results_profile(h, prof)

@@ -210,7 +210,9 @@ struct bl_decoder {
   double slack = 1.0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;  // H2D of grid chunks, overlapped with decoding
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  std::vector<cudaEvent_t> ev_copy;
   // device scorer
   int sc_order = 1, sc_nent = 0, sc_w = 1;
   DevBuf sc_ctx_len, sc_ctx, sc_row, sc_rows, sc_rowsf;
@@ -231,6 +233,7 @@ struct bl_results {
   };
   std::vector<One> r;
   uint64_t steps = 0, queries = 0, frames = 0, k1 = 0, fallback = 0, contenders = 0;
+  uint64_t h2d = 0, d2h = 0;
   double kernel_ms = 0.0;
   int launches = 0;
   double prof[16] = {0};  // mean cycles per utterance per phase
@@ -351,8 +354,8 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     desc[i].max_steps = static_cast<int>(std::ceil(d->cfg.max_steps_ratio * T));
     S = std::max(S, desc[i].max_steps);
     desc[i].need_tail = d->cfg.margin_m2 < T ? 1 : 0;
-    goff[i] = gtotal;
-    gtotal += ((size_t)T * V + 31) & ~(size_t)31;  // 128-B aligned starts
+    goff[i] = gtotal;  // dense packing: a contiguous host batch is one copy
+    gtotal += (size_t)T * V;
   }
   const int Tp = (Tmax + 2) & ~1;
   const int caps = std::min(2 * B + 16, bl::kNT);
@@ -382,12 +385,37 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   d->h_cnt.ensure(sizeof(unsigned long long) * (size_t)U * 8);
 
   cudaStream_t st = d->stream;
+  // Host grids: runs of utterances contiguous in host memory become single
+  // copies, straight from the caller's buffer when it is pinned, else via
+  // pinned staging; chunks of utterances are copied on a second stream while
+  // earlier chunks decode.
+  struct Run {
+    int i0, i1;  // utterances [i0, i1)
+    const float* src;
+  };
+  std::vector<Run> runs;
   if (!on_device) {
     d->grid.ensure(sizeof(float) * gtotal);
-    d->h_grid.ensure(sizeof(float) * gtotal);
-    float* hg = static_cast<float*>(d->h_grid.p);
-    for (int i = 0; i < n; ++i)
-      std::memcpy(hg + goff[i], utts[i].logp, sizeof(float) * (size_t)desc[i].T * V);
+    for (int i = 0; i < n; ++i) {
+      if (!runs.empty() && runs.back().i1 == i &&
+          utts[i].logp == utts[i - 1].logp + (size_t)desc[i - 1].T * V)
+        runs.back().i1 = i + 1;
+      else
+        runs.push_back({i, i + 1, utts[i].logp});
+    }
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, utts[0].logp) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (!pinned) {
+      d->h_grid.ensure(sizeof(float) * gtotal);
+      float* hg = static_cast<float*>(d->h_grid.p);
+      for (auto& r : runs) {
+        const size_t len = goff[r.i1 - 1] + (size_t)desc[r.i1 - 1].T * V - goff[r.i0];
+        std::memcpy(hg + goff[r.i0], r.src, sizeof(float) * len);
+        r.src = hg + goff[r.i0];
+      }
+    }
   }
 
   bl::KParams p{};
@@ -447,13 +475,43 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   if (bl::decode_smem_bytes(p) > 227 * 1024)
     throw std::invalid_argument("utterance too long for the device decoder's shared memory plan");
 
-  if (!on_device)
-    CK(cudaMemcpyAsync(d->grid.p, d->h_grid.p, sizeof(float) * gtotal,
-                       cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(d->utts.p, d->h_utts.p, sizeof(bl::UttDesc) * U,
                      cudaMemcpyHostToDevice, st));
-  CK(cudaEventRecord(d->ev0, st));
-  CK(bl::launch_decode(p, st));
+  // chunking: one launch when grids are resident; otherwise ~600 utterances
+  // (two waves of resident CTAs) per chunk so copies overlap decoding
+  const int nchunk = on_device ? 1 : std::max(1, std::min(8, U / 600));
+  if ((int)d->ev_copy.size() < nchunk) {
+    for (int k = (int)d->ev_copy.size(); k < nchunk; ++k) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      d->ev_copy.push_back(e);
+    }
+  }
+  if (!on_device) CK(cudaEventRecord(d->ev0, st));  // copies start after the descriptors
+  if (!on_device) CK(cudaStreamWaitEvent(d->copy, d->ev0, 0));
+  int launches = 0;
+  for (int k = 0; k < nchunk; ++k) {
+    const int a = (int)((long long)U * k / nchunk), b = (int)((long long)U * (k + 1) / nchunk);
+    if (!on_device) {
+      for (const auto& r : runs) {
+        const int i0 = std::max(r.i0, a), i1 = std::min(r.i1, b);
+        if (i0 >= i1) continue;
+        const size_t len = goff[i1 - 1] + (size_t)desc[i1 - 1].T * V - goff[i0];
+        CK(cudaMemcpyAsync(static_cast<float*>(d->grid.p) + goff[i0],
+                           r.src + (goff[i0] - goff[r.i0]), sizeof(float) * len,
+                           cudaMemcpyHostToDevice, d->copy));
+        res->h2d += sizeof(float) * len;
+      }
+      CK(cudaEventRecord(d->ev_copy[k], d->copy));
+      CK(cudaStreamWaitEvent(st, d->ev_copy[k], 0));
+    }
+    if (k == 0) CK(cudaEventRecord(d->ev0, st));
+    bl::KParams pk = p;
+    pk.u0 = a;
+    pk.U = b - a;
+    CK(bl::launch_decode(pk, st));
+    ++launches;
+  }
   CK(cudaEventRecord(d->ev1, st));
   CK(cudaMemcpyAsync(d->h_res.p, d->res.p, sizeof(int) * (size_t)U * rs,
                      cudaMemcpyDeviceToHost, st));
@@ -471,7 +529,8 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
   res->kernel_ms = ms;
-  res->launches = 1;
+  res->launches = launches;
+  res->d2h = sizeof(int) * (size_t)U * rs + sizeof(unsigned long long) * (size_t)U * 8;
 
   const int* hr = static_cast<const int*>(d->h_res.p);
   const unsigned long long* hc = static_cast<const unsigned long long*>(d->h_cnt.p);
@@ -664,6 +723,7 @@ int bl_decoder_create(int device, const bl_config* cfg, const bl_scorer* scorer,
     d->cfg = *cfg;
     d->num_tokens = scorer->num_tokens;
     CK(cudaStreamCreateWithFlags(&d->own, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking));
     d->stream = d->own;
     CK(cudaEventCreate(&d->ev0));
     CK(cudaEventCreate(&d->ev1));
@@ -695,6 +755,8 @@ void bl_decoder_destroy(bl_decoder* d) {
   cudaStreamSynchronize(d->stream);
   if (d->ev0) cudaEventDestroy(d->ev0);
   if (d->ev1) cudaEventDestroy(d->ev1);
+  for (auto e : d->ev_copy) cudaEventDestroy(e);
+  if (d->copy) cudaStreamDestroy(d->copy);
   if (d->own) cudaStreamDestroy(d->own);
   delete d;
 }
@@ -752,6 +814,12 @@ int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1,
   if (launches) *launches = r->launches;
   if (fallback) *fallback = r->fallback;
   if (contenders) *contenders = r->contenders;
+  return BL_OK;
+}
+
+int bl_results_transfer(const bl_results* r, uint64_t* h2d, uint64_t* d2h) {
+  if (h2d) *h2d = r->h2d;
+  if (d2h) *d2h = r->d2h;
   return BL_OK;
 }
 

@@ -42,6 +42,7 @@ struct HistRec {
 struct KParams {
   const UttDesc* utts;
   int U, V, C, B;
+  int u0;          // first utterance of this launch (chunked launches)
   int Tmax;        // max T over the batch
   int Tp;          // stride of one gamma array (>= Tmax + 1)
   int S;           // max max_steps over the batch

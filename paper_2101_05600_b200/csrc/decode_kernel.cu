@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
   __shared__ Shared<BMAX> sh;
   __shared__ SpTables tb;
 
-  const int u = blockIdx.x;
+  const int u = blockIdx.x + P.u0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const UttDesc ud = P.utts[u];
   const float* __restrict__ grid = ud.grid;
