@@ -149,6 +149,11 @@ int bl_results_counters(const bl_results* r, uint64_t* steps,
 int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1_bytes,
                      int* launches, uint64_t* fallback_steps,
                      uint64_t* contenders);
+/* Bulk export (one call for all utterances): row i of tokens/label_times
+ * (stride cap >= bl_results_max_tokens) holds n_tokens[i] entries. */
+int bl_results_max_tokens(const bl_results* r);
+int bl_results_export(const bl_results* r, int cap, int* n_tokens, int* steps,
+                      int* trigger, double* joint, int* tokens, int* label_times);
 /* Bytes moved host->device (grids) and device->host (result records). */
 int bl_results_transfer(const bl_results* r, uint64_t* h2d, uint64_t* d2h);
 /* Per-phase device cycle accounting, mean per utterance (16 slots), filled

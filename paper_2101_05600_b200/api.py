@@ -13,6 +13,7 @@ import json
 import math
 import os
 import struct
+from collections.abc import Sequence as _Seq
 from dataclasses import dataclass, field
 from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 
@@ -96,6 +97,9 @@ def lib() -> C.CDLL:
     L.bl_results_stats.argtypes = [vp, dp, u64p, ip, u64p, u64p]
     L.bl_results_profile.argtypes = [vp, dp]
     L.bl_results_transfer.argtypes = [vp, u64p, u64p]
+    L.bl_results_max_tokens.argtypes = [vp]
+    L.bl_results_export.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_void_p]
     L.bl_results_destroy.argtypes = [vp]
     _lib = L
     return L
@@ -372,6 +376,33 @@ def save_table_scorer(path: str, scorer: TableScorer) -> None:
         f.write(json.dumps(j) + "\n")
 
 
+class ResultSet(_Seq):
+    """Results of one decode call as flat arrays (one bulk export from the
+    C ABI); indexing materialises DecodeResult objects lazily."""
+
+    def __init__(self, ids, n_tokens, steps, trigger, joint, tokens, label_times, nbest=None):
+        self.ids, self.n_tokens, self.steps, self.trigger = ids, n_tokens, steps, trigger
+        self.joint, self.tokens, self.label_times = joint, tokens, label_times
+        self.nbest = nbest
+
+    def __len__(self):
+        return len(self.ids)
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(len(self)))]
+        if i < 0:
+            i += len(self)
+        n = int(self.n_tokens[i])
+        return DecodeResult(self.ids[i], self.tokens[i, :n].tolist(), float(self.joint[i]),
+                            self.label_times[i, :n].tolist(), int(self.steps[i]),
+                            TRIGGERS[int(self.trigger[i])],
+                            self.nbest[i] if self.nbest is not None else [])
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+
 # ------------------------------------------------------------------ decoder
 class Decoder:
     """One device decoder (one GPU, one CUDA stream)."""
@@ -379,6 +410,7 @@ class Decoder:
     def __init__(self, scorer: Scorer, cfg: Optional[DecoderConfig] = None,
                  device: int = 0, nbest: int = 1, exact: bool = False,
                  slack: float = 1.0):
+        self.nbest = nbest
         self.cfg = cfg or DecoderConfig()
         self.scorer = scorer
         self.device = device
@@ -411,7 +443,7 @@ class Decoder:
         h = C.c_void_p()
         _check(lib().bl_decode(self._h, n, arr, 1 if on_device else 0, C.byref(h)))
         try:
-            return self._collect(h, counters)
+            return self._collect(h, counters, [d[0] for d in descs])
         finally:
             lib().bl_results_destroy(h)
 
@@ -422,28 +454,33 @@ class Decoder:
                                  g.ctypes.data) for u, g in zip(utterances, keep)],
                                on_device=False, counters=counters)
 
-    def _collect(self, h, counters) -> List[DecodeResult]:
+    def _collect(self, h, counters, ids) -> "ResultSet":
         L = lib()
-        out = []
+        n = L.bl_results_count(h)
+        cap = max(1, L.bl_results_max_tokens(h))
+        nt = np.zeros(n, np.int32)
+        st = np.zeros(n, np.int32)
+        tr = np.zeros(n, np.int32)
+        jt = np.zeros(n, np.float64)
+        tok = np.zeros((n, cap), np.int32)
+        lt = np.zeros((n, cap), np.int32)
+        if n:
+            _check(L.bl_results_export(h, cap, nt.ctypes.data, st.ctypes.data, tr.ctypes.data,
+                                       jt.ctypes.data, tok.ctypes.data, lt.ctypes.data))
+        nbest = [] if self.nbest > 1 else None
         ip = C.POINTER(C.c_int)
-        for i in range(L.bl_results_count(h)):
-            uid = C.c_char_p()
-            tok, lt = ip(), ip()
-            nt, st, tr = C.c_int(), C.c_int(), C.c_int()
-            jt = C.c_double()
-            _check(L.bl_results_get(h, i, C.byref(uid), C.byref(tok), C.byref(nt),
-                                    C.byref(jt), C.byref(lt), C.byref(st),
-                                    C.byref(tr)))
-            n = nt.value
-            r = DecodeResult(uid.value.decode(), [tok[k] for k in range(n)], jt.value,
-                             [lt[k] for k in range(n)], st.value, TRIGGERS[tr.value])
-            for k in range(L.bl_results_nbest_count(h, i)):
-                _check(L.bl_results_nbest(h, i, k, C.byref(tok), C.byref(nt),
-                                          C.byref(jt), C.byref(lt)))
-                m = nt.value
-                r.nbest.append(([tok[q] for q in range(m)], jt.value,
-                                [lt[q] for q in range(m)]))
-            out.append(r)
+        for i in range(n if nbest is not None else 0):
+            if nbest is not None:
+                lst = []
+                t_, l_ = ip(), ip()
+                m_, j_ = C.c_int(), C.c_double()
+                for k in range(L.bl_results_nbest_count(h, i)):
+                    _check(L.bl_results_nbest(h, i, k, C.byref(t_), C.byref(m_), C.byref(j_),
+                                              C.byref(l_)))
+                    lst.append(([t_[q] for q in range(m_.value)], j_.value,
+                                [l_[q] for q in range(m_.value)]))
+                nbest.append(lst)
+        out = ResultSet(ids, nt, st, tr, jt, tok, lt, nbest)
         s, q, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
         L.bl_results_counters(h, C.byref(s), C.byref(q), C.byref(f))
         if counters is not None:

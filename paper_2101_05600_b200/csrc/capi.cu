@@ -232,6 +232,7 @@ struct bl_results {
     std::vector<double> nb_joint;
   };
   std::vector<One> r;
+  int max_tokens = 0;
   uint64_t steps = 0, queries = 0, frames = 0, k1 = 0, fallback = 0, contenders = 0;
   uint64_t h2d = 0, d2h = 0;
   double kernel_ms = 0.0;
@@ -544,6 +545,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     o.trigger = r[2];
     std::memcpy(&o.joint, r + 4, sizeof(double));
     o.tokens.assign(r + bl::kResHdr, r + bl::kResHdr + nt);
+    res->max_tokens = std::max(res->max_tokens, nt);
     o.label_times.assign(r + bl::kResHdr + S, r + bl::kResHdr + S + nt);
     const int nn = r[3];
     for (int k = 0; k < nn; ++k) {
@@ -767,6 +769,7 @@ int bl_decode(bl_decoder* d, int n, const bl_utt* utts, int on_device,
 }
 
 int bl_results_count(const bl_results* r) { return (int)r->r.size(); }
+int bl_results_max_tokens(const bl_results* r) { return r->max_tokens; }
 
 int bl_results_get(const bl_results* r, int i, const char** id, const int** tokens,
                    int* n_tokens, double* joint, const int** label_times, int* steps,
@@ -814,6 +817,22 @@ int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1,
   if (launches) *launches = r->launches;
   if (fallback) *fallback = r->fallback;
   if (contenders) *contenders = r->contenders;
+  return BL_OK;
+}
+
+int bl_results_export(const bl_results* r, int cap, int* n_tokens, int* steps, int* trigger,
+                      double* joint, int* tokens, int* label_times) {
+  for (size_t i = 0; i < r->r.size(); ++i) {
+    const auto& o = r->r[i];
+    const int n = (int)o.tokens.size();
+    if (n > cap) return fail(BL_INVALID_ARGUMENT, "result longer than the export capacity");
+    n_tokens[i] = n;
+    steps[i] = o.steps;
+    trigger[i] = o.trigger;
+    joint[i] = o.joint;
+    std::memcpy(tokens + i * (size_t)cap, o.tokens.data(), sizeof(int) * n);
+    std::memcpy(label_times + i * (size_t)cap, o.label_times.data(), sizeof(int) * n);
+  }
   return BL_OK;
 }
 

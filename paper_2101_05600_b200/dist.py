@@ -12,7 +12,7 @@ from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .api import TRIGGERS, DecodeResult
+from .api import TRIGGERS, DecodeResult, ResultSet
 
 HDR = 5  # n_tokens, steps, trigger, joint (2 x int32 bit pattern)
 
@@ -33,6 +33,19 @@ def pack_results(results: Sequence[DecodeResult], max_tokens: int,
     """Fixed-size int32 records (padded to `rows`): the gather payload."""
     rows = len(results) if rows is None else rows
     out = np.full((rows, record_width(max_tokens)), -1, dtype=np.int32)
+    if isinstance(results, ResultSet):  # vectorised path (bulk-exported arrays)
+        n = len(results)
+        w = min(max_tokens, results.tokens.shape[1])
+        if n and int(results.n_tokens.max()) > max_tokens:
+            raise ValueError("result longer than the record capacity")
+        out[:n, 0] = results.n_tokens
+        out[:n, 1] = results.steps
+        out[:n, 2] = results.trigger
+        out[:n, 3:5] = results.joint.astype("<f8").view("<i4").reshape(n, 2)
+        mask = np.arange(w)[None, :] < results.n_tokens[:, None]
+        out[:n, HDR:HDR + w] = np.where(mask, results.tokens[:, :w], -1)
+        out[:n, HDR + max_tokens:HDR + max_tokens + w] = np.where(mask, results.label_times[:, :w], -1)
+        return out
     for i, r in enumerate(results):
         n = len(r.tokens)
         if n > max_tokens:
