@@ -217,7 +217,7 @@ struct bl_decoder {
   int sc_order = 1, sc_nent = 0, sc_w = 1;
   DevBuf sc_ctx_len, sc_ctx, sc_row, sc_rows, sc_rowsf;
   // workspace
-  DevBuf grid, utts, gam, Ftab, Gtab, kubg, xs, taken, hist, fin, res, cnt, prof;
+  DevBuf grid, utts, gam, Ftab, Gtab, kubg, ubitsg, xs, taken, hist, fin, res, cnt, prof;
   HostBuf h_grid, h_utts, h_res, h_cnt, h_prof;
   bool profile = getenv("BL_PROFILE") != nullptr;
 };
@@ -372,8 +372,20 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   d->Gtab.ensure(sizeof(double) * (size_t)U * Tp);
   d->Ftab.ensure(tail ? sizeof(double) * (size_t)U * Tp * C : 8);
   const int bmax = bl::bmax_for(B);
-  int kub_smem = bl::smem_plan(Tmax, B, bmax, C, caps, S, 1).total <= 100 * 1024 ? 1 : 0;
-  if (!kub_smem) d->kubg.ensure(sizeof(float) * (size_t)U * B * C);
+  // shared-memory plan: the aliased region (P3-P5 keys, P6 staging) is sized
+  // so the whole plan fits 3 CTAs/SM (~71 KB) when the fixed parts allow it;
+  // the upper keys move to HBM when they do not fit.
+  const size_t fixed = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).total;
+  const size_t budget = 66 * 1024;  // + static smem + 1 KB reserve: 3 CTAs in 228 KB
+  const size_t need1 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 1).region_need;
+  const size_t need0 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).region_need;
+  size_t region = fixed + need1 <= budget ? budget - fixed : std::max(need0, budget > fixed ? budget - fixed : 0);
+  const int kub_smem = need1 <= region ? 1 : 0;
+  region = (std::max(region, kub_smem ? need1 : need0) + 15) & ~(size_t)15;
+  if (!kub_smem) {
+    d->kubg.ensure(sizeof(float) * (size_t)U * B * C);
+    d->ubitsg.ensure(sizeof(unsigned) * (size_t)U * (((size_t)B * C + 31) / 32));
+  }
   d->xs.ensure(sizeof(double) * (size_t)U * B * (C + 1));
   d->taken.ensure((size_t)U * B * (C + 1));
   d->hist.ensure(sizeof(bl::HistRec) * (size_t)U * (S + 1) * B);
@@ -451,7 +463,9 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.Ftab = static_cast<double*>(d->Ftab.p);
   p.Gtab = static_cast<double*>(d->Gtab.p);
   p.kubg = static_cast<float*>(d->kubg.p);
+  p.ubitsg = static_cast<unsigned*>(d->ubitsg.p);
   p.kub_smem = kub_smem;
+  p.region_bytes = (int)region;
   p.sc_rowsf = static_cast<const float*>(d->sc_rowsf.p);
   p.xs = static_cast<double*>(d->xs.p);
   p.taken = static_cast<unsigned char*>(d->taken.p);

@@ -69,7 +69,9 @@ struct KParams {
   double* Ftab;    // [U][Tp][C]   eos tail tables (need_tail only)
   double* Gtab;    // [U][Tp]
   float* kubg;     // [U][B][C]    certified upper keys when they do not fit in smem
+  unsigned* ubitsg;  // [U][(B*C+31)/32] underflow-key flags (with kubg)
   int kub_smem;    // 1: upper keys live in shared memory
+  int region_bytes;  // aliased smem region (see smem_plan)
   double* xs;      // [U][B][C+1]  exact joints (fallback path)
   unsigned char* taken;  // [U][B][C+1]
   HistRec* hist;   // [U][S+1][B]
@@ -81,27 +83,30 @@ struct KParams {
 };
 
 // Dynamic shared-memory plan (identical on host and device).
+constexpr int kListCap = 256;  // keys reaching theta0 (P5), 16 B each
+
 struct SmemPlan {
-  size_t phi, phir, region, items, bbl, total;
-  size_t phif, kub;  // P3 view of `region`
-  size_t stl, stb;   // P6 view of `region`
+  size_t phi, region, items, bbl, total;
+  size_t phif, kub, ubits, clist, region_need;  // P3-P5 view of `region`
 };
 constexpr int kItemBytes = 24;  // score(double) + parent, token, tau, taut
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
-__host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C,
-                                              int caps, int S, int kub_smem) {
+// region_bytes: size of the aliased region (P3-P5: fp32 factors, upper keys,
+// underflow flags, theta0 list; P6: contender staging with stride W). The
+// host sizes it so the whole plan fits 3 CTAs per SM when possible.
+__host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, int caps,
+                                              int S, size_t region_bytes, int kub_smem) {
   SmemPlan p;
   p.phi = 0;
-  p.phir = align16(p.phi + sizeof(double) * (size_t)B * Tmax);
-  p.region = align16(p.phir + sizeof(double) * (size_t)B * Tmax);
+  p.region = align16(p.phi + sizeof(double) * (size_t)B * Tmax);
   p.phif = 0;
   p.kub = align16(sizeof(float) * (size_t)Tmax * bmax);
-  const size_t a = p.kub + (kub_smem ? sizeof(float) * (size_t)B * C : 0);
-  p.stl = 0;
-  p.stb = align16(sizeof(float) * (size_t)caps * Tmax);
-  const size_t b = p.stb + sizeof(float) * (size_t)Tmax;
-  p.items = align16(p.region + (a > b ? a : b));
-  p.bbl = align16(p.items + (size_t)kItemBytes * (kNT + bmax));
+  const size_t words = ((size_t)B * C + 31) / 32;
+  p.ubits = kub_smem ? align16(p.kub + sizeof(float) * (size_t)B * C) : p.kub;
+  p.clist = kub_smem ? align16(p.ubits + sizeof(unsigned) * words) : p.kub;
+  p.region_need = p.clist + 16 * (size_t)kListCap;
+  p.items = align16(p.region + region_bytes);
+  p.bbl = align16(p.items + (size_t)kItemBytes * (caps + bmax));
   p.total = align16(p.bbl + sizeof(double) * (size_t)(S + 2));
   return p;
 }

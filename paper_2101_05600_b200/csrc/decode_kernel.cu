@@ -120,8 +120,10 @@ struct Shared {
   int red_p[kNWarp], red_t[kNWarp];
   int s, e, W, nb, n_cont, nsel, nchild, n_fin, n_fin_new, count_long, best_fin;
   int done, trigger, steps, fallback;
+  int row_same;  // scorer row shared by every live parent, or -1
   double best_all, best_fin_val, off;
-  float theta;
+  float theta, theta2;
+  int n_list;
   unsigned long long c_queries, c_frames, c_k1, c_fallback, c_cont, c_steps;
 };
 
@@ -209,6 +211,40 @@ __device__ double child_recursion_smem(const double* ph, const float* lc,
   return psi;
 }
 
+// gamma_n'/gamma_b' chains only (psi is computed in parallel by other warps),
+// same operation order as ctc_prefix.cpp:47-57, argmax as :63-77.
+__device__ void child_state_smem(const double* ph, const float* lc, const float* lb, int s,
+                                 int W, int tau_p, double* gnc, double* gbc, int* tau_out,
+                                 int* taut_out, const SpTables& tb) {
+  const int lo = tau_p > 1 ? tau_p : 1;
+  int best_n = lo, best_b = lo;
+  double val_n = kLogZero, val_b = kLogZero;
+  double gn_prev = kLogZero, gb_prev = kLogZero;
+  for (int i = 0; i < W; ++i) {
+    const int t = s + i;
+    double an, ab;
+    log_add2(gn_prev, ph[i], gb_prev, gn_prev, tb, &an, &ab);
+    const double gn = log_mul(an, (double)lc[i]);
+    const double gb = log_mul(ab, (double)lb[i]);
+    gnc[t] = gn;
+    gbc[t] = gb;
+    if (t >= lo) {
+      if (gn > val_n) {
+        val_n = gn;
+        best_n = t;
+      }
+      if (gb > val_b) {
+        val_b = gb;
+        best_b = t;
+      }
+    }
+    gn_prev = gn;
+    gb_prev = gb;
+  }
+  *tau_out = best_n;
+  *taut_out = best_b;
+}
+
 // Same recursion reading the grid and the parent from global memory
 // (fallback path).
 template <int BMAX>
@@ -280,7 +316,7 @@ __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
   }
 
 template <int BMAX>
-__global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
+__global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const KParams P) {
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ Shared<BMAX> sh;
   __shared__ SpTables tb;
@@ -295,16 +331,18 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
   long long prof_t = clock64();
 
   // dynamic smem carve-up (smem_plan, decode.cuh)
-  const SmemPlan pl = smem_plan(P.Tmax, B, BMAX, C, P.caps, P.S, P.kub_smem);
+  const SmemPlan pl = smem_plan(P.Tmax, B, BMAX, C, P.caps, P.S, P.region_bytes, P.kub_smem);
   double* phi = reinterpret_cast<double*>(dsm + pl.phi);    // [B][Tmax]
-  double* phir = reinterpret_cast<double*>(dsm + pl.phir);  // [B][Tmax]
-  float* PhiF = reinterpret_cast<float*>(dsm + pl.region + pl.phif);  // [Tmax][BMAX]
-  float* kub = P.kub_smem ? reinterpret_cast<float*>(dsm + pl.region + pl.kub)
-                          : P.kubg + (size_t)u * B * C;           // [B][C]
-  // P6 staging (aliases the P3 region)
-  float* stL = reinterpret_cast<float*>(dsm + pl.region + pl.stl);  // [caps][Tmax]
-  float* stB = reinterpret_cast<float*>(dsm + pl.region + pl.stb);  // [Tmax]
-  Item* items = reinterpret_cast<Item*>(dsm + pl.items);            // [kNT + BMAX]
+  unsigned char* region = dsm + pl.region;                  // aliased, region_bytes
+  float* PhiF = reinterpret_cast<float*>(region + pl.phif);  // [Tmax][BMAX]
+  float* kub = P.kub_smem ? reinterpret_cast<float*>(region + pl.kub)
+                          : P.kubg + (size_t)u * B * C;      // [B][C]
+  const int ub_words = (B * C + 31) >> 5;
+  unsigned* ubits = P.kub_smem ? reinterpret_cast<unsigned*>(region + pl.ubits)
+                               : P.ubitsg + (size_t)u * ub_words;  // underflow-key flags
+  float4* clist = reinterpret_cast<float4*>(region + pl.clist);    // [kListCap]
+  const int caps = P.caps;
+  Item* items = reinterpret_cast<Item*>(dsm + pl.items);     // [caps + BMAX], eos at caps
   double* best_by_len = reinterpret_cast<double*>(dsm + pl.bbl);    // [S+2]
 
   const HistRec* hist_c = P.hist + (size_t)u * (P.S + 1) * B;
@@ -407,7 +445,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         it.parent = j;
         it.token = C;
         it.tau = it.taut = 0;
-        items[kNT + j] = it;  // eos candidates live past the contender slots
+        items[caps + j] = it;  // eos candidates live past the contender slots
         jm = sh.b_joint[cur][j];
       }
 #pragma unroll
@@ -417,7 +455,10 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         tail += __shfl_xor_sync(0xffffffffu, tail, o);
       }
       jm = warp_max_d(jm);
+      const int r0 = sh.b_row[cur][0];
+      const bool same = __all_sync(0xffffffffu, j >= nb || sh.b_row[cur][j] == r0);
       if (lane == 0) {
+        sh.row_same = same ? r0 : -1;
         sh.s = ws;
         sh.e = we;
         const int W = we - ws + 1;
@@ -442,7 +483,6 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
       const double* gbp = gnp + P.Tp;
       const double gb = gread(gbp, t - 1, vlo, cov);
       phi[(size_t)j * P.Tmax + i] = log_add(gb, gread(gnp, t - 1, vlo, cov), tb);
-      phir[(size_t)j * P.Tmax + i] = gb;  // repeat column: ctc_prefix.cpp:50
     }
     __syncthreads();
 
@@ -476,106 +516,155 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         }
         PhiF[(size_t)i * BMAX + j] = v;
       }
+      for (int idx = tid; idx < ub_words; idx += kNT) ubits[idx] = 0u;
       __syncthreads();
       PROF_MARK(2);
 
       // ---- P3: K1 bulk prefix score + certified fp32 joint keys ----
-      float list[BMAX];
-#pragma unroll
-      for (int q = 0; q < BMAX; ++q) list[q] = -INFINITY;
+      // Two adjacent token columns per thread. Every key's upper bound goes to
+      // `kub` (underflow keys flagged in `ubits`); each thread keeps only its
+      // top-2 certified lower bounds (theta0, P4), the exact theta comes from
+      // the short list of keys that reach theta0 (P5).
+      float l1 = -INFINITY, l2 = -INFINITY;
       const float hw = (float)(lam * (P.dpsi0 + W * P.dpsi1)) + 1e-4f;
       const float gf = P.guard_f;
-      for (int c = tid; c < C; c += kNT) {
-        float S[BMAX];
+      const int row_same = sh.row_same;
+      const bool vec2 = (V & 1) == 0;  // float2 loads need 8-byte aligned rows
+      auto acc = [&](float(&Sx)[BMAX], float& m, float x, const float4* ph) {
+        if (x > gf) {
+          if (x > m + 8.f) {
+            const float r = __expf(m - x);
 #pragma unroll
-        for (int q = 0; q < BMAX; ++q) S[q] = 0.f;
-        float m = -INFINITY;
-        const float* col = grid + (size_t)(s - 1) * V + c;
-        for (int i0 = 0; i0 < W; i0 += 8) {
-          float xv[8];
+            for (int q = 0; q < BMAX; ++q) Sx[q] *= r;
+            m = x;
+          }
+          const float pe = __expf(x - m);
 #pragma unroll
-          for (int k = 0; k < 8; ++k)
-            xv[k] = (i0 + k < W) ? __ldg(col + (size_t)(i0 + k) * V) : -INFINITY;
-#pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            const float x = xv[k];
-            if (x > gf) {
-              if (x > m + 8.f) {
-                const float r = __expf(m - x);
-#pragma unroll
-                for (int q = 0; q < BMAX; ++q) S[q] *= r;
-                m = x;
-              }
-              const float p = __expf(x - m);
-              const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)(i0 + k) * BMAX);
-#pragma unroll
-              for (int q = 0; q < BMAX / 4; ++q) {
-                const float4 f = ph[q];
-                S[4 * q + 0] = fmaf(f.x, p, S[4 * q + 0]);
-                S[4 * q + 1] = fmaf(f.y, p, S[4 * q + 1]);
-                S[4 * q + 2] = fmaf(f.z, p, S[4 * q + 2]);
-                S[4 * q + 3] = fmaf(f.w, p, S[4 * q + 3]);
-              }
-            }
+          for (int q = 0; q < BMAX / 4; ++q) {
+            const float4 f = ph[q];
+            Sx[4 * q + 0] = fmaf(f.x, pe, Sx[4 * q + 0]);
+            Sx[4 * q + 1] = fmaf(f.y, pe, Sx[4 * q + 1]);
+            Sx[4 * q + 2] = fmaf(f.z, pe, Sx[4 * q + 2]);
+            Sx[4 * q + 3] = fmaf(f.w, pe, Sx[4 * q + 3]);
           }
         }
-        // certified keys: [key - hw', key + hw'] contains joint(j, c) - off
+      };
+      long long tq_frames = 0, tq_keys = 0;
+      for (int c0 = 2 * tid; c0 < C; c0 += 2 * kNT) {
+        const long long tq1 = clock64();
+        const bool two = c0 + 1 < C;
+        float S0[BMAX], S1[BMAX];
 #pragma unroll
-        for (int q = 0; q < BMAX; ++q) {
-          if (q >= nb) break;
-          float klo = -INFINITY, kub_v = -INFINITY;
-          if (c != sh.b_last[cur][q]) {
-            const float r = P.sc_rowsf[(size_t)sh.b_row[cur][q] * V + c];
-            if (r == -INFINITY) {
-              klo = kub_v = kZeroKey;  // att is log-zero: joint exactly kLogZero
-            } else if (lam <= 0.0) {
-              const float key = sh.kb[q] + r;
-              const float h = hw + fabsf(key) * 2.4e-7f;
-              klo = key - h;
-              kub_v = key + h;
-            } else if (sh.mzero[q] || m == -INFINITY) {
-              klo = kub_v = kZeroKey;  // psi exactly kLogZero
-            } else if (S[q] >= 7.888609052210118e-31f) {  // 2^-100
-              const float key = sh.kb[q] + lamf * (m + logf(S[q])) + r;
-              const float h = hw + fabsf(key) * 2.4e-7f;
-              klo = key - h;
-              kub_v = key + h;
-            } else {  // fp32 underflow: certified upper bound only
-              const float key = sh.kb[q] + lamf * (m - 68.62157f) + r;
-              klo = -INFINITY;
-              kub_v = key + hw + fabsf(key) * 2.4e-7f;
-            }
-            if (klo > list[BMAX - 1]) {
-              float v = klo;
+        for (int q = 0; q < BMAX; ++q) S0[q] = S1[q] = 0.f;
+        float m0 = -INFINITY, m1 = -INFINITY;
+        const float r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
+        const float r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
+        const float* col = grid + (size_t)(s - 1) * V + c0;
+        auto ld = [&](int i, float& a, float& b) {
+          if (i >= W) {
+            a = b = -INFINITY;
+          } else if (vec2 && two) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(col + (size_t)i * V));
+            a = v.x;
+            b = v.y;
+          } else {
+            a = __ldg(col + (size_t)i * V);
+            b = two ? __ldg(col + (size_t)i * V + 1) : -INFINITY;
+          }
+        };
+        float xa[4], xb[4];
 #pragma unroll
-              for (int rr = 0; rr < BMAX; ++rr) {
-                if (v > list[rr]) {
-                  const float t2 = list[rr];
-                  list[rr] = v;
-                  v = t2;
+        for (int k = 0; k < 4; ++k) ld(k, xa[k], xb[k]);
+        for (int i0 = 0; i0 < W; i0 += 4) {
+          float ya[4], yb[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            ya[k] = xa[k];
+            yb[k] = xb[k];
+          }
+#pragma unroll
+          for (int k = 0; k < 4; ++k) ld(i0 + 4 + k, xa[k], xb[k]);  // prefetch
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)(i0 + k) * BMAX);
+            acc(S0, m0, ya[k], ph);
+            acc(S1, m1, yb[k], ph);
+          }
+        }
+        const long long tq2 = clock64();
+        tq_frames += tq2 - tq1;
+        // certified keys: joint(j, c) - off in [key - h, key + h]
+#pragma unroll
+        for (int cc = 0; cc < 2; ++cc) {
+          const int c = c0 + cc;
+          if (cc == 1 && !two) break;
+          const float m = cc ? m1 : m0;
+#pragma unroll
+          for (int q = 0; q < BMAX; ++q) {
+            if (q < nb) {
+              const float Sq = cc ? S1[q] : S0[q];
+              float klo = -INFINITY, kub_v = -INFINITY;
+              bool under = false;
+              if (c != sh.b_last[cur][q]) {
+                const float r = row_same >= 0 ? (cc ? r1s : r0s)
+                                              : P.sc_rowsf[(size_t)sh.b_row[cur][q] * V + c];
+                if (r == -INFINITY) {
+                  klo = kub_v = kZeroKey;  // att is log-zero: joint exactly kLogZero
+                } else if (lam <= 0.0) {
+                  const float key = sh.kb[q] + r;
+                  const float h = hw + fabsf(key) * 2.4e-7f;
+                  klo = key - h;
+                  kub_v = key + h;
+                } else if (sh.mzero[q] || m == -INFINITY) {
+                  klo = kub_v = kZeroKey;  // psi exactly kLogZero
+                } else if (Sq >= 7.888609052210118e-31f) {  // 2^-100
+                  const float key = sh.kb[q] + lamf * (m + __logf(Sq)) + r;
+                  const float h = hw + fabsf(key) * 2.4e-7f;
+                  klo = key - h;
+                  kub_v = key + h;
+                } else {  // fp32 underflow: certified upper bound only
+                  const float key = sh.kb[q] + lamf * (m - 68.62157f) + r;
+                  klo = -INFINITY;
+                  kub_v = key + hw + fabsf(key) * 2.4e-7f;
+                  under = true;
+                }
+                if (klo > l2) {
+                  if (klo > l1) {
+                    l2 = l1;
+                    l1 = klo;
+                  } else {
+                    l2 = klo;
+                  }
                 }
               }
+              const int kidx = q * C + c;
+              kub[kidx] = kub_v;
+              if (under) atomicOr(&ubits[kidx >> 5], 1u << (kidx & 31));
             }
           }
-          kub[(size_t)q * C + c] = kub_v;
         }
+        tq_keys += clock64() - tq2;
+      }
+      if (P.prof && tid == 0) {
+        P.prof[(size_t)u * 16 + 12] += tq_frames;
+        P.prof[(size_t)u * 16 + 13] += tq_keys;
       }
 
-      // ---- P4: theta = B-th largest certified lower bound ----
+      // ---- P4: theta0 = B-th largest of the per-thread top-2 lower bounds:
+      // a valid bound (B candidates certainly reach it) ----
       for (int r = 0; r < B; ++r) {
-        const float h = list[0];
-        const float mx = warp_max_f(h);
-        const unsigned who = __ballot_sync(0xffffffffu, h == mx);
+        const float mx = warp_max_f(l1);
+        const unsigned who = __ballot_sync(0xffffffffu, l1 == mx);
         if (lane == __ffs(who) - 1) {
-#pragma unroll
-          for (int q = 0; q < BMAX - 1; ++q) list[q] = list[q + 1];
-          list[BMAX - 1] = -INFINITY;
+          l1 = l2;
+          l2 = -INFINITY;
         }
         if (lane == 0) sh.wl[warp][r] = mx;
       }
       __syncthreads();
       PROF_MARK(3);
       if (warp == 0) {
+        float list[BMAX];
 #pragma unroll
         for (int q = 0; q < BMAX; ++q)
           list[q] = (lane < kNWarp && q < B) ? sh.wl[lane][q] : -INFINITY;
@@ -591,36 +680,65 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
           }
           th = mx;
         }
-        if (lane == 0) sh.theta = th;
+        if (lane == 0) {
+          sh.theta = th;
+          sh.theta2 = -INFINITY;  // stays when fewer than B keys are listed
+          sh.n_list = 0;
+        }
       }
       __syncthreads();
       PROF_MARK(4);
 
-      // ---- P5: contenders (warp-aggregated appends) ----
-      const float theta = sh.theta;
-      for (int c0 = 0; c0 < C; c0 += kNT) {
-        const int c = c0 + tid;
+      // ---- P5: every key whose upper bound reaches theta0 goes to a short
+      // list; the exact theta (B-th largest lower bound) is ranked inside it
+      // and the contenders are the list entries that reach max(theta, theta0).
+      const float theta0 = sh.theta;
+      for (int c = tid; c < C; c += kNT) {
         for (int q = 0; q < nb; ++q) {
-          const bool hit = c < C && c != sh.b_last[cur][q] && kub[(size_t)q * C + c] >= theta;
-          const unsigned mask = __ballot_sync(0xffffffffu, hit);
-          if (mask) {
-            int base = 0;
-            if (lane == 0) base = atomicAdd(&sh.n_cont, __popc(mask));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (hit) {
-              const int idx = base + __popc(mask & ((1u << lane) - 1));
-              if (idx < kNT) {
-                items[idx].parent = q;
-                items[idx].token = c;
-              }
+          const int kidx = q * C + c;
+          const float ku = kub[kidx];
+          if (ku >= theta0 && c != sh.b_last[cur][q]) {
+            const int idx = atomicAdd(&sh.n_list, 1);
+            if (idx < kListCap) {
+              const bool under = (ubits[kidx >> 5] >> (kidx & 31)) & 1u;
+              // derived lower bound: never above the key's true lower bound
+              clist[idx] = make_float4(
+                  under ? -INFINITY : ku - 2.000002f * (hw + (fabsf(ku) + hw) * 2.4e-7f), ku,
+                  __int_as_float(q), __int_as_float(c));
             }
+          }
+        }
+      }
+      __syncthreads();
+      const int nl = sh.n_list;
+      if (nl > kListCap) {
+        if (tid == 0) sh.n_cont = P.caps + 1;  // overflow: exact fallback
+      } else {
+        if (tid < nl) {
+          const float lo = clist[tid].x;
+          int rank = 0;
+          for (int k = 0; k < nl; ++k) {
+            const float o = clist[k].x;
+            rank += (o > lo || (o == lo && k < tid)) ? 1 : 0;
+          }
+          if (rank == B - 1) sh.theta2 = lo;  // unique writer (ranks are distinct)
+        }
+      }
+      __syncthreads();
+      if (nl <= kListCap) {
+        const float theta = fmaxf(sh.theta2, theta0);
+        if (tid < nl && clist[tid].y >= theta) {
+          const int idx = atomicAdd(&sh.n_cont, 1);
+          if (idx < caps) {
+            items[idx].parent = __float_as_int(clist[tid].z);
+            items[idx].token = __float_as_int(clist[tid].w);
           }
         }
       }
       __syncthreads();
       if (warp == 0 && lane < nb && sh.b_last[cur][lane] >= 0) {
         const int idx = atomicAdd(&sh.n_cont, 1);  // repeat column: always exact
-        if (idx < kNT) {
+        if (idx < caps) {
           items[idx].parent = lane;
           items[idx].token = sh.b_last[cur][lane];
         }
@@ -636,44 +754,102 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
 
     if (!sh.fallback) {
       const int nc = sh.n_cont;
-      // ---- P6a: stage the contenders' grid columns and the blank column ----
-      for (int idx = tid; idx < (nc + 1) * W; idx += kNT) {
-        const int q = idx / W, i = idx - q * W;
-        const int c = q < nc ? items[q].token : blank;
-        const float v = grid[(size_t)(s - 1 + i) * V + c];
-        if (q < nc) stL[(size_t)q * P.Tmax + i] = v;
-        else stB[i] = v;
+      const long long ts0 = clock64();
+      // ---- P6a: stage the contenders' grid columns, the blank column and the
+      // repeat-column phi (gamma_b[t-1], ctc_prefix.cpp:50) with stride W ----
+      const size_t offB = align16(sizeof(float) * (size_t)nc * W);
+      const size_t offR = offB + align16(sizeof(float) * (size_t)W);
+      const bool staged = offR + sizeof(double) * (size_t)nb * W <= (size_t)P.region_bytes;
+      float* stL = reinterpret_cast<float*>(region);
+      float* stB = reinterpret_cast<float*>(region + offB);
+      double* stR = reinterpret_cast<double*>(region + offR);
+      if (staged) {
+        for (int idx = tid; idx < (nc + 1) * W; idx += kNT) {
+          const int q = idx / W, i = idx - q * W;
+          const int c = q < nc ? items[q].token : blank;
+          const float v = grid[(size_t)(s - 1 + i) * V + c];
+          if (q < nc) stL[idx] = v;
+          else stB[i] = v;
+        }
+        for (int idx = tid; idx < nb * W; idx += kNT) {
+          const int j = idx / W, i = idx - j * W;
+          if (sh.b_last[cur][j] < 0) continue;
+          const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
+          stR[idx] = gread(gbp, s + i - 1, sh.b_vlo[cur][j], sh.b_cov[cur][j]);
+        }
       }
       __syncthreads();
-      // ---- P6: exact re-scoring of contenders, with their child states ----
-      // (reference op order, ctc_prefix.cpp:47-77; one thread per contender)
-      if (tid < nc) {
-        const int j = items[tid].parent, c = items[tid].token;
-        const bool repeat = sh.b_last[cur][j] == c;
-        double* gnc = gam_ptr(P, u, nxt, tid, 0);
-        double* gbc = gnc + P.Tp;
-        int tau, taut;
-        const double psi = child_recursion_smem(
-            (repeat ? phir : phi) + (size_t)j * P.Tmax, stL + (size_t)tid * P.Tmax, stB,
-            s, W, sh.b_tau[cur][j], gnc, gbc, &tau, &taut, tb);
-        const double att = __dadd_rn(sh.b_att[cur][j],
-                                     P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
-        items[tid].score = mix_joint(lam, psi, att);
-        items[tid].tau = tau;
-        items[tid].taut = taut;
+      if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 15] += clock64() - ts0;
+      // ---- P6: contenders re-scored exactly. Warps [0, nser): the serial
+      // gamma_n'/gamma_b' chains (one thread per contender, reference op
+      // order); the other warps: psi by a parallel fp64 log-sum-exp. ----
+      const int nser = (nc + 31) >> 5;
+      if (warp < nser) {
+        const int q = tid;
+        if (q < nc) {
+          const int j = items[q].parent, c = items[q].token;
+          const bool repeat = sh.b_last[cur][j] == c;
+          double* gnc = gam_ptr(P, u, nxt, q, 0);
+          double* gbc = gnc + P.Tp;
+          int tau, taut;
+          const long long tr0 = clock64();
+          if (staged) {
+            child_state_smem(repeat ? stR + (size_t)j * W : phi + (size_t)j * P.Tmax,
+                             stL + (size_t)q * W, stB, s, W, sh.b_tau[cur][j], gnc, gbc, &tau,
+                             &taut, tb);
+          } else {
+            const double psi = child_recursion_global<BMAX>(
+                P, sh, u, cur, j, c, s, e, grid, phi + (size_t)j * P.Tmax, gnc, gbc, &tau,
+                &taut, tb);
+            const double att = __dadd_rn(sh.b_att[cur][j],
+                                         P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+            items[q].score = mix_joint(lam, psi, att);
+          }
+          items[q].tau = tau;
+          items[q].taut = taut;
+          if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - tr0;
+        }
+      } else if (staged) {
+        for (int q = warp - nser; q < nc; q += kNWarp - nser) {
+          const int j = items[q].parent, c = items[q].token;
+          const bool repeat = sh.b_last[cur][j] == c;
+          const double* ph = repeat ? stR + (size_t)j * W : phi + (size_t)j * P.Tmax;
+          const float* lc = stL + (size_t)q * W;
+          double mloc = -HUGE_VAL;
+          for (int i = lane; i < W; i += 32) {
+            const double term = log_mul(ph[i], (double)lc[i]);
+            if (!is_zero(term) && term > mloc) mloc = term;
+          }
+          const double M = warp_max_d(mloc);
+          double sum = 0.0;
+          if (M != -HUGE_VAL) {
+            for (int i = lane; i < W; i += 32) {
+              const double term = log_mul(ph[i], (double)lc[i]);
+              if (!is_zero(term)) sum += exp(term - M);
+            }
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+          if (lane == 0) {
+            const double psi = M == -HUGE_VAL ? kLogZero : M + log(sum);
+            const double att = __dadd_rn(sh.b_att[cur][j],
+                                         P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+            items[q].score = mix_joint(lam, psi, att);
+          }
+        }
       }
       __syncthreads();
       PROF_MARK(6);
       // ---- P7: exact order over contenders + eos (warp-ballot ranks) ----
       const int ni = nc + nb;
       for (int i = warp; i < ni; i += kNWarp) {
-        const Item me = items[i < nc ? i : kNT + (i - nc)];
+        const Item me = items[i < nc ? i : caps + (i - nc)];
         int rank = 0;
         for (int q0 = 0; q0 < ni; q0 += 32) {
           const int qq = q0 + lane;
           bool b = false;
           if (qq < ni) {
-            const Item o = items[qq < nc ? qq : kNT + (qq - nc)];
+            const Item o = items[qq < nc ? qq : caps + (qq - nc)];
             b = before(o.score, o.parent, o.token, me.score, me.parent, me.token);
           }
           rank += __popc(__ballot_sync(0xffffffffu, b));
@@ -701,7 +877,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         const int j = idx / (C + 1), c = idx - j * (C + 1);
         double sc;
         if (c == C) {
-          sc = items[kNT + j].score;
+          sc = items[caps + j].score;
         } else {
           const double att = __dadd_rn(sh.b_att[cur][j],
                                        P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
@@ -899,6 +1075,38 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
   const int fcur = sh.steps & 1;  // beam after the last processed step
   int* res = P.res + (size_t)u * P.res_stride;
   const int S = P.S;
+  // The back-pointer walks are serial pointer chases: stage the history in
+  // shared memory first (packed {token, parent | tau << 16}) when it fits.
+  const int nsteps = sh.steps;
+  int2* hs = reinterpret_cast<int2*>(region);
+  const bool hist_smem = (size_t)(nsteps + 1) * B * sizeof(int2) <= (size_t)P.region_bytes;
+  if (hist_smem) {
+    for (int idx = tid + B; idx < (nsteps + 1) * B; idx += kNT) {
+      const HistRec h = hist_c[idx];
+      hs[idx] = make_int2(h.token, h.parent | (h.tau << 16));
+    }
+  }
+  __syncthreads();
+  auto walk = [&](int bp_step, int bp_slot, int* tok, int* lt) {
+    int k = bp_slot;
+    for (int st = bp_step; st >= 1; --st) {
+      int token, parent, tau;
+      if (hist_smem) {
+        const int2 h = hs[(size_t)st * B + k];
+        token = h.x;
+        parent = h.y & 0xffff;
+        tau = h.y >> 16;
+      } else {
+        const HistRec h = hist_c[(size_t)st * B + k];
+        token = h.token;
+        parent = h.parent;
+        tau = h.tau;
+      }
+      tok[st - 1] = token;
+      lt[st - 1] = tau;
+      k = parent;
+    }
+  };
   if (tid == 0) {
     int bp_step, bp_slot, trig = sh.trigger;
     double joint;
@@ -923,13 +1131,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
     reinterpret_cast<double*>(res + 4)[0] = joint;
     res[6] = sh.n_fin;
     res[7] = 0;
-    int k = bp_slot;
-    for (int st = bp_step; st >= 1; --st) {
-      const HistRec h = hist_c[(size_t)st * B + k];
-      res[kResHdr + st - 1] = h.token;
-      res[kResHdr + S + st - 1] = h.tau;
-      k = h.parent;
-    }
+    walk(bp_step, bp_slot, res + kResHdr, res + kResHdr + S);
     unsigned long long* cn = P.cnt + (size_t)u * 8;
     cn[0] = sh.c_steps;
     cn[1] = sh.c_queries;
@@ -989,13 +1191,7 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
         nb_rec[0] = f.bp_step;
         nb_rec[1] = wi;
         reinterpret_cast<double*>(nb_rec + 2)[0] = f.joint;
-        int k = f.bp_slot;
-        for (int st = f.bp_step; st >= 1; --st) {
-          const HistRec h = hist_c[(size_t)st * B + k];
-          nb_rec[4 + st - 1] = h.token;
-          nb_rec[4 + S + st - 1] = h.tau;
-          k = h.parent;
-        }
+        walk(f.bp_step, f.bp_slot, nb_rec + 4, nb_rec + 4 + S);
         res[3] = r + 1;
         sh.red_s[0] = ws2;
         sh.red_p[0] = wi;
@@ -1014,13 +1210,15 @@ __global__ void __launch_bounds__(kNT, 2) decode_kernel(const KParams P) {
 int bmax_for(int B) {
   if (B <= 4) return 4;
   if (B <= 8) return 8;
+  if (B <= 12) return 12;
   if (B <= 16) return 16;
+  if (B <= 24) return 24;
   if (B <= 32) return 32;
   return 0;
 }
 
 size_t decode_smem_bytes(const KParams& p) {
-  return smem_plan(p.Tmax, p.B, bmax_for(p.B), p.C, p.caps, p.S, p.kub_smem).total;
+  return smem_plan(p.Tmax, p.B, bmax_for(p.B), p.C, p.caps, p.S, p.region_bytes, p.kub_smem).total;
 }
 
 template <int BMAX>
@@ -1038,7 +1236,9 @@ cudaError_t launch_decode(const KParams& p, cudaStream_t st) {
   switch (bmax_for(p.B)) {
     case 4: return launch_t<4>(p, st);
     case 8: return launch_t<8>(p, st);
+    case 12: return launch_t<12>(p, st);
     case 16: return launch_t<16>(p, st);
+    case 24: return launch_t<24>(p, st);
     case 32: return launch_t<32>(p, st);
   }
   return cudaErrorInvalidValue;

@@ -3,7 +3,7 @@ os.environ["BL_PROFILE"] = "1"
 sys.path.insert(0, ".")
 import numpy as np
 import paper_2101_05600_b200 as bl
-names = ["init+Ftab", "P1 window/eos", "P2 phi/PhiF", "P3 bulk(+P4a)", "P4 theta", "P5 collect", "P6 contenders", "P7 rank", "fallback", "P8 walk", "P9 end", "finalize"]
+names = ["init+Ftab", "P1 window/eos", "P2 phi/PhiF", "P3 bulk(+P4a)", "P4 theta", "P5 collect", "P6 contenders", "P7 rank", "fallback", "P8 walk", "P9 end", "finalize", "t0:P3 frames", "t0:P3 keys", "t0:P6 serial", "t0:P6 staging"]
 rng = np.random.default_rng(1)
 for (V, B, M2, U) in [(500, 10, 20, 64), (500, 10, bl.NO_MARGIN, 64), (5000, 10, bl.NO_MARGIN, 32)]:
     G = []
@@ -14,7 +14,7 @@ for (V, B, M2, U) in [(500, 10, 20, 64), (500, 10, bl.NO_MARGIN, 64), (5000, 10,
     for rep in range(2):
         dec.decode(utts)
     st = dec.last_stats
-    pc = st["profile_cycles"]; tot = sum(pc)
-    print(f"V={V} B={B} M2={M2} U={U}: kernel {st['kernel_ms']:.2f} ms, steps/utt {st['steps']/U:.0f}, contenders/step {st['contenders']/st['steps']:.1f}, fallback {st['fallback_steps']}")
+    pc = st["profile_cycles"]; tot = sum(pc[:12])
+    print(f"V={V} B={B} M2={M2} U={U} W~{st['ctc_frames_evaluated'] / max(1, st['scorer_queries']) / (V - 1):.1f}: kernel {st['kernel_ms']:.2f} ms, steps/utt {st['steps']/U:.0f}, contenders/step {st['contenders']/st['steps']:.1f}, fallback {st['fallback_steps']}")
     for n, c in zip(names, pc):
         print(f"   {n:16s} {c/1e3:10.1f} kcyc {100*c/tot:5.1f}%  per-step {c/(st['steps']/U):8.0f} cyc")
