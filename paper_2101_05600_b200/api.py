@@ -56,6 +56,9 @@ class _Utt(C.Structure):
 
 
 _lib = None
+_UTT_DTYPE = np.dtype([("id", np.uint64), ("num_frames", np.uint32), ("vocab", np.uint32),
+                       ("frame_shift_ms", np.uint32), ("pad", np.uint32), ("logp", np.uint64)])
+assert _UTT_DTYPE.itemsize == C.sizeof(_Utt)
 
 
 def lib() -> C.CDLL:
@@ -411,6 +414,7 @@ class Decoder:
                  device: int = 0, nbest: int = 1, exact: bool = False,
                  slack: float = 1.0):
         self.nbest = nbest
+        self._desc_cache = None
         self.cfg = cfg or DecoderConfig()
         self.scorer = scorer
         self.device = device
@@ -431,19 +435,37 @@ class Decoder:
 
     def decode_raw(self, descs: Sequence[Tuple[str, int, int, int]],
                    on_device: bool, counters: Optional[DecodeCounters] = None,
-                   frame_shift_ms: int = 10) -> List[DecodeResult]:
-        """descs: (id, num_frames, vocab, data pointer)."""
+                   frame_shift_ms: int = 10) -> "ResultSet":
+        """descs: (id, num_frames, vocab, data pointer). The bl_utt array is
+        built vectorised (one ids buffer, numpy structured records)."""
         n = len(descs)
-        arr = (_Utt * max(n, 1))()
-        keep = []
-        for i, (uid, T, V, ptr) in enumerate(descs):
-            b = uid.encode()
-            keep.append(b)
-            arr[i] = _Utt(b, T, V, frame_shift_ms, C.c_void_p(ptr))
+        ids = [d[0] for d in descs]
+        key = (id(descs), n, frame_shift_ms)
+        cached = self._desc_cache
+        if cached is not None and cached[0] == key and cached[1] is descs:
+            arr = cached[2]
+        else:
+            blob = b"".join(i.encode() + b"\0" for i in ids)
+            buf = C.create_string_buffer(blob, len(blob))
+            offs = np.zeros(n, np.int64)
+            if n:
+                lens = np.fromiter((len(i.encode()) + 1 for i in ids), np.int64, n)
+                offs[1:] = np.cumsum(lens)[:-1]
+            rec = np.zeros(max(n, 1), dtype=_UTT_DTYPE)
+            if n:
+                rec["id"][:n] = C.addressof(buf) + offs
+                rec["num_frames"][:n] = [d[1] for d in descs]
+                rec["vocab"][:n] = [d[2] for d in descs]
+                rec["frame_shift_ms"][:n] = frame_shift_ms
+                rec["logp"][:n] = [d[3] for d in descs]
+            arr = (rec, buf)
+            self._desc_cache = (key, descs, arr)
+        rec = arr[0]
         h = C.c_void_p()
-        _check(lib().bl_decode(self._h, n, arr, 1 if on_device else 0, C.byref(h)))
+        _check(lib().bl_decode(self._h, n, rec.ctypes.data_as(C.POINTER(_Utt)),
+                               1 if on_device else 0, C.byref(h)))
         try:
-            return self._collect(h, counters, [d[0] for d in descs])
+            return self._collect(h, counters, ids)
         finally:
             lib().bl_results_destroy(h)
 

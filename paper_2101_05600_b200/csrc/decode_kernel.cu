@@ -530,100 +530,120 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const
       const float gf = P.guard_f;
       const int row_same = sh.row_same;
       const bool vec2 = (V & 1) == 0;  // float2 loads need 8-byte aligned rows
+      // m starts at the log-zero guard (not -inf): a log-zero grid entry then
+      // never triggers a rescale and contributes exp(-1e30 - m) = 0, so the
+      // per-element guard test disappears (an all-zero column keeps m == gf).
       auto acc = [&](float(&Sx)[BMAX], float& m, float x, const float4* ph) {
-        if (x > gf) {
-          if (x > m + 8.f) {
-            const float r = __expf(m - x);
+        if (x > m + 8.f) {
+          const float r = __expf(m - x);
 #pragma unroll
-            for (int q = 0; q < BMAX; ++q) Sx[q] *= r;
-            m = x;
-          }
-          const float pe = __expf(x - m);
+          for (int q = 0; q < BMAX; ++q) Sx[q] *= r;
+          m = x;
+        }
+        const float pe = __expf(x - m);
 #pragma unroll
-          for (int q = 0; q < BMAX / 4; ++q) {
-            const float4 f = ph[q];
-            Sx[4 * q + 0] = fmaf(f.x, pe, Sx[4 * q + 0]);
-            Sx[4 * q + 1] = fmaf(f.y, pe, Sx[4 * q + 1]);
-            Sx[4 * q + 2] = fmaf(f.z, pe, Sx[4 * q + 2]);
-            Sx[4 * q + 3] = fmaf(f.w, pe, Sx[4 * q + 3]);
-          }
+        for (int q = 0; q < BMAX / 4; ++q) {
+          const float4 f = ph[q];
+          Sx[4 * q + 0] = fmaf(f.x, pe, Sx[4 * q + 0]);
+          Sx[4 * q + 1] = fmaf(f.y, pe, Sx[4 * q + 1]);
+          Sx[4 * q + 2] = fmaf(f.z, pe, Sx[4 * q + 2]);
+          Sx[4 * q + 3] = fmaf(f.w, pe, Sx[4 * q + 3]);
         }
       };
       long long tq_frames = 0, tq_keys = 0;
+      constexpr int kCh = 2;  // frames per prefetch chunk (register budget)
+      const int W4 = W & ~(kCh - 1);
       for (int c0 = 2 * tid; c0 < C; c0 += 2 * kNT) {
         const long long tq1 = clock64();
         const bool two = c0 + 1 < C;
         float S0[BMAX], S1[BMAX];
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) S0[q] = S1[q] = 0.f;
-        float m0 = -INFINITY, m1 = -INFINITY;
+        float m0 = gf, m1 = gf;
         const float r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
         const float r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
         const float* col = grid + (size_t)(s - 1) * V + c0;
-        auto ld = [&](int i, float& a, float& b) {
-          if (i >= W) {
-            a = b = -INFINITY;
-          } else if (vec2 && two) {
-            const float2 v = __ldg(reinterpret_cast<const float2*>(col + (size_t)i * V));
+        const int c1off = two ? 1 : 0;
+        auto ld = [&](const float* pp, float& a, float& b) {
+          if (vec2 && two) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(pp));
             a = v.x;
             b = v.y;
           } else {
-            a = __ldg(col + (size_t)i * V);
-            b = two ? __ldg(col + (size_t)i * V + 1) : -INFINITY;
+            a = __ldg(pp);
+            b = __ldg(pp + c1off);
           }
         };
-        float xa[4], xb[4];
+        const float4* phr = reinterpret_cast<const float4*>(PhiF);
+        const int phs = BMAX / 4;  // float4 per PhiF row
+        float xa[kCh], xb[kCh];
+        const float* pp = col;
+        if (W4 > 0) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) ld(k, xa[k], xb[k]);
-        for (int i0 = 0; i0 < W; i0 += 4) {
-          float ya[4], yb[4];
+          for (int k = 0; k < kCh; ++k) ld(pp + (size_t)k * V, xa[k], xb[k]);
+        }
+        for (int i0 = 0; i0 < W4; i0 += kCh) {
+          float ya[kCh], yb[kCh];
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
+          for (int k = 0; k < kCh; ++k) {
             ya[k] = xa[k];
             yb[k] = xb[k];
           }
+          pp += (size_t)kCh * V;
+          if (i0 + kCh < W4) {  // prefetch the next full chunk
 #pragma unroll
-          for (int k = 0; k < 4; ++k) ld(i0 + 4 + k, xa[k], xb[k]);  // prefetch
+            for (int k = 0; k < kCh; ++k) ld(pp + (size_t)k * V, xa[k], xb[k]);
+          }
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float4* ph = reinterpret_cast<const float4*>(PhiF + (size_t)(i0 + k) * BMAX);
-            acc(S0, m0, ya[k], ph);
-            acc(S1, m1, yb[k], ph);
+          for (int k = 0; k < kCh; ++k) {
+            acc(S0, m0, ya[k], phr + (i0 + k) * phs);
+            acc(S1, m1, yb[k], phr + (i0 + k) * phs);
           }
         }
+        for (int i = W4; i < W; ++i) {  // remainder frames
+          float a, b;
+          ld(col + (size_t)i * V, a, b);
+          acc(S0, m0, a, phr + i * phs);
+          acc(S1, m1, b, phr + i * phs);
+        }
+        if (!two) m1 = gf;
         const long long tq2 = clock64();
         tq_frames += tq2 - tq1;
-        // certified keys: joint(j, c) - off in [key - h, key + h]
+        // certified keys: joint(j, c) - off in [key - h, key + h]; parent-major
+        // so each parent's constants are read once for both columns
 #pragma unroll
-        for (int cc = 0; cc < 2; ++cc) {
-          const int c = c0 + cc;
-          if (cc == 1 && !two) break;
-          const float m = cc ? m1 : m0;
+        for (int q = 0; q < BMAX; ++q) {
+          if (q < nb) {
+            const int last = sh.b_last[cur][q];
+            const float kbq = sh.kb[q];
+            const bool mz = sh.mzero[q] != 0;
 #pragma unroll
-          for (int q = 0; q < BMAX; ++q) {
-            if (q < nb) {
+            for (int cc = 0; cc < 2; ++cc) {
+              const int c = c0 + cc;
+              if (cc == 1 && !two) break;
+              const float m = cc ? m1 : m0;
               const float Sq = cc ? S1[q] : S0[q];
               float klo = -INFINITY, kub_v = -INFINITY;
               bool under = false;
-              if (c != sh.b_last[cur][q]) {
+              if (c != last) {
                 const float r = row_same >= 0 ? (cc ? r1s : r0s)
                                               : P.sc_rowsf[(size_t)sh.b_row[cur][q] * V + c];
                 if (r == -INFINITY) {
                   klo = kub_v = kZeroKey;  // att is log-zero: joint exactly kLogZero
                 } else if (lam <= 0.0) {
-                  const float key = sh.kb[q] + r;
+                  const float key = kbq + r;
                   const float h = hw + fabsf(key) * 2.4e-7f;
                   klo = key - h;
                   kub_v = key + h;
-                } else if (sh.mzero[q] || m == -INFINITY) {
+                } else if (mz || m == gf) {
                   klo = kub_v = kZeroKey;  // psi exactly kLogZero
                 } else if (Sq >= 7.888609052210118e-31f) {  // 2^-100
-                  const float key = sh.kb[q] + lamf * (m + __logf(Sq)) + r;
+                  const float key = kbq + lamf * (m + __logf(Sq)) + r;
                   const float h = hw + fabsf(key) * 2.4e-7f;
                   klo = key - h;
                   kub_v = key + h;
                 } else {  // fp32 underflow: certified upper bound only
-                  const float key = sh.kb[q] + lamf * (m - 68.62157f) + r;
+                  const float key = kbq + lamf * (m - 68.62157f) + r;
                   klo = -INFINITY;
                   kub_v = key + hw + fabsf(key) * 2.4e-7f;
                   under = true;
