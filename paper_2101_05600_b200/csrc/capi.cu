@@ -211,6 +211,8 @@ struct bl_decoder {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // H2D of grid chunks, overlapped with decoding
+  cudaStream_t alt = nullptr;   // second compute stream: chunk kernels overlap at their tails
+  cudaEvent_t ev_alt = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaEvent_t> ev_copy;
   // device scorer
@@ -494,7 +496,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
                      cudaMemcpyHostToDevice, st));
   // chunking: one launch when grids are resident; otherwise ~600 utterances
   // (two waves of resident CTAs) per chunk so copies overlap decoding
-  const int nchunk = on_device ? 1 : std::max(1, std::min(8, U / 600));
+  const int nchunk = on_device ? 1 : std::max(1, std::min(16, U / 360));
   if ((int)d->ev_copy.size() < nchunk) {
     for (int k = (int)d->ev_copy.size(); k < nchunk; ++k) {
       cudaEvent_t e;
@@ -502,8 +504,9 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       d->ev_copy.push_back(e);
     }
   }
-  if (!on_device) CK(cudaEventRecord(d->ev0, st));  // copies start after the descriptors
+  CK(cudaEventRecord(d->ev0, st));  // timing start; copies start after the descriptors
   if (!on_device) CK(cudaStreamWaitEvent(d->copy, d->ev0, 0));
+  if (nchunk > 1) CK(cudaStreamWaitEvent(d->alt, d->ev0, 0));
   int launches = 0;
   for (int k = 0; k < nchunk; ++k) {
     const int a = (int)((long long)U * k / nchunk), b = (int)((long long)U * (k + 1) / nchunk);
@@ -518,14 +521,18 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
         res->h2d += sizeof(float) * len;
       }
       CK(cudaEventRecord(d->ev_copy[k], d->copy));
-      CK(cudaStreamWaitEvent(st, d->ev_copy[k], 0));
     }
-    if (k == 0) CK(cudaEventRecord(d->ev0, st));
+    cudaStream_t cs = (k & 1) ? d->alt : st;
+    if (!on_device) CK(cudaStreamWaitEvent(cs, d->ev_copy[k], 0));
     bl::KParams pk = p;
     pk.u0 = a;
     pk.U = b - a;
-    CK(bl::launch_decode(pk, st));
+    CK(bl::launch_decode(pk, cs));
     ++launches;
+  }
+  if (nchunk > 1) {
+    CK(cudaEventRecord(d->ev_alt, d->alt));
+    CK(cudaStreamWaitEvent(st, d->ev_alt, 0));
   }
   CK(cudaEventRecord(d->ev1, st));
   CK(cudaMemcpyAsync(d->h_res.p, d->res.p, sizeof(int) * (size_t)U * rs,
@@ -740,6 +747,8 @@ int bl_decoder_create(int device, const bl_config* cfg, const bl_scorer* scorer,
     d->num_tokens = scorer->num_tokens;
     CK(cudaStreamCreateWithFlags(&d->own, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&d->copy, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&d->alt, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&d->ev_alt, cudaEventDisableTiming));
     d->stream = d->own;
     CK(cudaEventCreate(&d->ev0));
     CK(cudaEventCreate(&d->ev1));
@@ -773,6 +782,8 @@ void bl_decoder_destroy(bl_decoder* d) {
   if (d->ev1) cudaEventDestroy(d->ev1);
   for (auto e : d->ev_copy) cudaEventDestroy(e);
   if (d->copy) cudaStreamDestroy(d->copy);
+  if (d->alt) cudaStreamDestroy(d->alt);
+  if (d->ev_alt) cudaEventDestroy(d->ev_alt);
   if (d->own) cudaStreamDestroy(d->own);
   delete d;
 }

@@ -359,21 +359,27 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const
     double* gn0 = gam_ptr(P, u, 0, 0, 0);
     for (int t = tid; t <= T; t += kNT) gn0[t] = kLogZero;
   }
+  // the blank column, staged once so the two serial scans below read shared
+  // memory instead of chasing T dependent global loads
+  float* bcol = reinterpret_cast<float*>(region);                       // [T]
+  double* Gs = reinterpret_cast<double*>(region + align16(sizeof(float) * (size_t)T));  // [T+1]
+  for (int t = tid; t < T; t += kNT) bcol[t] = grid[(size_t)t * V + blank];
+  __syncthreads();
   if (tid == 0) {
     // init_state, ctc_prefix.cpp:10-26 (sequential: exact reference order)
     double* gb0 = gam_ptr(P, u, 0, 0, 1);
     double acc = 0.0;
     gb0[0] = acc;
     for (int t = 1; t <= T; ++t) {
-      acc = log_mul(acc, (double)grid[(size_t)(t - 1) * V + blank]);
+      acc = log_mul(acc, (double)bcol[t - 1]);
       gb0[t] = acc;
     }
     if (ud.need_tail) {  // G[k] = blank mass of frames k+1..T
       double g = 0.0;
-      Gt[T] = g;
+      Gs[T] = g;
       for (int k = T - 1; k >= 0; --k) {
-        g = log_mul((double)grid[(size_t)k * V + blank], g);
-        Gt[k] = g;
+        g = log_mul((double)bcol[k], g);
+        Gs[k] = g;
       }
     }
     sh.nb = 1;
@@ -401,11 +407,12 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const
   if (ud.need_tail) {
     // F[k][c]: label c held from frame k to some k' then blank to T
     // (the eos tail of ctc_prefix.cpp:88-104 in closed form).
+    for (int t = tid; t <= T; t += kNT) Gt[t] = Gs[t];
     for (int c = tid; c < C; c += kNT) {
       double f = 0.0;
       Ft[(size_t)T * C + c] = f;
       for (int k = T - 1; k >= 0; --k) {
-        f = log_add(log_mul((double)grid[(size_t)k * V + c], f), Gt[k], tb);
+        f = log_add(log_mul((double)grid[(size_t)k * V + c], f), Gs[k], tb);
         Ft[(size_t)k * C + c] = f;
       }
     }
@@ -713,11 +720,11 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const
       // list; the exact theta (B-th largest lower bound) is ranked inside it
       // and the contenders are the list entries that reach max(theta, theta0).
       const float theta0 = sh.theta;
-      for (int c = tid; c < C; c += kNT) {
-        for (int q = 0; q < nb; ++q) {
-          const int kidx = q * C + c;
-          const float ku = kub[kidx];
-          if (ku >= theta0 && c != sh.b_last[cur][q]) {
+      for (int kidx = tid; kidx < nb * C; kidx += kNT) {
+        const float ku = kub[kidx];
+        if (ku >= theta0) {
+          const int q = kidx / C, c = kidx - q * C;
+          if (c != sh.b_last[cur][q]) {
             const int idx = atomicAdd(&sh.n_list, 1);
             if (idx < kListCap) {
               const bool under = (ubits[kidx >> 5] >> (kidx & 31)) & 1u;
