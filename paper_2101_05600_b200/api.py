@@ -20,7 +20,7 @@ from typing import Dict, Iterable, List, Optional, Sequence, Tuple
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libbl_b200.so")
+LIB_PATH = os.environ.get("BL_LIB", os.path.join(_HERE, "libbl_b200.so"))
 
 NO_MARGIN = 1 << 29  # kNoMargin, ctc_prefix.hpp:12
 K_LOG_ZERO = -1e30   # logmath.hpp:11

@@ -374,15 +374,31 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   d->Gtab.ensure(sizeof(double) * (size_t)U * Tp);
   d->Ftab.ensure(tail ? sizeof(double) * (size_t)U * Tp * C : 8);
   const int bmax = bl::bmax_for(B);
+  // TMA streaming of the K1 slab for large vocabularies: needs every grid in
+  // one dense row-major buffer (always true for host input; checked for
+  // device pointers) with 16-byte rows.
+  const float* gbase = nullptr;
+  bool use_tma = V >= 1024 && V % 4 == 0 && std::getenv("BL_NO_TMA") == nullptr;
+  if (use_tma) {
+    if (!on_device) {
+      d->grid.ensure(sizeof(float) * gtotal);
+      gbase = static_cast<const float*>(d->grid.p);
+    } else {
+      gbase = utts[0].logp;
+      for (int i = 0; i < n && use_tma; ++i) use_tma = utts[i].logp == gbase + goff[i];
+    }
+    use_tma = use_tma && (reinterpret_cast<uintptr_t>(gbase) & 15) == 0;
+  }
+  const int tma_stages = use_tma ? (U <= 148 ? bl::kTmaStagesMax : 4) : 0;
   // shared-memory plan: the aliased region (P3-P5 keys, P6 staging) is sized
   // so the whole plan fits 3 CTAs/SM (~71 KB) when the fixed parts allow it;
   // the upper keys move to HBM when they do not fit.
   const size_t fixed = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).total;
   const size_t budget = 66 * 1024;  // + static smem + 1 KB reserve: 3 CTAs in 228 KB
   const size_t need1 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 1).region_need;
-  const size_t need0 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).region_need;
+  const size_t need0 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0, tma_stages).region_need;
   size_t region = fixed + need1 <= budget ? budget - fixed : std::max(need0, budget > fixed ? budget - fixed : 0);
-  const int kub_smem = need1 <= region ? 1 : 0;
+  const int kub_smem = (!use_tma && need1 <= region) ? 1 : 0;
   region = (std::max(region, kub_smem ? need1 : need0) + 15) & ~(size_t)15;
   if (!kub_smem) {
     d->kubg.ensure(sizeof(float) * (size_t)U * B * C);
@@ -468,6 +484,34 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.ubitsg = static_cast<unsigned*>(d->ubitsg.p);
   p.kub_smem = kub_smem;
   p.region_bytes = (int)region;
+  p.use_tma = use_tma ? 1 : 0;
+  p.tma_stages = tma_stages;
+  if (use_tma) {
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn encode = nullptr;
+    if (!encode) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+      if (!fn || q != cudaDriverEntryPointSuccess)
+        throw BlError{BL_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
+      encode = reinterpret_cast<EncodeFn>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)V, (cuuint64_t)(gtotal / V)};
+    const cuuint64_t strides[1] = {(cuuint64_t)V * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)bl::kTmaBoxCols, (cuuint32_t)bl::kTmaRows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                              const_cast<float*>(gbase), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+      throw BlError{BL_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
+  }
   p.sc_rowsf = static_cast<const float*>(d->sc_rowsf.p);
   p.xs = static_cast<double*>(d->xs.p);
   p.taken = static_cast<unsigned char*>(d->taken.p);
@@ -485,9 +529,11 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     p.prof = static_cast<long long*>(d->prof.p);
   }
 
-  for (int i = 0; i < n; ++i)
+  for (int i = 0; i < n; ++i) {
     desc[i].grid = on_device ? utts[i].logp
                              : static_cast<const float*>(d->grid.p) + goff[i];
+    desc[i].row0 = (int)(goff[i] / V);
+  }
   std::memcpy(d->h_utts.p, desc.data(), sizeof(bl::UttDesc) * U);
   if (bl::decode_smem_bytes(p) > 227 * 1024)
     throw std::invalid_argument("utterance too long for the device decoder's shared memory plan");

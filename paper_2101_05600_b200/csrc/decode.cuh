@@ -1,6 +1,7 @@
 // decode.cuh — device data layout shared by the decode kernel and the host
 // planner (capi.cu). See DESIGN.md "Data layout in HBM".
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -17,7 +18,7 @@ struct UttDesc {
   int T;
   int max_steps;      // ceil(max_steps_ratio * T), batched.cpp:112-113
   int need_tail;      // margin_m2 < T: eos tails need the F/G tables
-  int pad;
+  int row0;           // first row of this utterance in the TMA tensor map
 };
 
 // Finished (eos-ended) entry, FinishedEntry (beam_search.hpp:53-61) with a
@@ -39,7 +40,16 @@ struct HistRec {
   int pad;
 };
 
+// TMA streaming of the CTC window slab (large vocabularies): 512-column tiles
+// (two columns per thread) x kTmaRows-row chunks, kTmaStagesMax stages.
+constexpr int kTmaBoxCols = 256;
+constexpr int kTmaRows = 8;
+constexpr int kTmaStagesMax = 6;
+constexpr int kTmaStageBytes = 2 * kTmaRows * kTmaBoxCols * 4;
+
 struct KParams {
+  CUtensorMap tmap;  // 2D map over all utterances' grid rows [sum T][V] (fp32)
+  int use_tma, tma_stages;
   const UttDesc* utts;
   int U, V, C, B;
   int u0;          // first utterance of this launch (chunked launches)
@@ -87,7 +97,7 @@ constexpr int kListCap = 256;  // keys reaching theta0 (P5), 16 B each
 
 struct SmemPlan {
   size_t phi, region, items, bbl, total;
-  size_t phif, kub, ubits, clist, region_need;  // P3-P5 view of `region`
+  size_t phif, kub, ubits, clist, stages, region_need;  // P3-P5 view of `region`
 };
 constexpr int kItemBytes = 24;  // score(double) + parent, token, tau, taut
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -95,7 +105,8 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t
 // underflow flags, theta0 list; P6: contender staging with stride W). The
 // host sizes it so the whole plan fits 3 CTAs per SM when possible.
 __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, int caps,
-                                              int S, size_t region_bytes, int kub_smem) {
+                                              int S, size_t region_bytes, int kub_smem,
+                                              int tma_stages = 0) {
   SmemPlan p;
   p.phi = 0;
   p.region = align16(p.phi + sizeof(double) * (size_t)B * Tmax);
@@ -104,7 +115,11 @@ __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, 
   const size_t words = ((size_t)B * C + 31) / 32;
   p.ubits = kub_smem ? align16(p.kub + sizeof(float) * (size_t)B * C) : p.kub;
   p.clist = kub_smem ? align16(p.ubits + sizeof(unsigned) * words) : p.kub;
-  p.region_need = p.clist + 16 * (size_t)kListCap;
+  // TMA stages (kub/ubits then live in HBM): after the list, 128-byte
+  // aligned in absolute shared-memory offset (cp.async.bulk.tensor dst)
+  p.stages = ((p.region + p.clist + 16 * (size_t)kListCap + 127) & ~(size_t)127) - p.region;
+  p.region_need = tma_stages ? p.stages + (size_t)tma_stages * kTmaStageBytes
+                             : p.clist + 16 * (size_t)kListCap;
   p.items = align16(p.region + region_bytes);
   p.bbl = align16(p.items + (size_t)kItemBytes * (caps + bmax));
   p.total = align16(p.bbl + sizeof(double) * (size_t)(S + 2));

@@ -25,6 +25,8 @@
 // arg-max selection — slower, same results.
 #include <cfloat>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 
 #include "decode.cuh"
 #include "softplus.cuh"
@@ -94,6 +96,37 @@ __device__ __forceinline__ float warp_max_f(float v) {
 }
 
 constexpr float kZeroKey = -3.0e38f;  // key of a joint that is exactly kLogZero
+
+// ------------------------------------------------------- TMA / mbarrier PTX
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
 
 struct SelE {
   double score;
@@ -315,11 +348,13 @@ __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
     prof_t = _now;                                     \
   }
 
-template <int BMAX>
-__global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const KParams P) {
-  extern __shared__ __align__(16) unsigned char dsm[];
+template <int BMAX, bool kTma>
+__global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
+    decode_kernel(const __grid_constant__ KParams P) {
+  extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ Shared<BMAX> sh;
   __shared__ SpTables tb;
+  __shared__ __align__(8) unsigned long long mbar[kTmaStagesMax];
 
   const int u = blockIdx.x + P.u0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -352,6 +387,11 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const
   double* Gt = P.Gtab + (size_t)u * P.Tp;
 
   // ---------------------------------------------------------------- init
+  unsigned tma_jobs = 0;  // TMA jobs issued so far (stage = job % stages, parity = job / stages)
+  if (kTma && tid == 0) {
+    for (int k = 0; k < P.tma_stages; ++k) mbar_init(&mbar[k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int i = tid; i < 320; i += kNT)
     reinterpret_cast<double*>(&tb)[i] = reinterpret_cast<const double*>(&c_sptab)[i];
   for (int i = tid; i <= P.S + 1; i += kNT) best_by_len[i] = -HUGE_VAL;
@@ -560,64 +600,12 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const
       long long tq_frames = 0, tq_keys = 0;
       constexpr int kCh = 2;  // frames per prefetch chunk (register budget)
       const int W4 = W & ~(kCh - 1);
-      for (int c0 = 2 * tid; c0 < C; c0 += 2 * kNT) {
-        const long long tq1 = clock64();
-        const bool two = c0 + 1 < C;
-        float S0[BMAX], S1[BMAX];
-#pragma unroll
-        for (int q = 0; q < BMAX; ++q) S0[q] = S1[q] = 0.f;
-        float m0 = gf, m1 = gf;
-        const float r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
-        const float r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
-        const float* col = grid + (size_t)(s - 1) * V + c0;
-        const int c1off = two ? 1 : 0;
-        auto ld = [&](const float* pp, float& a, float& b) {
-          if (vec2 && two) {
-            const float2 v = __ldg(reinterpret_cast<const float2*>(pp));
-            a = v.x;
-            b = v.y;
-          } else {
-            a = __ldg(pp);
-            b = __ldg(pp + c1off);
-          }
-        };
-        const float4* phr = reinterpret_cast<const float4*>(PhiF);
-        const int phs = BMAX / 4;  // float4 per PhiF row
-        float xa[kCh], xb[kCh];
-        const float* pp = col;
-        if (W4 > 0) {
-#pragma unroll
-          for (int k = 0; k < kCh; ++k) ld(pp + (size_t)k * V, xa[k], xb[k]);
-        }
-        for (int i0 = 0; i0 < W4; i0 += kCh) {
-          float ya[kCh], yb[kCh];
-#pragma unroll
-          for (int k = 0; k < kCh; ++k) {
-            ya[k] = xa[k];
-            yb[k] = xb[k];
-          }
-          pp += (size_t)kCh * V;
-          if (i0 + kCh < W4) {  // prefetch the next full chunk
-#pragma unroll
-            for (int k = 0; k < kCh; ++k) ld(pp + (size_t)k * V, xa[k], xb[k]);
-          }
-#pragma unroll
-          for (int k = 0; k < kCh; ++k) {
-            acc(S0, m0, ya[k], phr + (i0 + k) * phs);
-            acc(S1, m1, yb[k], phr + (i0 + k) * phs);
-          }
-        }
-        for (int i = W4; i < W; ++i) {  // remainder frames
-          float a, b;
-          ld(col + (size_t)i * V, a, b);
-          acc(S0, m0, a, phr + i * phs);
-          acc(S1, m1, b, phr + i * phs);
-        }
-        if (!two) m1 = gf;
-        const long long tq2 = clock64();
-        tq_frames += tq2 - tq1;
-        // certified keys: joint(j, c) - off in [key - h, key + h]; parent-major
-        // so each parent's constants are read once for both columns
+      // certified keys: joint(j, c) - off in [key - h, key + h]; parent-major
+      // so each parent's constants are read once for both columns
+      const float4* phr = reinterpret_cast<const float4*>(PhiF);
+      const int phs = BMAX / 4;  // float4 per PhiF row
+      auto emit_keys = [&](int c0, bool two, const float(&S0)[BMAX], const float(&S1)[BMAX],
+                           float m0, float m1, float r0s, float r1s) {
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) {
           if (q < nb) {
@@ -670,7 +658,124 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 ? 3 : 2)) decode_kernel(const
             }
           }
         }
+      };
+      if constexpr (kTma) {
+        // K1 slab streamed by TMA: job j = (512-column tile, kTmaRows-row
+        // chunk); thread 0 keeps tma_stages jobs in flight on mbarriers, all
+        // threads consume each chunk from shared memory.
+        const int nch = (W + kTmaRows - 1) / kTmaRows;
+        const int ntile = (C + 2 * kNT - 1) / (2 * kNT);
+        const int J = ntile * nch;
+        const int NST = P.tma_stages;
+        float* stages = reinterpret_cast<float*>(region + pl.stages);
+        const int urow = ud.row0 + s - 1;
+        auto issue = [&](int j, unsigned g) {
+          const int st = (int)(g % (unsigned)NST);
+          const int tile = j / nch, k = j - tile * nch;
+          float* dst = stages + (size_t)st * (kTmaStageBytes / 4);
+          mbar_expect_tx(&mbar[st], kTmaStageBytes);
+          tma_load_2d(dst, &P.tmap, tile * 2 * kNT, urow + k * kTmaRows, &mbar[st]);
+          tma_load_2d(dst + kTmaRows * kTmaBoxCols, &P.tmap, tile * 2 * kNT + kTmaBoxCols,
+                      urow + k * kTmaRows, &mbar[st]);
+        };
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          for (int j = 0; j < NST && j < J; ++j) issue(j, tma_jobs + j);
+        }
+        float S0[BMAX], S1[BMAX];
+        float m0 = gf, m1 = gf, r0s = 0.f, r1s = 0.f;
+        const int colb = ((2 * tid) >= kTmaBoxCols ? kTmaRows * kTmaBoxCols : 0) +
+                         ((2 * tid) & (kTmaBoxCols - 1));
+        for (int j = 0; j < J; ++j) {
+          const unsigned g = tma_jobs + j;
+          const int st = (int)(g % (unsigned)NST);
+          const int tile = j / nch, k = j - tile * nch;
+          const int c0 = tile * 2 * kNT + 2 * tid;
+          const bool active = c0 < C, two = c0 + 1 < C;
+          if (k == 0) {
+#pragma unroll
+            for (int q = 0; q < BMAX; ++q) S0[q] = S1[q] = 0.f;
+            m0 = m1 = gf;
+            r0s = (row_same >= 0 && active) ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
+            r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
+          }
+          mbar_wait(&mbar[st], (g / (unsigned)NST) & 1u);
+          if (active) {
+            const float* sb = stages + (size_t)st * (kTmaStageBytes / 4) + colb;
+            const int nrow = min(kTmaRows, W - k * kTmaRows);
+            const int f0 = k * kTmaRows;
+            for (int i = 0; i < nrow; ++i) {
+              const float2 v = *reinterpret_cast<const float2*>(sb + i * kTmaBoxCols);
+              acc(S0, m0, v.x, phr + (f0 + i) * phs);
+              acc(S1, m1, v.y, phr + (f0 + i) * phs);
+            }
+            if (k == nch - 1) emit_keys(c0, two, S0, S1, m0, two ? m1 : gf, r0s, r1s);
+          }
+          __syncthreads();  // stage consumed by every thread
+          if (tid == 0 && j + NST < J) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(j + NST, g + NST);
+          }
+        }
+        tma_jobs += J;
+      } else {
+      for (int c0 = 2 * tid; c0 < C; c0 += 2 * kNT) {
+        const long long tq1 = clock64();
+        const bool two = c0 + 1 < C;
+        float S0[BMAX], S1[BMAX];
+#pragma unroll
+        for (int q = 0; q < BMAX; ++q) S0[q] = S1[q] = 0.f;
+        float m0 = gf, m1 = gf;
+        const float r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
+        const float r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
+        const float* col = grid + (size_t)(s - 1) * V + c0;
+        const int c1off = two ? 1 : 0;
+        auto ld = [&](const float* pp, float& a, float& b) {
+          if (vec2 && two) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(pp));
+            a = v.x;
+            b = v.y;
+          } else {
+            a = __ldg(pp);
+            b = __ldg(pp + c1off);
+          }
+        };
+        float xa[kCh], xb[kCh];
+        const float* pp = col;
+        if (W4 > 0) {
+#pragma unroll
+          for (int k = 0; k < kCh; ++k) ld(pp + (size_t)k * V, xa[k], xb[k]);
+        }
+        for (int i0 = 0; i0 < W4; i0 += kCh) {
+          float ya[kCh], yb[kCh];
+#pragma unroll
+          for (int k = 0; k < kCh; ++k) {
+            ya[k] = xa[k];
+            yb[k] = xb[k];
+          }
+          pp += (size_t)kCh * V;
+          if (i0 + kCh < W4) {  // prefetch the next full chunk
+#pragma unroll
+            for (int k = 0; k < kCh; ++k) ld(pp + (size_t)k * V, xa[k], xb[k]);
+          }
+#pragma unroll
+          for (int k = 0; k < kCh; ++k) {
+            acc(S0, m0, ya[k], phr + (i0 + k) * phs);
+            acc(S1, m1, yb[k], phr + (i0 + k) * phs);
+          }
+        }
+        for (int i = W4; i < W; ++i) {  // remainder frames
+          float a, b;
+          ld(col + (size_t)i * V, a, b);
+          acc(S0, m0, a, phr + i * phs);
+          acc(S1, m1, b, phr + i * phs);
+        }
+        if (!two) m1 = gf;
+        const long long tq2 = clock64();
+        tq_frames += tq2 - tq1;
+        emit_keys(c0, two, S0, S1, m0, m1, r0s, r1s);
         tq_keys += clock64() - tq2;
+      }
       }
       if (P.prof && tid == 0) {
         P.prof[(size_t)u * 16 + 12] += tq_frames;
@@ -1245,18 +1350,32 @@ int bmax_for(int B) {
 }
 
 size_t decode_smem_bytes(const KParams& p) {
-  return smem_plan(p.Tmax, p.B, bmax_for(p.B), p.C, p.caps, p.S, p.region_bytes, p.kub_smem).total;
+  return smem_plan(p.Tmax, p.B, bmax_for(p.B), p.C, p.caps, p.S, p.region_bytes, p.kub_smem,
+                   p.tma_stages).total;
+}
+
+template <int BMAX, bool kTma>
+static cudaError_t launch_v(const KParams& p, cudaStream_t st) {
+  const size_t sm = decode_smem_bytes(p);
+  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX, kTma>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+  if (err != cudaSuccess) return err;
+  if (std::getenv("BL_DEBUG")) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decode_kernel<BMAX, kTma>, kNT, sm);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, decode_kernel<BMAX, kTma>);
+    std::fprintf(stderr, "[bl] decode_kernel<%d,%d>: grid %d, dyn smem %zu, static %zu, regs %d, %d CTA/SM\n",
+                 BMAX, (int)kTma, p.U, sm, fa.sharedSizeBytes, fa.numRegs, nb);
+  }
+  decode_kernel<BMAX, kTma><<<p.U, kNT, sm, st>>>(p);
+  return cudaGetLastError();
 }
 
 template <int BMAX>
 static cudaError_t launch_t(const KParams& p, cudaStream_t st) {
-  const size_t sm = decode_smem_bytes(p);
-  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
-  if (err != cudaSuccess) return err;
-  decode_kernel<BMAX><<<p.U, kNT, sm, st>>>(p);
-  return cudaGetLastError();
+  return p.use_tma ? launch_v<BMAX, true>(p, st) : launch_v<BMAX, false>(p, st);
 }
 
 cudaError_t launch_decode(const KParams& p, cudaStream_t st) {
