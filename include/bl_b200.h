@@ -161,6 +161,59 @@ int bl_results_transfer(const bl_results* r, uint64_t* h2d, uint64_t* d2h);
 int bl_results_profile(const bl_results* r, double* out16);
 void bl_results_destroy(bl_results* r);
 
+/* ------------------------------------------------------------------------
+ * CTC encoder forward (SURVEY.md §8 a'1, the producer of the PosteriorGrid).
+ * The reference takes grids from files (`read_grid`, grid.cpp:108-127); this
+ * encoder writes them straight into device memory for bl_decode
+ * (grids_on_device = 1). ESPnet-style Transformer encoder, eval mode:
+ * Conv2dSubsampling(1->d->d, 3x3 stride 2, ReLU), linear(d*F2 -> d),
+ * x*sqrt(d) + sinusoidal PE, `layers` x pre-LN [MHA, FFN(ReLU)] with
+ * residuals, final LayerNorm (eps 1e-12), CTC linear(d -> vocab),
+ * log_softmax. bf16 tensor-core GEMMs (tcgen05) with fp32 accumulation.
+ *
+ * Weights: one flat fp32 array in torch layouts, in this order:
+ *   conv1.w[d][1][3][3] conv1.b[d] conv2.w[d][d][3][3] conv2.b[d]
+ *   out.w[d][d*F2] out.b[d]        (F2 = frames_out(idim), input index c*F2+f)
+ *   per layer: ln1.g[d] ln1.b[d] wq[d][d] bq[d] wk[d][d] bk[d] wv[d][d] bv[d]
+ *              wo[d][d] bo[d] ln2.g[d] ln2.b[d] w1[dff][d] b1[dff]
+ *              w2[d][dff] b2[d]
+ *   after_norm.g[d] after_norm.b[d] ctc.w[vocab][d] ctc.b[vocab]
+ * ---------------------------------------------------------------------- */
+typedef struct bl_encoder_spec {
+  int idim;    /* fbank features per frame (80) */
+  int d_model; /* multiple of 64, <= 1024 */
+  int heads;   /* d_model / 64 */
+  int d_ff;
+  int layers;
+  int vocab;   /* CTC width |C|+1, multiple of 4 */
+} bl_encoder_spec;
+typedef struct bl_encoder bl_encoder;
+
+/* Encoder frames for `frames_in` fbank frames (1000 -> 249); 0 if < 7. */
+int bl_encoder_frames_out(int frames_in);
+size_t bl_encoder_num_weights(const bl_encoder_spec* spec);
+int bl_encoder_create(int device, const bl_encoder_spec* spec, const float* weights,
+                      size_t n_weights, bl_encoder** out);
+int bl_encoder_set_stream(bl_encoder* e, void* stream);
+/* Segments processed per internal chunk (workspace ~ chunk x 50 MB at d=512). */
+int bl_encoder_set_chunk(bl_encoder* e, int segments);
+/* n equal-length segments, fbank [n][frames_in][idim] fp32 (host or device),
+ * grid [n][frames_out][vocab] fp32 DEVICE memory. Enqueued on the encoder's
+ * stream; returns after enqueue unless `sync` is non-zero. */
+int bl_encoder_forward(bl_encoder* e, int n, int frames_in, const float* fbank,
+                       int fbank_on_device, float* grid, int sync);
+/* Kernels launched by the last forward. */
+int bl_encoder_launches(const bl_encoder* e);
+void bl_encoder_destroy(bl_encoder* e);
+
+/* Tensor-core GEMM used by the encoder, exported for tests/benchmarks:
+ * C[M,N] = A[M,K] . B[N,K]^T, A/B bf16 device pointers (K-major, strides in
+ * elements, multiples of 8); epilogue mode 0 plain, 1 ReLU, 2 residual
+ * (out_f32 += ...), 3 scale + positional table (scale, pe[pe_rows][N]). */
+int bl_gemm_bf16(int M, int N, int K, const void* A, int lda, const void* B, int ldb,
+                 int mode, const float* bias, float* out_f32, void* out_bf16, int ldo,
+                 float scale, const float* pe, int pe_rows, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -104,6 +104,17 @@ def lib() -> C.CDLL:
     L.bl_results_export.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p]
     L.bl_results_destroy.argtypes = [vp]
+    L.bl_encoder_frames_out.argtypes = [C.c_int]
+    L.bl_encoder_num_weights.argtypes = [vp]
+    L.bl_encoder_num_weights.restype = C.c_size_t
+    L.bl_encoder_create.argtypes = [C.c_int, vp, vp, C.c_size_t, C.POINTER(vp)]
+    L.bl_encoder_set_stream.argtypes = [vp, vp]
+    L.bl_encoder_set_chunk.argtypes = [vp, C.c_int]
+    L.bl_encoder_forward.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int]
+    L.bl_encoder_launches.argtypes = [vp]
+    L.bl_encoder_destroy.argtypes = [vp]
+    L.bl_gemm_bf16.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int,
+                               vp, vp, vp, C.c_int, C.c_float, vp, C.c_int, vp]
     _lib = L
     return L
 

@@ -21,6 +21,8 @@
 
 #include "../../include/bl_b200.h"
 #include "decode.cuh"
+#include "encoder.cuh"
+#include "gemm.cuh"
 
 namespace bl {
 cudaError_t launch_decode(const KParams& p, cudaStream_t st);
@@ -919,5 +921,113 @@ int bl_results_profile(const bl_results* r, double* out16) {
 }
 
 void bl_results_destroy(bl_results* r) { delete r; }
+
+
+// ------------------------------------------------------------------ encoder
+struct bl_encoder {
+  int device = 0;
+  bl::EncoderImpl* impl = nullptr;
+  cudaStream_t own = nullptr;
+  int chunk = 64;
+  int launches = 0;
+};
+
+static bl::EncSpec enc_spec(const bl_encoder_spec* s) {
+  return bl::EncSpec{s->idim, s->d_model, s->heads, s->d_ff, s->layers, s->vocab};
+}
+
+int bl_encoder_frames_out(int frames_in) { return bl::enc_frames_out(frames_in); }
+
+size_t bl_encoder_num_weights(const bl_encoder_spec* spec) {
+  if (!spec || !bl::enc_validate(enc_spec(spec)).empty()) return 0;
+  return bl::enc_num_weights(enc_spec(spec));
+}
+
+int bl_encoder_create(int device, const bl_encoder_spec* spec, const float* weights,
+                      size_t n_weights, bl_encoder** out) {
+  return guarded([&] {
+    if (!spec || !weights || !out) throw std::invalid_argument("null argument");
+    const bl::EncSpec s = enc_spec(spec);
+    const std::string why = bl::enc_validate(s);
+    if (!why.empty()) throw std::invalid_argument(why);
+    if (n_weights != bl::enc_num_weights(s))
+      throw std::invalid_argument("encoder weight count mismatch: expected " +
+                                  std::to_string(bl::enc_num_weights(s)) + ", got " +
+                                  std::to_string(n_weights));
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+      throw BlError{BL_CUDA_ERROR, "no CUDA device " + std::to_string(device)};
+    CK(cudaSetDevice(device));
+    std::unique_ptr<bl_encoder> e(new bl_encoder);
+    e->device = device;
+    CK(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
+    CK(bl::enc_create(s, weights, &e->impl));
+    bl::enc_set_stream(e->impl, e->own);
+    *out = e.release();
+    return BL_OK;
+  });
+}
+
+int bl_encoder_set_stream(bl_encoder* e, void* stream) {
+  bl::enc_set_stream(e->impl, stream ? static_cast<cudaStream_t>(stream) : e->own);
+  return BL_OK;
+}
+
+int bl_encoder_set_chunk(bl_encoder* e, int segments) {
+  if (segments < 1) return fail(BL_INVALID_ARGUMENT, "chunk must be >= 1");
+  e->chunk = segments;
+  return BL_OK;
+}
+
+int bl_encoder_forward(bl_encoder* e, int n, int frames_in, const float* fbank,
+                       int fbank_on_device, float* grid, int sync) {
+  return guarded([&] {
+    if (n < 0) throw std::invalid_argument("segment count must be >= 0");
+    if (n == 0) return BL_OK;
+    if (!fbank || !grid) throw std::invalid_argument("null fbank or grid");
+    if (bl::enc_frames_out(frames_in) < 1)
+      throw std::invalid_argument("segment too short: " + std::to_string(frames_in) +
+                                  " frames (need >= 7)");
+    CK(cudaSetDevice(e->device));
+    CK(bl::enc_forward(e->impl, n, frames_in, fbank, fbank_on_device != 0, grid, e->chunk,
+                       &e->launches));
+    if (sync) CK(cudaStreamSynchronize(bl::enc_stream(e->impl)));
+    return BL_OK;
+  });
+}
+
+int bl_encoder_launches(const bl_encoder* e) { return e->launches; }
+
+void bl_encoder_destroy(bl_encoder* e) {
+  if (!e) return;
+  cudaSetDevice(e->device);
+  cudaStreamSynchronize(bl::enc_stream(e->impl));
+  bl::enc_destroy(e->impl);
+  if (e->own) cudaStreamDestroy(e->own);
+  delete e;
+}
+
+int bl_gemm_bf16(int M, int N, int K, const void* A, int lda, const void* B, int ldb, int mode,
+                 const float* bias, float* out_f32, void* out_bf16, int ldo, float scale,
+                 const float* pe, int pe_rows, void* stream) {
+  return guarded([&] {
+    if (M < 1 || N < 1 || K < 8 || K % 8 || lda % 8 || ldb % 8 || lda < K || ldb < K)
+      throw std::invalid_argument("gemm: bad shape or stride");
+    if (mode < 0 || mode > 3) throw std::invalid_argument("gemm: bad epilogue mode");
+    if (!out_f32 && !out_bf16) throw std::invalid_argument("gemm: no output");
+    if ((mode == 2 && !out_f32) || (mode == 3 && (!pe || pe_rows < 1)))
+      throw std::invalid_argument("gemm: epilogue operand missing");
+    bl::GemmDesc g;
+    g.M = M; g.N = N; g.K = K;
+    g.A = static_cast<const __nv_bfloat16*>(A); g.lda = lda;
+    g.B = static_cast<const __nv_bfloat16*>(B); g.ldb = ldb;
+    g.mode = mode; g.bias = bias; g.out_f32 = out_f32;
+    g.out_bf16 = static_cast<__nv_bfloat16*>(out_bf16); g.ldo = ldo;
+    g.scale = scale; g.pe = pe; g.pe_rows = pe_rows;
+    CK(bl::gemm_bf16(g, static_cast<cudaStream_t>(stream)));
+    return BL_OK;
+  });
+}
 
 }  // extern "C"

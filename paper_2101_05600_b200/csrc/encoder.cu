@@ -1,0 +1,566 @@
+// encoder.cu — the CTC encoder forward (SURVEY §8 a'1) that produces the
+// PosteriorGrid the decoder consumes, written straight into device memory.
+//
+// Model (ESPnet Transformer encoder, pre-LN, eval mode):
+//   Conv2dSubsampling: conv1(1->d,3x3/2)+ReLU, conv2(d->d,3x3/2)+ReLU,
+//   linear(d*F2 -> d), x*sqrt(d) + PE;  L x [LN, MHA, +res, LN, FFN(ReLU), +res];
+//   final LN; CTC linear(d -> V); log_softmax.
+//
+// Device layout (per chunk of S segments, all equal length T_in frames):
+//   c1  bf16 [S][T1][F1][d]       channel-last conv1 output
+//   col bf16 [S*T2*F2][9d]        im2col rows for conv2 (k = (kh*3+kw)*d + c)
+//   c2  bf16 [S*T2][F2*d]         channel-last conv2 output == linear input
+//   X   f32  [S*T2][d]            residual stream
+//   Y   bf16 [S*T2][d]            LayerNorm output (GEMM A operand)
+//   QKV bf16 [S*T2][3d], AO bf16 [S*T2][d], H bf16 [S*T2][dff]
+//   grid f32 [S*T2][V]            caller's buffer, log-probabilities
+// All dense products go through gemm_bf16 (tcgen05, gemm_tcgen05.cu).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "encoder.cuh"
+#include "gemm.cuh"
+
+namespace bl {
+
+
+namespace {
+
+constexpr int kDk = 64;  // head width (d / heads)
+
+// ---------------------------------------------------------------- kernels
+// conv1 (1 -> d, 3x3, stride 2) + ReLU; fp32 math, bf16 channel-last output.
+__global__ void conv1_kernel(const float* __restrict__ fb, int T_in, int idim, int T1, int F1,
+                             int d, const float* __restrict__ w, const float* __restrict__ b,
+                             __nv_bfloat16* __restrict__ out, long long total) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % d);
+    long long r = i / d;
+    const int f = (int)(r % F1);
+    r /= F1;
+    const int t = (int)(r % T1);
+    const long long n = r / T1;
+    const float* x = fb + (n * T_in + 2 * t) * idim + 2 * f;
+    const float* wc = w + c * 9;
+    float acc = 0.f;
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) acc = fmaf(wc[kh * 3 + kw], x[kh * idim + kw], acc);
+    out[i] = __float2bfloat16_rn(fmaxf(acc + b[c], 0.f));
+  }
+}
+
+// im2col for conv2: col[(n,t2,f2)][(kh*3+kw)*d + c] = c1[n][2t2+kh][2f2+kw][c]
+__global__ void im2col_kernel(const __nv_bfloat16* __restrict__ c1, int T1, int F1, int T2,
+                              int F2, int d, __nv_bfloat16* __restrict__ col, long long total) {
+  const int c8n = d / 8;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c8 = (int)(i % c8n);
+    long long r = i / c8n;
+    const int tap = (int)(r % 9);
+    r /= 9;
+    const int f2 = (int)(r % F2);
+    const long long q = r / F2;
+    const int t2 = (int)(q % T2);
+    const long long n = q / T2;
+    const int kh = tap / 3, kw = tap % 3;
+    const uint4* src = reinterpret_cast<const uint4*>(
+        c1 + (((n * T1 + 2 * t2 + kh) * F1 + 2 * f2 + kw) * d + c8 * 8));
+    uint4* dst = reinterpret_cast<uint4*>(col + (r * 9 + tap) * (long long)d + c8 * 8);
+    *dst = *src;
+  }
+}
+
+// LayerNorm over d (biased variance, eps 1e-12), one warp per row, VPL = d/32.
+template <int VPL>
+__global__ void layernorm_kernel(const float* __restrict__ X, int rows, const float* __restrict__ g,
+                                 const float* __restrict__ b, __nv_bfloat16* __restrict__ Y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  constexpr int d = VPL * 32;
+  const float* x = X + (size_t)warp * d;
+  float v[VPL];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    v[i] = x[i * 32 + lane];
+    s += v[i];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    v[i] -= mean;
+    q = fmaf(v[i], v[i], q);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rs = rsqrtf(q / d + 1e-12f);
+  __nv_bfloat16* y = Y + (size_t)warp * d;
+#pragma unroll
+  for (int i = 0; i < VPL; ++i) {
+    const int k = i * 32 + lane;
+    y[k] = __float2bfloat16_rn(v[i] * rs * g[k] + b[k]);
+  }
+}
+
+// Multi-head self-attention, no mask (equal-length segments), head width 64.
+// One CTA per (segment, head): K and V staged in shared memory as bf16 with a
+// 66-element row pitch (conflict-free 4-byte reads); one warp per query row.
+constexpr int kAttnWarps = 8;
+constexpr int kKvPitch = kDk + 2;
+
+__global__ void __launch_bounds__(kAttnWarps * 32)
+    attention_kernel(const __nv_bfloat16* __restrict__ qkv, int T, int d, int heads,
+                     __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(sm);
+  __nv_bfloat16* Vs = Ks + (size_t)T * kKvPitch;
+  float* qs = reinterpret_cast<float*>(Vs + (size_t)T * kKvPitch);  // [warps][64]
+  float* ps = qs + kAttnWarps * kDk;                                // [warps][T]
+  const int seg = blockIdx.x, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t ld = 3 * (size_t)d;
+  const __nv_bfloat16* base = qkv + (size_t)seg * T * ld;
+  for (int i = threadIdx.x; i < T * (kDk / 2); i += blockDim.x) {
+    const int t = i / (kDk / 2), k2 = i % (kDk / 2);
+    const __nv_bfloat162* row = reinterpret_cast<const __nv_bfloat162*>(base + t * ld);
+    reinterpret_cast<__nv_bfloat162*>(Ks + t * kKvPitch)[k2] = row[(d + h * kDk) / 2 + k2];
+    reinterpret_cast<__nv_bfloat162*>(Vs + t * kKvPitch)[k2] = row[(2 * d + h * kDk) / 2 + k2];
+  }
+  __syncthreads();
+  const float scale = rsqrtf((float)kDk);
+  float* q = qs + warp * kDk;
+  float* p = ps + (size_t)warp * T;
+  for (int tq = warp; tq < T; tq += kAttnWarps) {
+    const __nv_bfloat162 qv =
+        reinterpret_cast<const __nv_bfloat162*>(base + tq * ld + h * kDk)[lane];
+    q[2 * lane] = __bfloat162float(qv.x);
+    q[2 * lane + 1] = __bfloat162float(qv.y);
+    __syncwarp();
+    float m = -INFINITY;
+    for (int j = lane; j < T; j += 32) {
+      const __nv_bfloat162* kr = reinterpret_cast<const __nv_bfloat162*>(Ks + j * kKvPitch);
+      float s = 0.f;
+#pragma unroll 8
+      for (int k2 = 0; k2 < kDk / 2; ++k2) {
+        const float2 kf = __bfloat1622float2(kr[k2]);
+        s = fmaf(q[2 * k2], kf.x, s);
+        s = fmaf(q[2 * k2 + 1], kf.y, s);
+      }
+      s *= scale;
+      p[j] = s;
+      m = fmaxf(m, s);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float sum = 0.f;
+    for (int j = lane; j < T; j += 32) {
+      const float e = expf(p[j] - m);
+      p[j] = e;
+      sum += e;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    __syncwarp();
+    float a0 = 0.f, a1 = 0.f;
+    for (int j = 0; j < T; ++j) {
+      const float pj = p[j];
+      const float2 vf =
+          __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(Vs + j * kKvPitch)[lane]);
+      a0 = fmaf(pj, vf.x, a0);
+      a1 = fmaf(pj, vf.y, a1);
+    }
+    const float inv = 1.f / sum;
+    reinterpret_cast<__nv_bfloat162*>(out + ((size_t)seg * T + tq) * d + h * kDk)[lane] =
+        __floats2bfloat162_rn(a0 * inv, a1 * inv);
+    __syncwarp();
+  }
+}
+
+// in-place log_softmax over rows of width V; one CTA per row
+__global__ void __launch_bounds__(256) log_softmax_kernel(float* __restrict__ x, int V) {
+  __shared__ float red[8];
+  float* r = x + (size_t)blockIdx.x * V;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float m = -INFINITY;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) m = fmaxf(m, r[i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = red[0];
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+  __syncthreads();
+  float s = 0.f;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) s += expf(r[i] - m);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  s = 0.f;
+  for (int w = 0; w < 8; ++w) s += red[w];
+  const float lse = m + logf(s);
+  for (int i = threadIdx.x; i < V; i += blockDim.x) r[i] -= lse;
+}
+
+template <int VPL>
+void ln_launch(const float* X, int rows, const float* g, const float* b, __nv_bfloat16* Y,
+               cudaStream_t st) {
+  layernorm_kernel<VPL><<<(rows + 7) / 8, 256, 0, st>>>(X, rows, g, b, Y);
+}
+
+void launch_layernorm(int d, const float* X, int rows, const float* g, const float* b,
+                      __nv_bfloat16* Y, cudaStream_t st) {
+  switch (d / 64) {
+    case 1: ln_launch<2>(X, rows, g, b, Y, st); break;
+    case 2: ln_launch<4>(X, rows, g, b, Y, st); break;
+    case 3: ln_launch<6>(X, rows, g, b, Y, st); break;
+    case 4: ln_launch<8>(X, rows, g, b, Y, st); break;
+    case 5: ln_launch<10>(X, rows, g, b, Y, st); break;
+    case 6: ln_launch<12>(X, rows, g, b, Y, st); break;
+    case 7: ln_launch<14>(X, rows, g, b, Y, st); break;
+    case 8: ln_launch<16>(X, rows, g, b, Y, st); break;
+    case 9: ln_launch<18>(X, rows, g, b, Y, st); break;
+    case 10: ln_launch<20>(X, rows, g, b, Y, st); break;
+    case 11: ln_launch<22>(X, rows, g, b, Y, st); break;
+    case 12: ln_launch<24>(X, rows, g, b, Y, st); break;
+    case 13: ln_launch<26>(X, rows, g, b, Y, st); break;
+    case 14: ln_launch<28>(X, rows, g, b, Y, st); break;
+    case 15: ln_launch<30>(X, rows, g, b, Y, st); break;
+    default: ln_launch<32>(X, rows, g, b, Y, st); break;
+  }
+}
+
+int blocks_for(long long total, int nt = 256) {
+  long long b = (total + nt - 1) / nt;
+  return (int)(b > 148LL * 16 ? 148LL * 16 : (b < 1 ? 1 : b));
+}
+
+uint16_t to_bf16(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);  // round to nearest even
+  return (uint16_t)(u >> 16);
+}
+
+}  // namespace
+
+int enc_frames_out(int frames_in) {
+  if (frames_in < 7) return 0;
+  const int t1 = (frames_in - 3) / 2 + 1;
+  return (t1 - 3) / 2 + 1;
+}
+
+size_t enc_num_weights(const EncSpec& s) {
+  const size_t d = s.d, F2 = (size_t)enc_frames_out(s.idim);
+  size_t n = d * 9 + d + d * d * 9 + d + d * F2 * d + d;
+  n += (size_t)s.layers * (2 * d + 4 * (d * d + d) + 2 * d + (s.dff * d + s.dff) + (d * s.dff + d));
+  n += 2 * d + (size_t)s.vocab * d + s.vocab;
+  return n;
+}
+
+std::string enc_validate(const EncSpec& s) {
+  if (s.idim < 7) return "encoder idim must be >= 7";
+  if (s.d < 64 || s.d > 1024 || s.d % 64) return "encoder d_model must be a multiple of 64 in [64, 1024]";
+  if (s.heads < 1 || s.d != s.heads * kDk) return "encoder heads must give a head width of 64";
+  if (s.dff < 8 || s.dff % 8) return "encoder d_ff must be a positive multiple of 8";
+  if (s.layers < 0) return "encoder layers must be >= 0";
+  if (s.vocab < 2 || s.vocab % 4) return "encoder vocab must be >= 2 and a multiple of 4";
+  return "";
+}
+
+struct EncLayer {
+  float *ln1g, *ln1b, *bqkv, *bo, *ln2g, *ln2b, *b1, *b2;
+  __nv_bfloat16 *wqkv, *wo, *w1, *w2;
+};
+
+struct EncoderImpl {
+  EncSpec s;
+  int F1, F2;
+  cudaStream_t st = nullptr;
+  void* wbuf = nullptr;
+  float *c1w, *c1b, *c2b, *ob, *ang, *anb, *cb, *pe = nullptr;
+  __nv_bfloat16 *c2w, *ow, *cw;
+  std::vector<EncLayer> L;
+  // workspace
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  int pe_rows = 0;
+  int launches = 0;
+
+  explicit EncoderImpl(const EncSpec& sp) : s(sp) {
+    F1 = (s.idim - 3) / 2 + 1;
+    F2 = (F1 - 3) / 2 + 1;
+  }
+  ~EncoderImpl() {
+    if (wbuf) cudaFree(wbuf);
+    if (ws) cudaFree(ws);
+    if (pe) cudaFree(pe);
+  }
+
+  // Weights in the flat order documented in bl_b200.h (torch layouts).
+  cudaError_t load(const float* w) {
+    const size_t d = s.d;
+    std::vector<float> f32;
+    std::vector<uint16_t> b16;
+    struct Slot {
+      bool bf;
+      size_t off;
+    };
+    std::vector<Slot> slots;
+    auto put32 = [&](const float* p, size_t n) {
+      slots.push_back({false, f32.size()});
+      f32.insert(f32.end(), p, p + n);
+    };
+    auto put16 = [&](const std::vector<float>& v) {
+      slots.push_back({true, b16.size()});
+      for (float x : v) b16.push_back(to_bf16(x));
+      while (b16.size() % 64) b16.push_back(0);  // keep 128-B alignment
+    };
+    const float* p = w;
+    put32(p, d * 9); p += d * 9;      // conv1.w [d][1][3][3]
+    put32(p, d); p += d;              // conv1.b
+    {                                 // conv2.w [o][c][kh][kw] -> [o][(kh*3+kw)*d + c]
+      std::vector<float> v(d * 9 * d);
+      for (size_t o = 0; o < d; ++o)
+        for (size_t c = 0; c < d; ++c)
+          for (int t = 0; t < 9; ++t) v[o * 9 * d + t * d + c] = p[(o * d + c) * 9 + t];
+      put16(v);
+      p += d * d * 9;
+    }
+    put32(p, d); p += d;              // conv2.b
+    {                                 // out.w [o][c*F2 + f] -> [o][f*d + c]
+      const size_t K = d * F2;
+      std::vector<float> v(d * K);
+      for (size_t o = 0; o < d; ++o)
+        for (size_t c = 0; c < d; ++c)
+          for (int f = 0; f < F2; ++f) v[o * K + f * d + c] = p[o * K + c * F2 + f];
+      put16(v);
+      p += d * K;
+    }
+    put32(p, d); p += d;              // out.b
+    for (int l = 0; l < s.layers; ++l) {
+      put32(p, d); p += d;            // ln1.g
+      put32(p, d); p += d;            // ln1.b
+      std::vector<float> qkv(3 * d * d), bq(3 * d);
+      for (int j = 0; j < 3; ++j) {   // wq,bq,wk,bk,wv,bv -> [3d][d], [3d]
+        std::memcpy(&qkv[j * d * d], p, d * d * 4); p += d * d;
+        std::memcpy(&bq[j * d], p, d * 4); p += d;
+      }
+      put16(qkv);
+      put32(bq.data(), 3 * d);
+      put16(std::vector<float>(p, p + d * d)); p += d * d;  // wo
+      put32(p, d); p += d;            // bo
+      put32(p, d); p += d;            // ln2.g
+      put32(p, d); p += d;            // ln2.b
+      put16(std::vector<float>(p, p + s.dff * d)); p += s.dff * d;  // w1 [dff][d]
+      put32(p, s.dff); p += s.dff;    // b1
+      put16(std::vector<float>(p, p + d * s.dff)); p += d * s.dff;  // w2 [d][dff]
+      put32(p, d); p += d;            // b2
+    }
+    put32(p, d); p += d;              // after_norm.g
+    put32(p, d); p += d;              // after_norm.b
+    put16(std::vector<float>(p, p + (size_t)s.vocab * d)); p += (size_t)s.vocab * d;  // ctc.w
+    put32(p, s.vocab);                // ctc.b
+    while (f32.size() % 32) f32.push_back(0.f);
+
+    const size_t bytes32 = f32.size() * 4, bytes16 = b16.size() * 2;
+    cudaError_t e = cudaMalloc(&wbuf, bytes32 + bytes16);
+    if (e != cudaSuccess) return e;
+    float* d32 = static_cast<float*>(wbuf);
+    __nv_bfloat16* d16 = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(wbuf) + bytes32);
+    if ((e = cudaMemcpy(d32, f32.data(), bytes32, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(d16, b16.data(), bytes16, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    size_t k = 0;
+    auto nx32 = [&]() { return d32 + slots[k++].off; };
+    auto nx16 = [&]() { return d16 + slots[k++].off; };
+    c1w = nx32(); c1b = nx32(); c2w = nx16(); c2b = nx32(); ow = nx16(); ob = nx32();
+    L.resize(s.layers);
+    for (auto& y : L) {
+      y.ln1g = nx32(); y.ln1b = nx32(); y.wqkv = nx16(); y.bqkv = nx32(); y.wo = nx16();
+      y.bo = nx32(); y.ln2g = nx32(); y.ln2b = nx32(); y.w1 = nx16(); y.b1 = nx32();
+      y.w2 = nx16(); y.b2 = nx32();
+    }
+    ang = nx32(); anb = nx32(); cw = nx16(); cb = nx32();
+    return cudaSuccess;
+  }
+
+  cudaError_t ensure_pe(int T2) {
+    if (pe_rows >= T2) return cudaSuccess;
+    if (pe) cudaFree(pe);
+    pe = nullptr;
+    std::vector<float> h((size_t)T2 * s.d);
+    const float k = -std::log(10000.0f) / s.d;
+    for (int t = 0; t < T2; ++t)
+      for (int i = 0; i < s.d; i += 2) {
+        const float div = std::exp((float)i * k);
+        const float a = (float)t * div;
+        h[(size_t)t * s.d + i] = std::sin(a);
+        h[(size_t)t * s.d + i + 1] = std::cos(a);
+      }
+    cudaError_t e = cudaMalloc(&pe, h.size() * 4);
+    if (e != cudaSuccess) return e;
+    pe_rows = T2;
+    return cudaMemcpy(pe, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+  }
+
+  static size_t al(size_t b) { return (b + 255) & ~(size_t)255; }
+
+  // Bytes of workspace for a chunk of S segments of T_in frames.
+  size_t chunk_bytes(int S, int T_in, bool host_fbank) const {
+    const size_t T1 = (T_in - 3) / 2 + 1, T2 = enc_frames_out(T_in), d = s.d;
+    size_t b = 0;
+    if (host_fbank) b += al((size_t)S * T_in * s.idim * 4);
+    b += al((size_t)S * T1 * F1 * d * 2);
+    b += al((size_t)S * T2 * F2 * 9 * d * 2);
+    b += al((size_t)S * T2 * F2 * d * 2);
+    b += al((size_t)S * T2 * d * 4);
+    b += al((size_t)S * T2 * d * 2) * 2;
+    b += al((size_t)S * T2 * 3 * d * 2);
+    b += al((size_t)S * T2 * s.dff * 2);
+    return b;
+  }
+
+  cudaError_t gemm(int M, int N, int K, const __nv_bfloat16* A, const __nv_bfloat16* B, int mode,
+                   const float* bias, float* of, __nv_bfloat16* ob16, int ldo) {
+    GemmDesc g;
+    g.M = M; g.N = N; g.K = K; g.A = A; g.lda = K; g.B = B; g.ldb = K;
+    g.mode = mode; g.bias = bias; g.out_f32 = of; g.out_bf16 = ob16; g.ldo = ldo;
+    if (mode == kScalePe) {
+      g.scale = std::sqrt((float)s.d);
+      g.pe = pe;
+      g.pe_rows = enc_frames_out(cur_tin);
+    }
+    ++launches;
+    return gemm_bf16(g, st);
+  }
+  int cur_tin = 0;
+
+  // n segments of T_in frames; fbank [n][T_in][idim] (host or device);
+  // grid [n][T2][vocab] device fp32.
+  cudaError_t forward(int n, int T_in, const float* fbank, bool on_device, float* grid,
+                      int chunk) {
+    cur_tin = T_in;
+    const int T1 = (T_in - 3) / 2 + 1, T2 = enc_frames_out(T_in), d = s.d;
+    cudaError_t e = ensure_pe(T2);
+    if (e != cudaSuccess) return e;
+    const int S = std::max(1, std::min(chunk, n));
+    const size_t need = chunk_bytes(S, T_in, !on_device);
+    if (need > ws_bytes) {
+      if (ws) cudaFree(ws);
+      ws = nullptr;
+      ws_bytes = 0;
+      if ((e = cudaMalloc(&ws, need)) != cudaSuccess) return e;
+      ws_bytes = need;
+    }
+    const int T2max = T2;
+    const size_t attn_smem =
+        (size_t)2 * T2max * kKvPitch * 2 + kAttnWarps * kDk * 4 + (size_t)kAttnWarps * T2max * 4;
+    if (attn_smem > 227 * 1024) return cudaErrorInvalidValue;
+    if ((e = cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)attn_smem)) != cudaSuccess)
+      return e;
+    launches = 0;
+    for (int s0 = 0; s0 < n; s0 += S) {
+      const int ns = std::min(S, n - s0);
+      char* p = static_cast<char*>(ws);
+      auto take = [&](size_t b) {
+        char* r = p;
+        p += al(b);
+        return r;
+      };
+      const float* fb = fbank + (size_t)s0 * T_in * s.idim;
+      if (!on_device) {
+        float* dfb = reinterpret_cast<float*>(take((size_t)S * T_in * s.idim * 4));
+        if ((e = cudaMemcpyAsync(dfb, fb, (size_t)ns * T_in * s.idim * 4, cudaMemcpyHostToDevice,
+                                 st)) != cudaSuccess)
+          return e;
+        fb = dfb;
+      }
+      auto* c1 = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T1 * F1 * d * 2));
+      auto* col = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * F2 * 9 * d * 2));
+      auto* c2 = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * F2 * d * 2));
+      auto* X = reinterpret_cast<float*>(take((size_t)S * T2 * d * 4));
+      auto* Y = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * d * 2));
+      auto* AO = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * d * 2));
+      auto* QKV = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * 3 * d * 2));
+      auto* H = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * s.dff * 2));
+      float* out = grid + (size_t)s0 * T2 * s.vocab;
+
+      const long long n1 = (long long)ns * T1 * F1 * d;
+      conv1_kernel<<<blocks_for(n1), 256, 0, st>>>(fb, T_in, s.idim, T1, F1, d, c1w, c1b, c1, n1);
+      const long long n2 = (long long)ns * T2 * F2 * 9 * (d / 8);
+      im2col_kernel<<<blocks_for(n2), 256, 0, st>>>(c1, T1, F1, T2, F2, d, col, n2);
+      launches += 2;
+      const int Mc = ns * T2 * F2, M = ns * T2;
+      if ((e = gemm(Mc, d, 9 * d, col, c2w, kRelu, c2b, nullptr, c2, d)) != cudaSuccess) return e;
+      if ((e = gemm(M, d, F2 * d, c2, ow, kScalePe, ob, X, nullptr, d)) != cudaSuccess) return e;
+      const int ln_blocks = (M + 7) / 8;
+      auto ln = [&](const float* g, const float* b) {
+        ++launches;
+        launch_layernorm(d, X, M, g, b, Y, st);
+      };
+      for (const auto& y : L) {
+        ln(y.ln1g, y.ln1b);
+        if ((e = gemm(M, 3 * d, d, Y, y.wqkv, kPlain, y.bqkv, nullptr, QKV, 3 * d)) != cudaSuccess)
+          return e;
+        attention_kernel<<<dim3(ns, s.heads), kAttnWarps * 32, attn_smem, st>>>(QKV, T2, d,
+                                                                               s.heads, AO);
+        ++launches;
+        if ((e = gemm(M, d, d, AO, y.wo, kResidual, y.bo, X, nullptr, d)) != cudaSuccess) return e;
+        ln(y.ln2g, y.ln2b);
+        if ((e = gemm(M, s.dff, d, Y, y.w1, kRelu, y.b1, nullptr, H, s.dff)) != cudaSuccess)
+          return e;
+        if ((e = gemm(M, d, s.dff, H, y.w2, kResidual, y.b2, X, nullptr, d)) != cudaSuccess)
+          return e;
+      }
+      ln(ang, anb);
+      if ((e = gemm(M, s.vocab, d, Y, cw, kPlain, cb, out, nullptr, s.vocab)) != cudaSuccess)
+        return e;
+      log_softmax_kernel<<<M, 256, 0, st>>>(out, s.vocab);
+      ++launches;
+    }
+    return cudaGetLastError();
+  }
+};
+
+}  // namespace bl
+
+namespace bl {
+
+cudaError_t enc_create(const EncSpec& s, const float* w, EncoderImpl** out) {
+  auto* e = new EncoderImpl(s);
+  cudaError_t r = e->load(w);
+  if (r != cudaSuccess) {
+    delete e;
+    return r;
+  }
+  *out = e;
+  return cudaSuccess;
+}
+void enc_destroy(EncoderImpl* e) { delete e; }
+void enc_set_stream(EncoderImpl* e, cudaStream_t st) { e->st = st; }
+cudaStream_t enc_stream(EncoderImpl* e) { return e->st; }
+cudaError_t enc_forward(EncoderImpl* e, int n, int T_in, const float* fb, bool on_device,
+                        float* grid, int chunk, int* launches) {
+  cudaError_t r = e->forward(n, T_in, fb, on_device, grid, chunk);
+  if (launches) *launches = e->launches;
+  return r;
+}
+size_t enc_workspace_bytes(EncoderImpl* e) { return e->ws_bytes; }
+
+}  // namespace bl

@@ -1,0 +1,35 @@
+// gemm.cuh — host interface of the tcgen05 bf16 GEMM (gemm_tcgen05.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace bl {
+
+enum GemmEpilogue : int {
+  kPlain = 0,     // out = acc (+ bias)
+  kRelu = 1,      // out = max(acc + bias, 0)
+  kResidual = 2,  // out_f32 += acc + bias   (in place residual stream)
+  kScalePe = 3,   // out = (acc + bias) * scale + pe[row % pe_rows][col]
+};
+
+// C[M,N] = A[M,K] . B[N,K]^T; A, B bf16 K-major (row strides lda/ldb in
+// elements, multiples of 8; K a multiple of 8). Either or both outputs.
+struct GemmDesc {
+  int M = 0, N = 0, K = 0;
+  const __nv_bfloat16* A = nullptr;
+  int lda = 0;
+  const __nv_bfloat16* B = nullptr;
+  int ldb = 0;
+  int mode = kPlain;
+  const float* bias = nullptr;
+  float* out_f32 = nullptr;
+  __nv_bfloat16* out_bf16 = nullptr;
+  int ldo = 0;
+  float scale = 1.f;
+  const float* pe = nullptr;
+  int pe_rows = 1;
+};
+
+cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t st);
+
+}  // namespace bl
