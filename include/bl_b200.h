@@ -194,6 +194,8 @@ int bl_encoder_frames_out(int frames_in);
 size_t bl_encoder_num_weights(const bl_encoder_spec* spec);
 int bl_encoder_create(int device, const bl_encoder_spec* spec, const float* weights,
                       size_t n_weights, bl_encoder** out);
+/* Stream used verbatim (NULL = the legacy default stream); the encoder starts
+ * on a private non-blocking stream. */
 int bl_encoder_set_stream(bl_encoder* e, void* stream);
 /* Segments processed per internal chunk (workspace ~ chunk x 50 MB at d=512). */
 int bl_encoder_set_chunk(bl_encoder* e, int segments);
@@ -209,7 +211,9 @@ void bl_encoder_destroy(bl_encoder* e);
 /* Tensor-core GEMM used by the encoder, exported for tests/benchmarks:
  * C[M,N] = A[M,K] . B[N,K]^T, A/B bf16 device pointers (K-major, strides in
  * elements, multiples of 8); epilogue mode 0 plain, 1 ReLU, 2 residual
- * (out_f32 += ...), 3 scale + positional table (scale, pe[pe_rows][N]). */
+ * (out_f32 += ...), 3 scale + positional table (scale, pe[pe_rows][N]).
+ * Exactly one of out_f32 / out_bf16 (modes 2 and 3: out_f32); output row
+ * stride ldo a multiple of 16 bytes. */
 int bl_gemm_bf16(int M, int N, int K, const void* A, int lda, const void* B, int ldb,
                  int mode, const float* bias, float* out_f32, void* out_bf16, int ldo,
                  float scale, const float* pe, int pe_rows, void* stream);

@@ -970,7 +970,7 @@ int bl_encoder_create(int device, const bl_encoder_spec* spec, const float* weig
 }
 
 int bl_encoder_set_stream(bl_encoder* e, void* stream) {
-  bl::enc_set_stream(e->impl, stream ? static_cast<cudaStream_t>(stream) : e->own);
+  bl::enc_set_stream(e->impl, static_cast<cudaStream_t>(stream));
   return BL_OK;
 }
 
@@ -1015,8 +1015,13 @@ int bl_gemm_bf16(int M, int N, int K, const void* A, int lda, const void* B, int
     if (M < 1 || N < 1 || K < 8 || K % 8 || lda % 8 || ldb % 8 || lda < K || ldb < K)
       throw std::invalid_argument("gemm: bad shape or stride");
     if (mode < 0 || mode > 3) throw std::invalid_argument("gemm: bad epilogue mode");
-    if (!out_f32 && !out_bf16) throw std::invalid_argument("gemm: no output");
-    if ((mode == 2 && !out_f32) || (mode == 3 && (!pe || pe_rows < 1)))
+    if ((out_f32 != nullptr) == (out_bf16 != nullptr))
+      throw std::invalid_argument("gemm: exactly one of out_f32 / out_bf16");
+    if (out_bf16 ? ldo % 8 : ldo % 4)
+      throw std::invalid_argument("gemm: output row stride must be a multiple of 16 bytes");
+    if ((mode == 2 || mode == 3) && !out_f32)
+      throw std::invalid_argument("gemm: residual / positional epilogues write fp32");
+    if (mode == 3 && (!pe || pe_rows < 1))
       throw std::invalid_argument("gemm: epilogue operand missing");
     bl::GemmDesc g;
     g.M = M; g.N = N; g.K = K;

@@ -27,6 +27,7 @@
 
 #include "encoder.cuh"
 #include "gemm.cuh"
+#include "tc_ptx.cuh"
 
 namespace bl {
 
@@ -37,25 +38,31 @@ constexpr int kDk = 64;  // head width (d / heads)
 
 // ---------------------------------------------------------------- kernels
 // conv1 (1 -> d, 3x3, stride 2) + ReLU; fp32 math, bf16 channel-last output.
+// One CTA per (segment, output frame t1): the three input frames are staged
+// in shared memory, each thread keeps its channel's 9 taps in registers and
+// sweeps the F1 output bins (stores coalesced along channels).
 __global__ void conv1_kernel(const float* __restrict__ fb, int T_in, int idim, int T1, int F1,
                              int d, const float* __restrict__ w, const float* __restrict__ b,
-                             __nv_bfloat16* __restrict__ out, long long total) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c = (int)(i % d);
-    long long r = i / d;
-    const int f = (int)(r % F1);
-    r /= F1;
-    const int t = (int)(r % T1);
-    const long long n = r / T1;
-    const float* x = fb + (n * T_in + 2 * t) * idim + 2 * f;
-    const float* wc = w + c * 9;
-    float acc = 0.f;
+                             __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float rows3[];  // [3][idim]
+  const int t = blockIdx.x, n = blockIdx.y;
+  const float* x = fb + ((size_t)n * T_in + 2 * t) * idim;
+  for (int i = threadIdx.x; i < 3 * idim; i += blockDim.x) rows3[i] = x[i];
+  __syncthreads();
+  __nv_bfloat16* o = out + ((size_t)n * T1 + t) * F1 * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float wc[9];
 #pragma unroll
-    for (int kh = 0; kh < 3; ++kh)
+    for (int k = 0; k < 9; ++k) wc[k] = w[c * 9 + k];
+    const float bc = b[c];
+    for (int f = 0; f < F1; ++f) {
+      float acc = 0.f;
 #pragma unroll
-      for (int kw = 0; kw < 3; ++kw) acc = fmaf(wc[kh * 3 + kw], x[kh * idim + kw], acc);
-    out[i] = __float2bfloat16_rn(fmaxf(acc + b[c], 0.f));
+      for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+        for (int kw = 0; kw < 3; ++kw) acc = fmaf(wc[kh * 3 + kw], rows3[kh * idim + 2 * f + kw], acc);
+      o[(size_t)f * d + c] = __float2bfloat16_rn(fmaxf(acc + bc, 0.f));
+    }
   }
 }
 
@@ -188,6 +195,166 @@ __global__ void __launch_bounds__(kAttnWarps * 32)
         __floats2bfloat162_rn(a0 * inv, a1 * inv);
     __syncwarp();
   }
+}
+
+// Self-attention on the tensor cores for segments of T <= 256 frames.
+// One CTA (128 threads) per (segment, head, 128-query tile):
+//   TMA: Q [128 x 64], K [256 x 64], V [256 x 64] bf16 tiles (SWIZZLE_128B)
+//   S = Q K^T   tcgen05.mma M=128 N=256 K=64 -> TMEM columns [0, 256)
+//   softmax     thread r owns query row r: two tcgen05.ld sweeps (max, then
+//               exp/sum), P = exp(...) as bf16 into a SWIZZLE_128B K-major
+//               tile in shared memory (aliasing the consumed Q/K tiles)
+//   O = P V     tcgen05.mma M=128 N=64 K=256, V as the MN-major operand,
+//               -> TMEM columns [0, 64); O / rowsum -> bf16 rows
+// Keys >= T (the next segment's rows, or zero fill past the end) are masked.
+constexpr int kAttQ = 128, kAttK = 256;
+constexpr int kAttSmem = 16384 /*Q*/ + 32768 /*K*/ + 16384 /*P tail*/ + 32768 /*V*/ + 1024;
+constexpr uint32_t kIdescS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kAttK >> 3) << 17) |
+                             ((uint32_t)(kAttQ >> 4) << 24);
+constexpr uint32_t kIdescO = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) /*B MN-major*/ |
+                             ((uint32_t)(kDk >> 3) << 17) | ((uint32_t)(kAttQ >> 4) << 24);
+
+__global__ void __launch_bounds__(128)
+    attention_tc_kernel(const __grid_constant__ CUtensorMap tQ,
+                        const __grid_constant__ CUtensorMap tKV, int T, int d,
+                        __nv_bfloat16* __restrict__ out) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char araw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(araw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* Qs = sm;
+  unsigned char* Ks = sm + 16384;
+  unsigned char* Ps = sm;           // 4 x [128 x 64] bf16 blocks = 64 KB (after S)
+  unsigned char* Vs = sm + 65536;
+  __shared__ __align__(8) uint64_t bar_ld, bar_mma;
+  __shared__ uint32_t tbase;
+  const int n = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int row0 = n * T;
+  if (tid == 0) {
+    mb_init(&bar_ld, 1);
+    mb_init(&bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mb_expect_tx(&bar_ld, 16384 + 2 * 32768);
+    tma2d(Qs, &tQ, h * kDk, row0 + qt * kAttQ, &bar_ld);
+    tma2d(Ks, &tKV, d + h * kDk, row0, &bar_ld);
+    tma2d(Vs, &tKV, 2 * d + h * kDk, row0, &bar_ld);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     s32(&tbase)),
+                 "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    mb_wait(&bar_ld, 0);
+    tc_fence_after();
+    const uint64_t dq = umma_desc(Qs), dk = umma_desc(Ks);
+#pragma unroll
+    for (int k = 0; k < kDk / 16; ++k) umma(tmem, dq + 2ull * k, dk + 2ull * k, kIdescS, k > 0);
+    umma_commit(&bar_mma);
+  }
+  __syncwarp();
+  mb_wait(&bar_mma, 0);
+  tc_fence_after();
+  const int r = warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const float c2 = 1.4426950408889634f * rsqrtf((float)kDk);  // log2(e) / sqrt(dk)
+  float m = -INFINITY;
+#pragma unroll 1
+  for (int c0 = 0; c0 < kAttK; c0 += 32) {
+    if (c0 >= T) break;
+    uint32_t v[32];
+    tmem_ld32(trow + c0, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (c0 + j < T) m = fmaxf(m, __uint_as_float(v[j]));
+  }
+  float sum = 0.f;
+#pragma unroll 1
+  for (int c0 = 0; c0 < kAttK; c0 += 32) {
+    uint32_t v[32];
+    if (c0 < T) tmem_ld32(trow + c0, v);
+    float p[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float e = (c0 + j < T) ? exp2f((__uint_as_float(v[j]) - m) * c2) : 0.f;
+      const float eb = __bfloat162float(__float2bfloat16_rn(e));
+      p[j] = e;
+      sum += eb;
+    }
+    // P block b = c0 / 64, 16-byte chunks (c0 % 64) / 8 .. +3 of row r
+    unsigned char* blk = Ps + (c0 >> 6) * 16384;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint4 u;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(p[8 * c], p[8 * c + 1]);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(p[8 * c + 2], p[8 * c + 3]);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(p[8 * c + 4], p[8 * c + 5]);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(p[8 * c + 6], p[8 * c + 7]);
+      u.x = *reinterpret_cast<uint32_t*>(&h0);
+      u.y = *reinterpret_cast<uint32_t*>(&h1);
+      u.z = *reinterpret_cast<uint32_t*>(&h2);
+      u.w = *reinterpret_cast<uint32_t*>(&h3);
+      *reinterpret_cast<uint4*>(blk + sw128(r, ((c0 & 63) >> 3) + c)) = u;
+    }
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    const uint64_t dv = umma_desc(Vs);
+#pragma unroll
+    for (int kk = 0; kk < kAttK / 16; ++kk) {
+      const uint64_t dp = umma_desc(Ps + (kk >> 2) * 16384) + 2ull * (kk & 3);
+      umma(tmem, dp, dv + 128ull * kk /* 16 keys = 2048 B */, kIdescO, kk > 0);
+    }
+    umma_commit(&bar_mma);
+  }
+  __syncwarp();
+  mb_wait(&bar_mma, 1);
+  tc_fence_after();
+  const float inv = 1.f / sum;
+  const int q = qt * kAttQ + r;
+  uint32_t o[64];
+  {
+    uint32_t v[32];
+    tmem_ld32(trow, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = v[j];
+    tmem_ld32(trow + 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[32 + j] = v[j];
+  }
+  if (q < T) {
+    uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)row0 + q) * d + h * kDk);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      uint4 u;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(o[8 * c]) * inv,
+                                                __uint_as_float(o[8 * c + 1]) * inv);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2]) * inv,
+                                                __uint_as_float(o[8 * c + 3]) * inv);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 4]) * inv,
+                                                __uint_as_float(o[8 * c + 5]) * inv);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 6]) * inv,
+                                                __uint_as_float(o[8 * c + 7]) * inv);
+      u.x = *reinterpret_cast<uint32_t*>(&h0);
+      u.y = *reinterpret_cast<uint32_t*>(&h1);
+      u.z = *reinterpret_cast<uint32_t*>(&h2);
+      u.w = *reinterpret_cast<uint32_t*>(&h3);
+      dst[c] = u;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
 // in-place log_softmax over rows of width V; one CTA per row
@@ -474,6 +641,10 @@ struct EncoderImpl {
     if ((e = cudaFuncSetAttribute(attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)attn_smem)) != cudaSuccess)
       return e;
+    if ((e = cudaFuncSetAttribute(attention_tc_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem)) !=
+        cudaSuccess)
+      return e;
     launches = 0;
     for (int s0 = 0; s0 < n; s0 += S) {
       const int ns = std::min(S, n - s0);
@@ -501,8 +672,8 @@ struct EncoderImpl {
       auto* H = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * s.dff * 2));
       float* out = grid + (size_t)s0 * T2 * s.vocab;
 
-      const long long n1 = (long long)ns * T1 * F1 * d;
-      conv1_kernel<<<blocks_for(n1), 256, 0, st>>>(fb, T_in, s.idim, T1, F1, d, c1w, c1b, c1, n1);
+      conv1_kernel<<<dim3(T1, ns), 256, 3 * s.idim * sizeof(float), st>>>(fb, T_in, s.idim, T1,
+                                                                          F1, d, c1w, c1b, c1);
       const long long n2 = (long long)ns * T2 * F2 * 9 * (d / 8);
       im2col_kernel<<<blocks_for(n2), 256, 0, st>>>(c1, T1, F1, T2, F2, d, col, n2);
       launches += 2;
@@ -518,8 +689,19 @@ struct EncoderImpl {
         ln(y.ln1g, y.ln1b);
         if ((e = gemm(M, 3 * d, d, Y, y.wqkv, kPlain, y.bqkv, nullptr, QKV, 3 * d)) != cudaSuccess)
           return e;
-        attention_kernel<<<dim3(ns, s.heads), kAttnWarps * 32, attn_smem, st>>>(QKV, T2, d,
-                                                                               s.heads, AO);
+        if (T2 <= kAttK) {
+          CUtensorMap tQ, tKV;
+          if (!make_tmap(&tQ, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, QKV, 3 * d, M, (size_t)6 * d,
+                         kDk, kAttQ, CU_TENSOR_MAP_SWIZZLE_128B) ||
+              !make_tmap(&tKV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, QKV, 3 * d, M, (size_t)6 * d,
+                         kDk, kAttK, CU_TENSOR_MAP_SWIZZLE_128B))
+            return cudaErrorInvalidValue;
+          attention_tc_kernel<<<dim3(ns, s.heads, (T2 + kAttQ - 1) / kAttQ), 128, kAttSmem,
+                                st>>>(tQ, tKV, T2, d, AO);
+        } else {
+          attention_kernel<<<dim3(ns, s.heads), kAttnWarps * 32, attn_smem, st>>>(QKV, T2, d,
+                                                                                 s.heads, AO);
+        }
         ++launches;
         if ((e = gemm(M, d, d, AO, y.wo, kResidual, y.bo, X, nullptr, d)) != cudaSuccess) return e;
         ln(y.ln2g, y.ln2b);

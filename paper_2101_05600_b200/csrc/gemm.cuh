@@ -1,5 +1,6 @@
 // gemm.cuh — host interface of the tcgen05 bf16 GEMM (gemm_tcgen05.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -31,5 +32,10 @@ struct GemmDesc {
 };
 
 cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t st);
+
+// 2D row-major tensor map [rows][cols] (row stride ld_bytes), box box_cols x
+// box_rows (cuTensorMapEncodeTiled through the runtime's driver entry point).
+bool make_tmap(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int cols, int rows,
+               size_t ld_bytes, int box_cols, int box_rows, CUtensorMapSwizzle sw);
 
 }  // namespace bl

@@ -122,7 +122,8 @@ def _run_encoder(spec, n, frames, seed):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("spec_name,n,frames", [("TINY", 3, 150), ("SMALL", 3, 1000),
-                                                 ("LARGE", 1, 1000)])
+                                                 ("LARGE", 1, 1000), ("TINY", 2, 1100),
+                                                 ("SMALL", 2, 2000)])
 def test_encoder_vs_torch(spec_name, n, frames):
     from torch_encoder import encoder_forward
     spec = {"TINY": TINY, "SMALL": enc.SMALL, "LARGE": enc.LARGE}[spec_name]
