@@ -8,7 +8,7 @@
 //
 // Device layout (per chunk of S segments, all equal length T_in frames):
 //   c1  bf16 [S][T1][F1][d]       channel-last conv1 output
-//   col bf16 [S*T2*F2][9d]        im2col rows for conv2 (k = (kh*3+kw)*d + c)
+//   (conv2 is an implicit GEMM: 4D TMA boxes over c1, k = (kh*3+kw)*d + c)
 //   c2  bf16 [S*T2][F2*d]         channel-last conv2 output == linear input
 //   X   f32  [S*T2][d]            residual stream
 //   Y   bf16 [S*T2][d]            LayerNorm output (GEMM A operand)
@@ -38,53 +38,59 @@ constexpr int kDk = 64;  // head width (d / heads)
 
 // ---------------------------------------------------------------- kernels
 // conv1 (1 -> d, 3x3, stride 2) + ReLU; fp32 math, bf16 channel-last output.
-// One CTA per (segment, output frame t1): the three input frames are staged
-// in shared memory, each thread keeps its channel's 9 taps in registers and
-// sweeps the F1 output bins (stores coalesced along channels).
-__global__ void conv1_kernel(const float* __restrict__ fb, int T_in, int idim, int T1, int F1,
-                             int d, const float* __restrict__ w, const float* __restrict__ b,
-                             __nv_bfloat16* __restrict__ out) {
-  extern __shared__ float rows3[];  // [3][idim]
-  const int t = blockIdx.x, n = blockIdx.y;
-  const float* x = fb + ((size_t)n * T_in + 2 * t) * idim;
-  for (int i = threadIdx.x; i < 3 * idim; i += blockDim.x) rows3[i] = x[i];
-  __syncthreads();
-  __nv_bfloat16* o = out + ((size_t)n * T1 + t) * F1 * d;
-  for (int c = threadIdx.x; c < d; c += blockDim.x) {
-    float wc[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) wc[k] = w[c * 9 + k];
-    const float bc = b[c];
-    for (int f = 0; f < F1; ++f) {
-      float acc = 0.f;
-#pragma unroll
-      for (int kh = 0; kh < 3; ++kh)
-#pragma unroll
-        for (int kw = 0; kw < 3; ++kw) acc = fmaf(wc[kh * 3 + kw], rows3[kh * idim + 2 * f + kw], acc);
-      o[(size_t)f * d + c] = __float2bfloat16_rn(fmaxf(acc + bc, 0.f));
-    }
-  }
-}
+// One CTA per (segment, run of kC1Frames output frames): the input frames are
+// staged in shared memory; each thread owns a fixed group of 8 consecutive
+// channels (72 taps in registers, loaded once) and sweeps a strided subset of
+// the (frame, bin) outputs, writing one 16-byte vector per output (a warp
+// covers 512 contiguous bytes).
+constexpr int kC1Frames = 16;
 
-// im2col for conv2: col[(n,t2,f2)][(kh*3+kw)*d + c] = c1[n][2t2+kh][2f2+kw][c]
-__global__ void im2col_kernel(const __nv_bfloat16* __restrict__ c1, int T1, int F1, int T2,
-                              int F2, int d, __nv_bfloat16* __restrict__ col, long long total) {
-  const int c8n = d / 8;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c8 = (int)(i % c8n);
-    long long r = i / c8n;
-    const int tap = (int)(r % 9);
-    r /= 9;
-    const int f2 = (int)(r % F2);
-    const long long q = r / F2;
-    const int t2 = (int)(q % T2);
-    const long long n = q / T2;
-    const int kh = tap / 3, kw = tap % 3;
-    const uint4* src = reinterpret_cast<const uint4*>(
-        c1 + (((n * T1 + 2 * t2 + kh) * F1 + 2 * f2 + kw) * d + c8 * 8));
-    uint4* dst = reinterpret_cast<uint4*>(col + (r * 9 + tap) * (long long)d + c8 * 8);
-    *dst = *src;
+__global__ void __launch_bounds__(256) conv1_kernel(const float* __restrict__ fb, int T_in,
+                                                    int idim, int T1, int F1, int d,
+                                                    const float* __restrict__ w,
+                                                    const float* __restrict__ b,
+                                                    __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float rows[];  // [2 * kC1Frames + 1][idim]
+  const int t0 = blockIdx.x * kC1Frames, n = blockIdx.y;
+  const int nt = min(kC1Frames, T1 - t0);
+  const int nrows = 2 * nt + 1;
+  const float* x = fb + ((size_t)n * T_in + 2 * t0) * idim;
+  for (int i = threadIdx.x; i < nrows * idim; i += blockDim.x) rows[i] = x[i];
+  __syncthreads();
+  // d <= 1024 (enc_validate): groups <= 128, so every group has >= 2 threads
+  const int groups = d / 8, per = blockDim.x / groups;
+  const int cg = threadIdx.x % groups, j0 = threadIdx.x / groups;
+  if (j0 >= per) return;
+  float wr[8][9], br[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) wr[j][k] = __ldg(w + (cg * 8 + j) * 9 + k);
+    br[j] = __ldg(b + cg * 8 + j);
+  }
+  uint4* o = reinterpret_cast<uint4*>(out + ((size_t)n * T1 + t0) * F1 * d);
+  for (int i = j0; i < nt * F1; i += per) {
+    const int tt = i / F1, f = i - tt * F1;
+    const float* xr = rows + 2 * tt * idim + 2 * f;
+    float in[9];
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh)
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) in[kh * 3 + kw] = xr[kh * idim + kw];
+    uint32_t packed[4];
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+      float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < 9; ++k) {
+        a0 = fmaf(wr[j][k], in[k], a0);
+        a1 = fmaf(wr[j + 1][k], in[k], a1);
+      }
+      const __nv_bfloat162 h =
+          __floats2bfloat162_rn(fmaxf(a0 + br[j], 0.f), fmaxf(a1 + br[j + 1], 0.f));
+      packed[j / 2] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    o[(size_t)i * groups + cg] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
   }
 }
 
@@ -468,12 +474,19 @@ struct EncoderImpl {
   size_t ws_bytes = 0;
   int pe_rows = 0;
   int launches = 0;
+  // host fbank: chunk i+1 is copied on `cp` while chunk i computes on `st`
+  cudaStream_t cp = nullptr;
+  cudaEvent_t ev_start = nullptr, ev_copied[2] = {nullptr, nullptr},
+              ev_free[2] = {nullptr, nullptr};
 
   explicit EncoderImpl(const EncSpec& sp) : s(sp) {
     F1 = (s.idim - 3) / 2 + 1;
     F2 = (F1 - 3) / 2 + 1;
   }
   ~EncoderImpl() {
+    if (cp) cudaStreamDestroy(cp);
+    for (cudaEvent_t ev : {ev_start, ev_copied[0], ev_copied[1], ev_free[0], ev_free[1]})
+      if (ev) cudaEventDestroy(ev);
     if (wbuf) cudaFree(wbuf);
     if (ws) cudaFree(ws);
     if (pe) cudaFree(pe);
@@ -591,9 +604,8 @@ struct EncoderImpl {
   size_t chunk_bytes(int S, int T_in, bool host_fbank) const {
     const size_t T1 = (T_in - 3) / 2 + 1, T2 = enc_frames_out(T_in), d = s.d;
     size_t b = 0;
-    if (host_fbank) b += al((size_t)S * T_in * s.idim * 4);
+    if (host_fbank) b += 2 * al((size_t)S * T_in * s.idim * 4);  // double-buffered
     b += al((size_t)S * T1 * F1 * d * 2);
-    b += al((size_t)S * T2 * F2 * 9 * d * 2);
     b += al((size_t)S * T2 * F2 * d * 2);
     b += al((size_t)S * T2 * d * 4);
     b += al((size_t)S * T2 * d * 2) * 2;
@@ -646,9 +658,37 @@ struct EncoderImpl {
         cudaSuccess)
       return e;
     launches = 0;
-    for (int s0 = 0; s0 < n; s0 += S) {
+    const size_t fb_elems = (size_t)S * T_in * s.idim;
+    float* stage[2] = {nullptr, nullptr};
+    char* p0 = static_cast<char*>(ws);
+    if (!on_device) {
+      if (!cp) {
+        if ((e = cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking)) != cudaSuccess) return e;
+        for (cudaEvent_t* ev : {&ev_start, &ev_copied[0], &ev_copied[1], &ev_free[0], &ev_free[1]})
+          if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return e;
+      }
+      stage[0] = reinterpret_cast<float*>(p0);
+      stage[1] = reinterpret_cast<float*>(p0 + al(fb_elems * 4));
+      p0 += 2 * al(fb_elems * 4);
+      // copies may start once earlier work on st (a previous forward) is done
+      if ((e = cudaEventRecord(ev_start, st)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(cp, ev_start, 0)) != cudaSuccess) return e;
+    }
+    auto prefetch = [&](int ci) -> cudaError_t {
+      const int c0 = ci * S, cn = std::min(S, n - c0);
+      const int b = ci & 1;
+      cudaError_t r;
+      if (ci >= 2 && (r = cudaStreamWaitEvent(cp, ev_free[b], 0)) != cudaSuccess) return r;
+      if ((r = cudaMemcpyAsync(stage[b], fbank + (size_t)c0 * T_in * s.idim,
+                               (size_t)cn * T_in * s.idim * 4, cudaMemcpyHostToDevice, cp)) !=
+          cudaSuccess)
+        return r;
+      return cudaEventRecord(ev_copied[b], cp);
+    };
+    if (!on_device && (e = prefetch(0)) != cudaSuccess) return e;
+    for (int s0 = 0, ci = 0; s0 < n; s0 += S, ++ci) {
       const int ns = std::min(S, n - s0);
-      char* p = static_cast<char*>(ws);
+      char* p = p0;
       auto take = [&](size_t b) {
         char* r = p;
         p += al(b);
@@ -656,14 +696,11 @@ struct EncoderImpl {
       };
       const float* fb = fbank + (size_t)s0 * T_in * s.idim;
       if (!on_device) {
-        float* dfb = reinterpret_cast<float*>(take((size_t)S * T_in * s.idim * 4));
-        if ((e = cudaMemcpyAsync(dfb, fb, (size_t)ns * T_in * s.idim * 4, cudaMemcpyHostToDevice,
-                                 st)) != cudaSuccess)
-          return e;
-        fb = dfb;
+        if (s0 + S < n && (e = prefetch(ci + 1)) != cudaSuccess) return e;
+        if ((e = cudaStreamWaitEvent(st, ev_copied[ci & 1], 0)) != cudaSuccess) return e;
+        fb = stage[ci & 1];
       }
       auto* c1 = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T1 * F1 * d * 2));
-      auto* col = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * F2 * 9 * d * 2));
       auto* c2 = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * F2 * d * 2));
       auto* X = reinterpret_cast<float*>(take((size_t)S * T2 * d * 4));
       auto* Y = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * d * 2));
@@ -672,13 +709,18 @@ struct EncoderImpl {
       auto* H = reinterpret_cast<__nv_bfloat16*>(take((size_t)S * T2 * s.dff * 2));
       float* out = grid + (size_t)s0 * T2 * s.vocab;
 
-      conv1_kernel<<<dim3(T1, ns), 256, 3 * s.idim * sizeof(float), st>>>(fb, T_in, s.idim, T1,
-                                                                          F1, d, c1w, c1b, c1);
-      const long long n2 = (long long)ns * T2 * F2 * 9 * (d / 8);
-      im2col_kernel<<<blocks_for(n2), 256, 0, st>>>(c1, T1, F1, T2, F2, d, col, n2);
+      conv1_kernel<<<dim3((T1 + kC1Frames - 1) / kC1Frames, ns), 256,
+                     (2 * kC1Frames + 1) * s.idim * sizeof(float), st>>>(fb, T_in, s.idim, T1,
+                                                                         F1, d, c1w, c1b, c1);
+      if (!on_device && (e = cudaEventRecord(ev_free[ci & 1], st)) != cudaSuccess) return e;
       launches += 2;
-      const int Mc = ns * T2 * F2, M = ns * T2;
-      if ((e = gemm(Mc, d, 9 * d, col, c2w, kRelu, c2b, nullptr, c2, d)) != cudaSuccess) return e;
+      const int M = ns * T2;
+      {
+        Conv2Desc cd;
+        cd.c1 = c1; cd.S = ns; cd.T1 = T1; cd.F1 = F1; cd.T2 = T2; cd.F2 = F2; cd.d = d;
+        cd.W = c2w; cd.bias = c2b; cd.out = c2;
+        if ((e = conv2_bf16(cd, st)) != cudaSuccess) return e;
+      }
       if ((e = gemm(M, d, F2 * d, c2, ow, kScalePe, ob, X, nullptr, d)) != cudaSuccess) return e;
       const int ln_blocks = (M + 7) / 8;
       auto ln = [&](const float* g, const float* b) {

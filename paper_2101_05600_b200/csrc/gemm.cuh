@@ -33,6 +33,18 @@ struct GemmDesc {
 
 cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t st);
 
+// conv2 (d -> d, 3x3, stride 2) + bias + ReLU as an implicit GEMM over the
+// channel-last conv1 output c1[S][T1][F1][d]; W [d][(kh*3+kw)*d + c] bf16;
+// out [S][T2][F2][d] bf16. No im2col buffer: the A tiles are 4D TMA boxes.
+struct Conv2Desc {
+  const __nv_bfloat16* c1 = nullptr;
+  int S = 0, T1 = 0, F1 = 0, T2 = 0, F2 = 0, d = 0;
+  const __nv_bfloat16* W = nullptr;
+  const float* bias = nullptr;
+  __nv_bfloat16* out = nullptr;
+};
+cudaError_t conv2_bf16(const Conv2Desc& c, cudaStream_t st);
+
 // 2D row-major tensor map [rows][cols] (row stride ld_bytes), box box_cols x
 // box_rows (cuTensorMapEncodeTiled through the runtime's driver entry point).
 bool make_tmap(CUtensorMap* m, CUtensorMapDataType dt, const void* base, int cols, int rows,

@@ -97,13 +97,16 @@ struct GemmArgs {
   float scale;
   const float* pe;
   int pe_rows;
+  // implicit conv2 (kConv): A tiles are 4D TMA boxes over the channel-last
+  // conv1 output; a tile covers `tpt` output frames x F2 bins = `rows` rows
+  int S, T2, F2, tpt, tps, ktin, rows;
 };
 
-template <int BN>
+template <int BN, bool kConv>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB,
                 const __grid_constant__ CUtensorMap tOb, const __grid_constant__ CUtensorMap tOf,
-                const GemmArgs g) {
+                const __grid_constant__ CUtensorMap tOr, const GemmArgs g) {
   using C = Cfg<BN>;
   constexpr int S = C::kStages;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -114,9 +117,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ uint32_t tmem_base;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int KT = (g.K + kBK - 1) / kBK;
+  const int KT = kConv ? 3 * g.ktin : (g.K + kBK - 1) / kBK;
   const int tiles_n = (g.N + BN - 1) / BN;
-  const int tiles = ((g.M + kBM - 1) / kBM) * tiles_n;
+  const int tiles = (kConv ? g.S * g.tps : (g.M + kBM - 1) / kBM) * tiles_n;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
@@ -151,8 +154,15 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int s = it % S;
           if (it >= S) mb_wait(&empty[s], ((it / S) - 1) & 1);
           unsigned char* st = smem + (size_t)s * C::kStage;
-          mb_expect_tx(&full[s], C::kStage);
-          tma2d(st, &tA, kt * kBK, m0, &full[s]);
+          mb_expect_tx(&full[s], kConv ? g.rows * 128 + C::kB : C::kStage);
+          if (kConv) {
+            const int mt = tile / tiles_n, seg = mt / g.tps, t20 = (mt % g.tps) * g.tpt;
+            const int kh = kt / g.ktin, kin = kt - kh * g.ktin;
+            // rows (f2, t2): conv1 rows 2*t2 + kh, columns 2*f2 .. 2*f2+2 (3d contiguous)
+            tma4d(st, &tA, kin * kBK, 0, 2 * t20 + kh, seg, &full[s]);
+          } else {
+            tma2d(st, &tA, kt * kBK, m0, &full[s]);
+          }
           tma2d(st + C::kA, &tB, kt * kBK, n0, &full[s]);
         }
       }
@@ -199,9 +209,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int rbase = m0 + q * 32, row = rbase + lane;
       const bool row_ok = row < g.M;
+      int qrows = 32, cy = 0, cz = 0;
+      if (kConv) {
+        const int mt = tile / tiles_n;
+        qrows = min(32, g.rows - q * 32);
+        cz = mt / g.tps;
+        cy = (mt % g.tps) * g.tpt * g.F2 + q * 32;
+      }
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += CW, ++nchunk) {
-        if (n0 + c0 >= g.N) break;
+        if (n0 + c0 >= g.N || qrows <= 0) break;
         float x[64];
         {
           uint32_t v[32];
@@ -276,7 +293,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store2d(tO, sb, col0, rbase);
+          if (kConv)
+            tma_store3d(qrows == 32 ? &tOb : &tOr, sb, col0, cy, cz);
+          else
+            tma_store2d(tO, sb, col0, rbase);
           bulk_commit();
         }
         (void)kCW32;
@@ -300,6 +320,21 @@ bool make_map(CUtensorMap* m, const void* base, int rows, int K, int ld, int box
                    box_rows, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
+// 3D bf16 output [z][rows][cols], box 64 cols x box_rows x 1, SW128
+bool make_tmap3(CUtensorMap* m, const void* base, int cols, int rows, int z, size_t ld_bytes,
+                int box_rows) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)cols, (cuuint64_t)rows, (cuuint64_t)z};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld_bytes, (cuuint64_t)ld_bytes * rows};
+  const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box,
+             es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+         CUDA_SUCCESS;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -310,33 +345,46 @@ int num_sms() {
   return n;
 }
 
-template <int BN>
-cudaError_t launch(const GemmDesc& d, cudaStream_t st) {
-  CUtensorMap tA, tB, tOb, tOf;
-  if (!make_map(&tA, d.A, d.M, d.K, d.lda, kBM) || !make_map(&tB, d.B, d.N, d.K, d.ldb, BN))
-    return cudaErrorInvalidValue;
+template <int BN, bool kConv>
+cudaError_t launch(const GemmDesc& d, const CUtensorMap& tA, const GemmArgs& g, int tiles,
+                   cudaStream_t st) {
+  CUtensorMap tB, tOb, tOf, tOr;
   std::memset(&tOb, 0, sizeof(tOb));
   std::memset(&tOf, 0, sizeof(tOf));
-  if (d.out_bf16 && !make_tmap(&tOb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, d.out_bf16, d.N, d.M,
-                               (size_t)d.ldo * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+  std::memset(&tOr, 0, sizeof(tOr));
+  if (!make_map(&tB, d.B, d.N, d.K, d.ldb, BN)) return cudaErrorInvalidValue;
+  if (kConv) {
+    // 3D output [S][T2*F2][N]: stores clip at each segment's last frame
+    if (!make_tmap3(&tOb, d.out_bf16, d.N, g.T2 * g.F2, g.S, (size_t)d.ldo * 2, 32) ||
+        (g.rows % 32 && !make_tmap3(&tOr, d.out_bf16, d.N, g.T2 * g.F2, g.S,
+                                    (size_t)d.ldo * 2, g.rows % 32)))
+      return cudaErrorInvalidValue;
+  } else if (d.out_bf16) {
+    if (!make_tmap(&tOb, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, d.out_bf16, d.N, d.M,
+                   (size_t)d.ldo * 2, 64, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+  } else if (!make_tmap(&tOf, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, d.out_f32, d.N, d.M,
+                        (size_t)d.ldo * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B)) {
     return cudaErrorInvalidValue;
-  if (!d.out_bf16 && !make_tmap(&tOf, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, d.out_f32, d.N, d.M,
-                                (size_t)d.ldo * 4, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  GemmArgs g{d.M, d.N, d.K, d.mode, d.bias, d.out_f32, d.out_bf16, d.ldo, d.scale, d.pe,
-             d.pe_rows};
+  }
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, kConv>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg<BN>::kSmem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int tiles = ((d.M + kBM - 1) / kBM) * ((d.N + BN - 1) / BN);
   const int grid = tiles < num_sms() ? tiles : num_sms();
-  gemm_kernel<BN><<<grid, kThreads, Cfg<BN>::kSmem, st>>>(tA, tB, tOb, tOf, g);
+  gemm_kernel<BN, kConv><<<grid, kThreads, Cfg<BN>::kSmem, st>>>(tA, tB, tOb, tOf, tOr, g);
   return cudaGetLastError();
+}
+
+GemmArgs args_of(const GemmDesc& d) {
+  GemmArgs g{};
+  g.M = d.M; g.N = d.N; g.K = d.K; g.mode = d.mode; g.bias = d.bias; g.out_f32 = d.out_f32;
+  g.out_bf16 = d.out_bf16; g.ldo = d.ldo; g.scale = d.scale; g.pe = d.pe; g.pe_rows = d.pe_rows;
+  return g;
 }
 
 }  // namespace
@@ -347,11 +395,47 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t st) {
   if ((d.out_bf16 != nullptr) == (d.out_f32 != nullptr)) return cudaErrorInvalidValue;
   if (d.out_bf16 ? (d.ldo % 8) : (d.ldo % 4)) return cudaErrorInvalidValue;
   if ((d.mode == kResidual || d.mode == kScalePe) && !d.out_f32) return cudaErrorInvalidValue;
+  CUtensorMap tA;
+  if (!make_map(&tA, d.A, d.M, d.K, d.lda, kBM)) return cudaErrorInvalidValue;
+  const GemmArgs g = args_of(d);
   // 256-wide tiles halve A re-reads; 128-wide when N is small or the
   // 256-wide grid would leave most SMs idle.
-  const long long t256 = (long long)((d.M + kBM - 1) / kBM) * ((d.N + 255) / 256);
-  if (d.N > 128 && t256 >= num_sms()) return launch<256>(d, st);
-  return launch<128>(d, st);
+  const int tm = (d.M + kBM - 1) / kBM;
+  const long long t256 = (long long)tm * ((d.N + 255) / 256);
+  if (d.N > 128 && t256 >= num_sms()) return launch<256, false>(d, tA, g, (int)t256, st);
+  return launch<128, false>(d, tA, g, tm * ((d.N + 127) / 128), st);
+}
+
+cudaError_t conv2_bf16(const Conv2Desc& c, cudaStream_t st) {
+  const int d = c.d;
+  if (d % 64 || c.F2 < 1 || c.F2 > kBM || c.T2 < 1 || c.S < 1) return cudaErrorInvalidValue;
+  // A: conv1 output [S][T1][F1][d] viewed as 4D {3d (kw,c), F2 (stride 2d),
+  // T1 (stride F1*d, traversed with element stride 2), S}
+  CUtensorMap tA;
+  {
+    EncodeFn enc = encode_fn();
+    if (!enc) return cudaErrorInvalidValue;
+    const int tpt = kBM / c.F2;
+    const cuuint64_t dims[4] = {(cuuint64_t)3 * d, (cuuint64_t)c.F2, (cuuint64_t)c.T1,
+                                (cuuint64_t)c.S};
+    const cuuint64_t strides[3] = {(cuuint64_t)2 * d * 2, (cuuint64_t)c.F1 * d * 2,
+                                   (cuuint64_t)c.T1 * c.F1 * d * 2};
+    const cuuint32_t box[4] = {(cuuint32_t)kBK, (cuuint32_t)c.F2, (cuuint32_t)(2 * tpt), 1};
+    const cuuint32_t es[4] = {1, 1, 2, 1};
+    if (enc(&tA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<__nv_bfloat16*>(c.c1), dims,
+            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  GemmDesc gd;
+  gd.M = c.S * c.T2 * c.F2; gd.N = d; gd.K = 9 * d;
+  gd.B = c.W; gd.ldb = 9 * d; gd.mode = kRelu; gd.bias = c.bias;
+  gd.out_bf16 = c.out; gd.ldo = d;
+  GemmArgs g = args_of(gd);
+  g.S = c.S; g.T2 = c.T2; g.F2 = c.F2; g.tpt = kBM / c.F2;
+  g.tps = (c.T2 + g.tpt - 1) / g.tpt; g.ktin = 3 * d / kBK; g.rows = g.tpt * c.F2;
+  const int tiles = c.S * g.tps * ((d + 255) / 256);
+  return launch<256, true>(gd, tA, g, tiles, st);
 }
 
 }  // namespace bl

@@ -75,6 +75,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tma4d(void* dst, const CUtensorMap* m, int x, int y, int z, int w,
+                                      uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(s32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(s32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_store3d(const CUtensorMap* m, const void* src, int x, int y,
+                                            int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(m)),
+      "r"(s32(src)), "r"(x), "r"(y), "r"(z)
+      : "memory");
+}
 // bulk tensor store smem -> global (2D), bulk-group completion
 __device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* src, int x, int y) {
   asm volatile(
