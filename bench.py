@@ -228,8 +228,8 @@ def run_pipeline(args, torch, dist, bl, dec, ids, n, world, dev, local):
     audio = world * n * T_ENC * FRAME_SHIFT_MS / 1000.0
     return {"value": audio / (ms / 1000.0), "unit": "audio-s/s", "ms_per_step": ms,
             "encoder_ms": enc_ms, "decode_ms": ms - enc_ms,
-            "encoder_gemm_tflops": n * flops_seg / (enc_ms / 1000.0) / 1e12,
-            "encoder_gemm_flops_per_segment": flops_seg,
+            "encoder_tflops": n * flops_seg / (enc_ms / 1000.0) / 1e12,
+            "encoder_flops_per_segment": flops_seg,
             "h2d_bytes_per_step": n * 1000 * spec.idim * 4,
             "d2h_bytes_per_step": dec.last_stats.get("d2h_bytes", 0),
             "model": "encoder 6 layers d=256 4 heads ff=2048 vocab 500 (random-init), "
@@ -244,7 +244,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--segments", type=int, default=2880, help="segments per GPU")
-    ap.add_argument("--sample", type=int, default=8, help="CPU baseline segments")
+    ap.add_argument("--sample", type=int, default=24, help="CPU baseline segments")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
