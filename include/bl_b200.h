@@ -119,6 +119,10 @@ int bl_decoder_create(int device, const bl_config* cfg, const bl_scorer* scorer,
 int bl_decoder_set_options(bl_decoder* d, int nbest, int exact, double slack);
 /* Use an external CUDA stream (cudaStream_t as void*); NULL = own stream. */
 int bl_decoder_set_stream(bl_decoder* d, void* stream);
+/* Step-granular decoding: one kernel launch per decode step with the search
+ * state saved in HBM between steps (what a network scorer needs); results are
+ * identical to the default single-launch decode. */
+int bl_decoder_set_step_mode(bl_decoder* d, int on);
 void bl_decoder_destroy(bl_decoder* d);
 
 /* batched_beam_search (batched.hpp:34-38): decodes the utterances of ONE

@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
     L.bl_decoder_create.argtypes = [C.c_int, C.POINTER(_Config), vp, C.POINTER(vp)]
     L.bl_decoder_set_options.argtypes = [vp, C.c_int, C.c_int, C.c_double]
     L.bl_decoder_set_stream.argtypes = [vp, vp]
+    L.bl_decoder_set_step_mode.argtypes = [vp, C.c_int]
     L.bl_decoder_destroy.argtypes = [vp]
     L.bl_decode.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.c_int, C.POINTER(vp)]
     L.bl_results_count.argtypes = [vp]
@@ -423,7 +424,7 @@ class Decoder:
 
     def __init__(self, scorer: Scorer, cfg: Optional[DecoderConfig] = None,
                  device: int = 0, nbest: int = 1, exact: bool = False,
-                 slack: float = 1.0):
+                 slack: float = 1.0, step_mode: bool = False):
         self.nbest = nbest
         self._desc_cache = None
         self.cfg = cfg or DecoderConfig()
@@ -434,6 +435,8 @@ class Decoder:
         _check(lib().bl_decoder_create(device, C.byref(c), scorer._h, C.byref(h)))
         self._h = h
         _check(lib().bl_decoder_set_options(h, nbest, 1 if exact else 0, slack))
+        if step_mode:
+            _check(lib().bl_decoder_set_step_mode(h, 1))
         self.last_stats: Dict[str, float] = {}
 
     def set_stream(self, stream_ptr: int) -> None:

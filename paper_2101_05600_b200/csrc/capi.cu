@@ -26,6 +26,7 @@
 
 namespace bl {
 cudaError_t launch_decode(const KParams& p, cudaStream_t st);
+size_t step_state_bytes(int B, int S);
 size_t decode_smem_bytes(const KParams& p);
 int bmax_for(int B);
 }  // namespace bl
@@ -224,6 +225,10 @@ struct bl_decoder {
   DevBuf grid, utts, gam, Ftab, Gtab, kubg, ubitsg, xs, taken, hist, fin, res, cnt, prof;
   HostBuf h_grid, h_utts, h_res, h_cnt, h_prof;
   bool profile = getenv("BL_PROFILE") != nullptr;
+  // step-granular decoding (forced for tests, or required by a network scorer)
+  int step_mode = 0;
+  DevBuf state, n_done;
+  HostBuf h_done;
 };
 
 struct bl_results {
@@ -326,6 +331,32 @@ float guard_float() {
   while (static_cast<double>(std::nextafter(f, INFINITY)) <= -1e29)
     f = std::nextafter(f, INFINITY);
   return f;
+}
+
+// Step-granular decode of all utterances of `p` in lockstep: one launch
+// per step; the host polls the finished-utterance counter every few steps.
+int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
+  const size_t stride = bl::step_state_bytes(p.B, p.S);
+  d->state.ensure(stride * (size_t)p.U);
+  d->n_done.ensure(sizeof(unsigned));
+  d->h_done.ensure(sizeof(unsigned));
+  CK(cudaMemsetAsync(d->n_done.p, 0, sizeof(unsigned), st));
+  p.state = static_cast<unsigned char*>(d->state.p);
+  p.state_stride = (int)stride;
+  p.n_done = static_cast<unsigned*>(d->n_done.p);
+  int launches = 0;
+  const int poll = 4;
+  for (int l = 1; l <= p.S + 1; ++l) {
+    p.step_l = l;
+    CK(bl::launch_decode(p, st));
+    ++launches;
+    if (l % poll == 0 || l == p.S + 1) {
+      CK(cudaMemcpyAsync(d->h_done.p, d->n_done.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (*static_cast<unsigned*>(d->h_done.p) >= (unsigned)p.U) break;
+    }
+  }
+  return launches;
 }
 
 int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
@@ -543,8 +574,10 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   CK(cudaMemcpyAsync(d->utts.p, d->h_utts.p, sizeof(bl::UttDesc) * U,
                      cudaMemcpyHostToDevice, st));
   // chunking: one launch when grids are resident; otherwise ~600 utterances
-  // (two waves of resident CTAs) per chunk so copies overlap decoding
-  const int nchunk = on_device ? 1 : std::max(1, std::min(16, U / 360));
+  // (two waves of resident CTAs) per chunk so copies overlap decoding.
+  // Step-granular mode: one group, one launch per decode step.
+  const bool stepm = d->step_mode != 0;
+  const int nchunk = (on_device || stepm) ? 1 : std::max(1, std::min(16, U / 360));
   if ((int)d->ev_copy.size() < nchunk) {
     for (int k = (int)d->ev_copy.size(); k < nchunk; ++k) {
       cudaEvent_t e;
@@ -575,8 +608,12 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     bl::KParams pk = p;
     pk.u0 = a;
     pk.U = b - a;
-    CK(bl::launch_decode(pk, cs));
-    ++launches;
+    if (stepm) {
+      launches += step_loop(d, pk, cs);
+    } else {
+      CK(bl::launch_decode(pk, cs));
+      ++launches;
+    }
   }
   if (nchunk > 1) {
     CK(cudaEventRecord(d->ev_alt, d->alt));
@@ -815,6 +852,11 @@ int bl_decoder_set_options(bl_decoder* d, int nbest, int exact, double slack) {
     d->slack = slack;
     return BL_OK;
   });
+}
+
+int bl_decoder_set_step_mode(bl_decoder* d, int on) {
+  d->step_mode = on ? 1 : 0;
+  return BL_OK;
 }
 
 int bl_decoder_set_stream(bl_decoder* d, void* stream) {

@@ -90,6 +90,17 @@ struct KParams {
   int res_stride;
   unsigned long long* cnt;  // [U][8]
   long long* prof;          // [U][16] phase cycles, or nullptr
+  // step-granular mode (a network scorer runs between steps): step_l > 0
+  // runs exactly step l of every live utterance, restoring / saving the
+  // per-utterance search state (`state`, state_stride bytes each); finished
+  // utterances bump *n_done once.
+  int step_l;
+  int state_stride;
+  unsigned char* state;
+  unsigned* n_done;
+  // per-hypothesis scorer rows (network scorer): hypothesis k of utterance u
+  // reads row u * B + k of sc_rows / sc_rowsf at every step
+  int net_rows;
 };
 
 // Dynamic shared-memory plan (identical on host and device).

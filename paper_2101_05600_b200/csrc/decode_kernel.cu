@@ -388,12 +388,24 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
 
   // ---------------------------------------------------------------- init
   unsigned tma_jobs = 0;  // TMA jobs issued so far (stage = job % stages, parity = job / stages)
+  const bool stepm = P.step_l > 0;
+  unsigned char* st_u = stepm ? P.state + (size_t)u * P.state_stride : nullptr;
+  if (stepm && P.step_l > 1 && *reinterpret_cast<volatile int*>(st_u)) return;  // finished
   if (kTma && tid == 0) {
     for (int k = 0; k < P.tma_stages; ++k) mbar_init(&mbar[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < 320; i += kNT)
     reinterpret_cast<double*>(&tb)[i] = reinterpret_cast<const double*>(&c_sptab)[i];
+  if (stepm && P.step_l > 1) {
+    // resume: the search state saved at the end of step l-1
+    const int* src = reinterpret_cast<const int*>(st_u + 16);
+    int* dst = reinterpret_cast<int*>(&sh);
+    for (int i = tid; i < (int)(sizeof(Shared<BMAX>) / 4); i += kNT) dst[i] = src[i];
+    const double* sb = reinterpret_cast<const double*>(st_u + 16 + align16(sizeof(Shared<BMAX>)));
+    for (int i = tid; i <= P.S + 1; i += kNT) best_by_len[i] = sb[i];
+    __syncthreads();
+  } else {
   for (int i = tid; i <= P.S + 1; i += kNT) best_by_len[i] = -HUGE_VAL;
   {
     double* gn0 = gam_ptr(P, u, 0, 0, 0);
@@ -441,7 +453,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     sh.trigger = 2;
     sh.steps = 0;
     sh.c_queries = sh.c_frames = sh.c_k1 = sh.c_fallback = sh.c_cont = sh.c_steps = 0;
-    sh.b_row[0][0] = lookup_row(P, hist_c, 0, 0, 0, 0);
+    sh.b_row[0][0] = P.net_rows ? u * B : lookup_row(P, hist_c, 0, 0, 0, 0);
   }
   __syncthreads();
   if (ud.need_tail) {
@@ -458,10 +470,11 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     }
   }
   __syncthreads();
+  }  // fresh start
   PROF_MARK(0);
 
   // ---------------------------------------------------------- step loop
-  for (int l = 1;; ++l) {
+  for (int l = stepm ? P.step_l : 1;; ++l) {
     const int cur = (l - 1) & 1, nxt = l & 1;
     if (l > ud.max_steps) break;  // batched.cpp:125-128
     const int nb = sh.nb;
@@ -1113,7 +1126,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           sh.b_att[nxt][k] = __dadd_rn(sh.b_att[cur][j],
                                        P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
           sh.b_joint[nxt][k] = x.score;
-          sh.b_row[nxt][k] = lookup_row(P, hist_c, l, l - 1, j, c);
+          sh.b_row[nxt][k] = P.net_rows ? u * B + k : lookup_row(P, hist_c, l, l - 1, j, c);
           HistRec h;
           h.token = c;
           h.parent = j;
@@ -1199,6 +1212,16 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     __syncthreads();
     PROF_MARK(10);
     if (sh.done) break;
+    if (stepm) {
+      // suspend: save the search state for step l + 1
+      int* dst = reinterpret_cast<int*>(st_u + 16);
+      const int* src = reinterpret_cast<const int*>(&sh);
+      for (int i = tid; i < (int)(sizeof(Shared<BMAX>) / 4); i += kNT) dst[i] = src[i];
+      double* sb = reinterpret_cast<double*>(st_u + 16 + align16(sizeof(Shared<BMAX>)));
+      for (int i = tid; i <= P.S + 1; i += kNT) sb[i] = best_by_len[i];
+      if (tid == 0) *reinterpret_cast<int*>(st_u) = 0;
+      return;
+    }
   }
 
   // ------------------------------------------------------------ finalize
@@ -1336,6 +1359,10 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
   }
   __syncthreads();
   PROF_MARK(11);
+  if (stepm && tid == 0) {
+    *reinterpret_cast<int*>(st_u) = 1;
+    atomicAdd(P.n_done, 1u);
+  }
 }
 
 // ------------------------------------------------------------ launchers
@@ -1347,6 +1374,20 @@ int bmax_for(int B) {
   if (B <= 24) return 24;
   if (B <= 32) return 32;
   return 0;
+}
+
+// per-utterance step-mode state: {done flag, pad}[16 B], Shared<BMAX>, best_by_len[S+2]
+size_t step_state_bytes(int B, int S) {
+  size_t sh = 0;
+  switch (bmax_for(B)) {
+    case 4: sh = sizeof(Shared<4>); break;
+    case 8: sh = sizeof(Shared<8>); break;
+    case 12: sh = sizeof(Shared<12>); break;
+    case 16: sh = sizeof(Shared<16>); break;
+    case 24: sh = sizeof(Shared<24>); break;
+    default: sh = sizeof(Shared<32>); break;
+  }
+  return align16(16 + align16(sh) + sizeof(double) * (size_t)(S + 2));
 }
 
 size_t decode_smem_bytes(const KParams& p) {
