@@ -208,6 +208,10 @@ int bl_encoder_set_chunk(bl_encoder* e, int segments);
  * stream; returns after enqueue unless `sync` is non-zero. */
 int bl_encoder_forward(bl_encoder* e, int n, int frames_in, const float* fbank,
                        int fbank_on_device, float* grid, int sync);
+/* Same, also writing the encoder output (final LayerNorm, the decoder's
+ * memory) as bf16 DEVICE memory [n][frames_out][d_model] when memory != NULL. */
+int bl_encoder_forward_mem(bl_encoder* e, int n, int frames_in, const float* fbank,
+                           int fbank_on_device, float* grid, void* memory, int sync);
 /* Kernels launched by the last forward. */
 int bl_encoder_launches(const bl_encoder* e);
 void bl_encoder_destroy(bl_encoder* e);
@@ -221,6 +225,47 @@ void bl_encoder_destroy(bl_encoder* e);
 int bl_gemm_bf16(int M, int N, int K, const void* A, int lda, const void* B, int ldb,
                  int mode, const float* bias, float* out_f32, void* out_bf16, int ldo,
                  float scale, const float* pe, int pe_rows, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Transformer attention-decoder scorer (SURVEY.md §8 a'2): the paper's
+ * network behind the reference's Scorer contract (scorer.hpp:11-22), run on
+ * device for every hypothesis of every utterance once per decode step
+ * (the decoder switches to step-granular decoding). ESPnet
+ * TransformerDecoder, eval mode: Embedding*sqrt(d)+PE, `layers` x pre-LN
+ * [causal self-attention (ancestor-indexed KV cache), source attention over
+ * the encoder memory, FFN(ReLU)], final LayerNorm, output linear,
+ * log_softmax with an fp64 normaliser. sos = eos = vocab-1.
+ *
+ * Weights: flat fp32, torch layouts, in this order:
+ *   embed.w[vocab][d]
+ *   per layer: ln1.g ln1.b wq bq wk bk wv bv wo bo        (self-attention)
+ *              ln2.g ln2.b wq2 bq2 wk2 bk2 wv2 bv2 wo2 bo2 (source attention)
+ *              ln3.g ln3.b w1[dff][d] b1[dff] w2[d][dff] b2[d]
+ *   after_norm.g after_norm.b out.w[vocab][d] out.b[vocab]
+ * ---------------------------------------------------------------------- */
+typedef struct bl_transformer_spec {
+  int d_model; /* multiple of 64, <= 1024 */
+  int heads;   /* d_model / 64 */
+  int d_ff;
+  int layers;
+  int vocab;   /* |C|+1, eos = sos = vocab-1 */
+} bl_transformer_spec;
+
+size_t bl_transformer_num_weights(const bl_transformer_spec* spec);
+int bl_scorer_create_transformer(int device, const bl_transformer_spec* spec,
+                                 const float* weights, size_t n_weights, bl_scorer** out);
+/* bl_decode with a transformer scorer: `memory` is the encoder output, bf16
+ * DEVICE memory [n][mem_frames][d_model] (bl_encoder_forward_mem), utterance
+ * i's rows at memory + i*mem_frames*d_model. */
+int bl_decode_memory(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
+                     const void* memory, int mem_frames, bl_results** out);
+/* Record mode (parity tests): keep every scorer row the network produced for
+ * a live hypothesis, with the utterance index and the token prefix, so a
+ * host replay scorer can drive the reference decoder with identical rows. */
+int bl_decoder_set_record(bl_decoder* d, int on);
+int bl_decoder_record_count(const bl_decoder* d);
+int bl_decoder_record_get(const bl_decoder* d, int i, int* utt, int* len, const int** prefix,
+                          const double** row);
 
 #ifdef __cplusplus
 }

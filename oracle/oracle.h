@@ -48,6 +48,10 @@ typedef struct orc_scorer {
   const double* logp;     /* [n_entries * (num_tokens+1)] */
   int loop_token;         /* loop only */
   double p_loop;          /* loop only */
+  /* replay only (kind 3, oracle/_ref): entry k belongs to utterance
+   * replay_ids[ent_utt[k]]; its full prefix is ctx[k*(order-1) ..] */
+  const int* ent_utt;
+  const char* const* replay_ids;
 } orc_scorer;
 
 typedef struct orc_counters {

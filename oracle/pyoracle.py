@@ -33,7 +33,8 @@ class OrcScorer(C.Structure):
     _fields_ = [("kind", C.c_int), ("num_tokens", C.c_int), ("order", C.c_int),
                 ("n_entries", C.c_int), ("ctx_len", C.POINTER(C.c_int)),
                 ("ctx", C.POINTER(C.c_int)), ("logp", C.POINTER(C.c_double)),
-                ("loop_token", C.c_int), ("p_loop", C.c_double)]
+                ("loop_token", C.c_int), ("p_loop", C.c_double),
+                ("ent_utt", C.POINTER(C.c_int)), ("replay_ids", C.POINTER(C.c_char_p))]
 
 
 class OrcCounters(C.Structure):
@@ -70,6 +71,7 @@ class ScorerSpec:
     entries: list = field(default_factory=list)  # [(ctx tuple, logp list)]
     loop_token: int = 0
     p_loop: float = 0.9
+    replay_ids: list = field(default_factory=list)  # replay: entries are (utt, ctx, logp)
 
 
 def config(beam_width=3, ctc_weight=0.3, eos_m=3, eos_dend=-10.0, eos_c=2,
@@ -83,21 +85,34 @@ def config(beam_width=3, ctc_weight=0.3, eos_m=3, eos_dend=-10.0, eos_c=2,
 
 class _ScorerC:
     def __init__(self, spec: ScorerSpec):
-        kind = {"uniform": 0, "table": 1, "loop": 2}[spec.kind]
-        w = max(spec.order - 1, 1)
-        n = len(spec.entries)
+        kind = {"uniform": 0, "table": 1, "loop": 2, "replay": 3}[spec.kind]
+        replay = kind == 3
+        ents = spec.entries
+        order = spec.order
+        if replay:   # (utt index, full prefix, row): order covers the longest prefix
+            order = max([len(c) for _, c, _ in ents] + [0]) + 1
+        w = max(order - 1, 1)
+        n = len(ents)
         V = spec.num_tokens + 1
         self.ctx_len = (C.c_int * max(n, 1))()
         self.ctx = (C.c_int * max(n * w, 1))()
-        self.logp = (C.c_double * max(n * V, 1))()
-        for k, (ctx, lp) in enumerate(spec.entries):
+        self.logp = np.zeros(max(n * V, 1), np.float64)
+        self.ent_utt = (C.c_int * max(n, 1))()
+        for k, e in enumerate(ents):
+            if replay:
+                self.ent_utt[k] = int(e[0])
+                ctx, lp = e[1], e[2]
+            else:
+                ctx, lp = e
             self.ctx_len[k] = len(ctx)
             for i, t in enumerate(ctx):
                 self.ctx[k * w + i] = int(t)
-            for i, v in enumerate(lp):
-                self.logp[k * V + i] = float(v)
-        self.s = OrcScorer(kind, spec.num_tokens, spec.order, n, self.ctx_len,
-                           self.ctx, self.logp, spec.loop_token, spec.p_loop)
+            self.logp[k * V:(k + 1) * V] = np.asarray(lp, np.float64)
+        self.ids = (C.c_char_p * max(len(spec.replay_ids), 1))(
+            *[i.encode() for i in spec.replay_ids])
+        self.s = OrcScorer(kind, spec.num_tokens, order, n, self.ctx_len, self.ctx,
+                           self.logp.ctypes.data_as(C.POINTER(C.c_double)), spec.loop_token,
+                           spec.p_loop, self.ent_utt, self.ids)
 
 
 def _grid_ptrs(grids: Sequence[np.ndarray]):
@@ -245,6 +260,8 @@ class Ref:
                                        C.POINTER(C.c_double)]
         L.ref_verify.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int,
                                  C.c_uint64]
+        L.ref_replay_misses.restype = C.c_longlong
+        L.ref_replay_misses.argtypes = [C.c_int]
 
     def _corpus(self, h):
         out = []
@@ -285,6 +302,10 @@ class Ref:
             raise ValueError(err.value.decode())
         return _collect(self.lib, "ref_", h, ids), (cnt.steps, cnt.scorer_queries,
                                                      cnt.ctc_frames_evaluated)
+
+    def replay_misses(self, reset=True) -> int:
+        """Queries the replay scorer could not answer since the last reset."""
+        return int(self.lib.ref_replay_misses(1 if reset else 0))
 
     def hard_segments(self, T, min_len, max_len):
         cap = max(1, T // max(1, max_len) + 2)

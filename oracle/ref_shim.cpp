@@ -5,8 +5,10 @@
 // oracle/_ref/libblref.so. Used by tests/ as the ground-truth checker and by
 // bench.py as the CPU baseline ("kind": "reference"). No reference source is
 // copied; this file only marshals arguments.
+#include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <exception>
 #include <memory>
 #include <random>
@@ -45,8 +47,47 @@ void set_err(char* err, int errlen, const std::string& msg) {
   }
 }
 
+// Replays the rows a device network scorer produced, keyed by (utterance id,
+// full prefix): the reference decoder then searches with exactly the device's
+// attention scores. A query the device never answered is a divergence; it is
+// counted (score() runs inside the reference's OpenMP workers, so it must not
+// throw) and answered with the uniform row.
+std::atomic<long long> g_replay_misses{0};
+
+class ReplayScorer : public Scorer {
+ public:
+  explicit ReplayScorer(int n) : n_(n) {}
+  int num_tokens() const override { return n_; }
+  std::vector<double> score(const std::string& id,
+                            const std::vector<int>& prefix) const override {
+    auto it = table_.find({id, prefix});
+    if (it != table_.end()) return it->second;
+    ++g_replay_misses;
+    return std::vector<double>(n_ + 1, -std::log(static_cast<double>(n_ + 1)));
+  }
+  void add(const std::string& id, std::vector<int> prefix, std::vector<double> row) {
+    check_normalized(row, static_cast<size_t>(n_) + 1, "replayed scorer row");
+    table_[{id, std::move(prefix)}] = std::move(row);
+  }
+
+ private:
+  int n_;
+  std::map<std::pair<std::string, std::vector<int>>, std::vector<double>> table_;
+};
+
 std::unique_ptr<Scorer> build_scorer(const orc_scorer* s) {
   if (s->kind == 0) return std::make_unique<UniformScorer>(s->num_tokens);
+  if (s->kind == 3) {
+    auto r = std::make_unique<ReplayScorer>(s->num_tokens);
+    const int w = s->order - 1 > 0 ? s->order - 1 : 1;
+    for (int k = 0; k < s->n_entries; ++k) {
+      std::vector<int> ctx(s->ctx + (size_t)k * w, s->ctx + (size_t)k * w + s->ctx_len[k]);
+      std::vector<double> lp(s->logp + (size_t)k * (s->num_tokens + 1),
+                             s->logp + (size_t)(k + 1) * (s->num_tokens + 1));
+      r->add(s->replay_ids[s->ent_utt[k]], std::move(ctx), std::move(lp));
+    }
+    return r;
+  }
   if (s->kind == 2)
     return std::make_unique<LoopScorer>(s->num_tokens, s->loop_token,
                                         s->p_loop);
@@ -248,6 +289,12 @@ int ref_verify(const char* suite, int trials, int max_frames, int max_vocab,
   else if (s == "exhaustive") r = verify_exhaustive_beam(trials, seed);
   else return -1;
   return r.failures;
+}
+
+long long ref_replay_misses(int reset) {
+  const long long m = g_replay_misses.load();
+  if (reset) g_replay_misses = 0;
+  return m;
 }
 
 int ref_num_threads(void) {

@@ -88,6 +88,9 @@ def lib() -> C.CDLL:
     L.bl_decoder_set_options.argtypes = [vp, C.c_int, C.c_int, C.c_double]
     L.bl_decoder_set_stream.argtypes = [vp, vp]
     L.bl_decoder_set_step_mode.argtypes = [vp, C.c_int]
+    L.bl_decoder_set_record.argtypes = [vp, C.c_int]
+    L.bl_decoder_record_count.argtypes = [vp]
+    L.bl_decoder_record_get.argtypes = [vp, C.c_int, ip, ip, C.POINTER(ip), C.POINTER(dp)]
     L.bl_decoder_destroy.argtypes = [vp]
     L.bl_decode.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.c_int, C.POINTER(vp)]
     L.bl_results_count.argtypes = [vp]
@@ -114,6 +117,12 @@ def lib() -> C.CDLL:
     L.bl_encoder_forward.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int]
     L.bl_encoder_launches.argtypes = [vp]
     L.bl_encoder_destroy.argtypes = [vp]
+    L.bl_transformer_num_weights.argtypes = [vp]
+    L.bl_transformer_num_weights.restype = C.c_size_t
+    L.bl_scorer_create_transformer.argtypes = [C.c_int, vp, vp, C.c_size_t, C.POINTER(vp)]
+    L.bl_decode_memory.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.c_int, vp, C.c_int,
+                                   C.POINTER(vp)]
+    L.bl_encoder_forward_mem.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, C.c_int]
     L.bl_gemm_bf16.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int,
                                vp, vp, vp, C.c_int, C.c_float, vp, C.c_int, vp]
     _lib = L
@@ -442,6 +451,24 @@ class Decoder:
     def set_stream(self, stream_ptr: int) -> None:
         lib().bl_decoder_set_stream(self._h, C.c_void_p(stream_ptr or None))
 
+    def set_record(self, on: bool) -> None:
+        """Record the network scorer's rows of every live hypothesis (tests)."""
+        _check(lib().bl_decoder_set_record(self._h, 1 if on else 0))
+
+    def records(self):
+        """[(utterance index, prefix tuple, float64 row)] of the last decode."""
+        L = lib()
+        out = []
+        u, n = C.c_int(), C.c_int()
+        pp, rp = C.POINTER(C.c_int)(), C.POINTER(C.c_double)()
+        V = self.scorer.num_tokens() + 1
+        for i in range(L.bl_decoder_record_count(self._h)):
+            _check(L.bl_decoder_record_get(self._h, i, C.byref(u), C.byref(n), C.byref(pp),
+                                           C.byref(rp)))
+            pre = tuple(pp[k] for k in range(n.value))
+            out.append((u.value, pre, np.ctypeslib.as_array(rp, shape=(V,)).copy()))
+        return out
+
     def __del__(self):
         if getattr(self, "_h", None) is not None and _lib is not None:
             _lib.bl_decoder_destroy(self._h)
@@ -449,9 +476,12 @@ class Decoder:
 
     def decode_raw(self, descs: Sequence[Tuple[str, int, int, int]],
                    on_device: bool, counters: Optional[DecodeCounters] = None,
-                   frame_shift_ms: int = 10) -> "ResultSet":
+                   frame_shift_ms: int = 10, memory: Optional[int] = None,
+                   mem_frames: int = 0) -> "ResultSet":
         """descs: (id, num_frames, vocab, data pointer). The bl_utt array is
-        built vectorised (one ids buffer, numpy structured records)."""
+        built vectorised (one ids buffer, numpy structured records).
+        memory: device pointer to the encoder output bf16 [n][mem_frames][d]
+        (required by the Transformer scorer)."""
         n = len(descs)
         ids = [d[0] for d in descs]
         key = (id(descs), n, frame_shift_ms)
@@ -476,8 +506,13 @@ class Decoder:
             self._desc_cache = (key, descs, arr)
         rec = arr[0]
         h = C.c_void_p()
-        _check(lib().bl_decode(self._h, n, rec.ctypes.data_as(C.POINTER(_Utt)),
-                               1 if on_device else 0, C.byref(h)))
+        if memory is not None:
+            _check(lib().bl_decode_memory(self._h, n, rec.ctypes.data_as(C.POINTER(_Utt)),
+                                          1 if on_device else 0, C.c_void_p(memory),
+                                          mem_frames, C.byref(h)))
+        else:
+            _check(lib().bl_decode(self._h, n, rec.ctypes.data_as(C.POINTER(_Utt)),
+                                   1 if on_device else 0, C.byref(h)))
         try:
             return self._collect(h, counters, ids)
         finally:

@@ -21,6 +21,7 @@
 
 #include "../../include/bl_b200.h"
 #include "decode.cuh"
+#include "decoder_net.cuh"
 #include "encoder.cuh"
 #include "gemm.cuh"
 
@@ -93,7 +94,15 @@ void check_normalized(const std::vector<double>& v, size_t expected,
 }  // namespace
 
 struct bl_scorer {
-  int kind = 0;  // 0 uniform, 1 table, 2 loop
+  int kind = 0;  // 0 uniform, 1 table, 2 loop, 3 transformer (device network)
+  bl::DecoderNet* net = nullptr;
+  int net_device = 0;
+  ~bl_scorer() {
+    if (net) {
+      cudaSetDevice(net_device);
+      bl::dec_destroy(net);
+    }
+  }
   int num_tokens = 0;
   int order = 1;
   std::map<std::vector<int>, std::vector<double>> table;
@@ -111,6 +120,8 @@ struct bl_scorer {
     return v;
   }
   std::vector<double> score(const std::vector<int>& prefix) const {
+    if (kind == 3)
+      throw std::logic_error("the transformer scorer runs on device inside the decoder");
     if (kind == 2) return loop_row();
     if (kind == 1) {  // scorer.cpp:53-62
       size_t n = std::min<size_t>(prefix.size(), order - 1);
@@ -229,6 +240,20 @@ struct bl_decoder {
   int step_mode = 0;
   DevBuf state, n_done;
   HostBuf h_done;
+  // network scorer (kind 3) and the encoder memory of the current call
+  bl::DecoderNet* net = nullptr;
+  const void* memory = nullptr;
+  int mem_frames = 0;
+  double net_ms = 0.0;
+  // record mode (tests): the scorer rows of every live hypothesis with its prefix
+  int record = 0;
+  struct Rec {
+    int utt;
+    std::vector<int> prefix;
+    std::vector<double> row;
+  };
+  std::vector<Rec> rec;
+  DevBuf rec_nb, nb_live;
 };
 
 struct bl_results {
@@ -252,6 +277,7 @@ struct bl_results {
 namespace {
 
 void upload_scorer(bl_decoder* d, const bl_scorer* s) {
+  d->net = s->kind == 3 ? s->net : nullptr;
   // rows: 0 = uniform fallback, then one row per entry
   const int V = s->num_tokens + 1;
   std::vector<double> rows = s->uniform_row();
@@ -336,6 +362,15 @@ float guard_float() {
 // Step-granular decode of all utterances of `p` in lockstep: one launch
 // per step; the host polls the finished-utterance counter every few steps.
 int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
+  if (d->net) {  // source-attention K/V of the encoder memory, KV cache, rows
+    CK(bl::dec_prepare(d->net, p.U, p.B, p.S + 1,
+                       static_cast<const __nv_bfloat16*>(d->memory) +
+                           (size_t)p.u0 * d->mem_frames * bl::dec_spec(d->net).d,
+                       d->mem_frames, st));
+    p.net_rows = 1;
+    d->nb_live.ensure(sizeof(int) * (size_t)(p.u0 + p.U));
+    p.nb_out = static_cast<int*>(d->nb_live.p);
+  }
   const size_t stride = bl::step_state_bytes(p.B, p.S);
   d->state.ensure(stride * (size_t)p.U);
   d->n_done.ensure(sizeof(unsigned));
@@ -346,14 +381,62 @@ int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
   p.n_done = static_cast<unsigned*>(d->n_done.p);
   int launches = 0;
   const int poll = 4;
+  const int V = p.V, B = p.B;
+  std::vector<std::vector<double>> rec_rows;  // record mode: att rows per step
+  if (d->record) {
+    d->rec_nb.ensure(sizeof(int) * (size_t)p.U * (p.S + 2));
+    CK(cudaMemsetAsync(d->rec_nb.p, 0, sizeof(int) * (size_t)p.U * (p.S + 2), st));
+    p.rec_nb = static_cast<int*>(d->rec_nb.p);
+  }
   for (int l = 1; l <= p.S + 1; ++l) {
     p.step_l = l;
+    if (d->net && l <= p.S) {  // att rows of the beam entering step l
+      CK(bl::dec_step(d->net, l, p.hist + (size_t)p.u0 * (p.S + 1) * p.B, (p.S + 1) * p.B,
+                      static_cast<const int*>(d->nb_live.p) + p.u0, d->cfg.ctc_weight, st));
+      p.sc_rows = bl::dec_att(d->net);
+      p.sc_rowsf = bl::dec_attf(d->net);
+      launches += bl::dec_launches_per_step(d->net);
+      if (d->record) {
+        rec_rows.emplace_back((size_t)p.U * B * V);
+        CK(cudaMemcpyAsync(rec_rows.back().data(), p.sc_rows, sizeof(double) * rec_rows.back().size(),
+                           cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+      }
+    }
     CK(bl::launch_decode(p, st));
     ++launches;
     if (l % poll == 0 || l == p.S + 1) {
       CK(cudaMemcpyAsync(d->h_done.p, d->n_done.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
       if (*static_cast<unsigned*>(d->h_done.p) >= (unsigned)p.U) break;
+    }
+  }
+  if (d->record && d->net) {  // pair each recorded row with its prefix
+    std::vector<int> nbh((size_t)p.U * (p.S + 2));
+    std::vector<bl::HistRec> hh((size_t)p.U * (p.S + 1) * B);
+    CK(cudaMemcpyAsync(nbh.data(), d->rec_nb.p, sizeof(int) * nbh.size(), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hh.data(), p.hist, sizeof(bl::HistRec) * hh.size(), cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t li = 0; li < rec_rows.size(); ++li) {
+      const int l = (int)li + 1;
+      for (int u = 0; u < p.U; ++u) {
+        const int nb = nbh[(size_t)u * (p.S + 2) + l];
+        for (int k = 0; k < nb; ++k) {
+          bl_decoder::Rec r;
+          r.utt = u + p.u0;
+          r.prefix.resize(l - 1);
+          int slot = k;
+          for (int st2 = l - 1; st2 >= 1; --st2) {
+            const bl::HistRec& h = hh[((size_t)u * (p.S + 1) + st2) * B + slot];
+            r.prefix[st2 - 1] = h.token;
+            slot = h.parent;
+          }
+          const double* row = rec_rows[li].data() + ((size_t)u * B + k) * V;
+          r.row.assign(row, row + V);
+          d->rec.push_back(std::move(r));
+        }
+      }
     }
   }
   return launches;
@@ -576,7 +659,12 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   // chunking: one launch when grids are resident; otherwise ~600 utterances
   // (two waves of resident CTAs) per chunk so copies overlap decoding.
   // Step-granular mode: one group, one launch per decode step.
-  const bool stepm = d->step_mode != 0;
+  const bool stepm = d->step_mode != 0 || d->net != nullptr;
+  if (d->net) {
+    if (!d->memory)
+      throw std::invalid_argument("the transformer scorer needs the encoder memory "
+                                  "(bl_decode_memory)");
+  }
   const int nchunk = (on_device || stepm) ? 1 : std::max(1, std::min(16, U / 360));
   if ((int)d->ev_copy.size() < nchunk) {
     for (int k = (int)d->ev_copy.size(); k < nchunk; ++k) {
@@ -816,6 +904,41 @@ int bl_scorer_score(const bl_scorer* s, const int* prefix, int n, double* out) {
 
 void bl_scorer_destroy(bl_scorer* s) { delete s; }
 
+static bl::DecSpec dec_spec_of(const bl_transformer_spec* s) {
+  return bl::DecSpec{s->d_model, s->heads, s->d_ff, s->layers, s->vocab};
+}
+
+size_t bl_transformer_num_weights(const bl_transformer_spec* spec) {
+  if (!spec || !bl::dec_validate(dec_spec_of(spec)).empty()) return 0;
+  return bl::dec_num_weights(dec_spec_of(spec));
+}
+
+int bl_scorer_create_transformer(int device, const bl_transformer_spec* spec,
+                                 const float* weights, size_t n_weights, bl_scorer** out) {
+  return guarded([&] {
+    if (!spec || !weights || !out) throw std::invalid_argument("null argument");
+    const bl::DecSpec s = dec_spec_of(spec);
+    const std::string why = bl::dec_validate(s);
+    if (!why.empty()) throw std::invalid_argument(why);
+    if (n_weights != bl::dec_num_weights(s))
+      throw std::invalid_argument("decoder weight count mismatch: expected " +
+                                  std::to_string(bl::dec_num_weights(s)) + ", got " +
+                                  std::to_string(n_weights));
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev)
+      throw BlError{BL_CUDA_ERROR, "no CUDA device " + std::to_string(device)};
+    CK(cudaSetDevice(device));
+    std::unique_ptr<bl_scorer> sc(new bl_scorer);
+    sc->kind = 3;
+    sc->num_tokens = s.vocab - 1;
+    sc->net_device = device;
+    CK(bl::dec_create(s, weights, &sc->net));
+    *out = sc.release();
+    return BL_OK;
+  });
+}
+
 int bl_decoder_create(int device, const bl_config* cfg, const bl_scorer* scorer,
                       bl_decoder** out) {
   return guarded([&] {
@@ -854,6 +977,25 @@ int bl_decoder_set_options(bl_decoder* d, int nbest, int exact, double slack) {
   });
 }
 
+int bl_decoder_set_record(bl_decoder* d, int on) {
+  d->record = on ? 1 : 0;
+  d->rec.clear();
+  return BL_OK;
+}
+
+int bl_decoder_record_count(const bl_decoder* d) { return (int)d->rec.size(); }
+
+int bl_decoder_record_get(const bl_decoder* d, int i, int* utt, int* len, const int** prefix,
+                          const double** row) {
+  if (i < 0 || i >= (int)d->rec.size()) return fail(BL_INVALID_ARGUMENT, "record index out of range");
+  const auto& r = d->rec[i];
+  *utt = r.utt;
+  *len = (int)r.prefix.size();
+  *prefix = r.prefix.data();
+  *row = r.row.data();
+  return BL_OK;
+}
+
 int bl_decoder_set_step_mode(bl_decoder* d, int on) {
   d->step_mode = on ? 1 : 0;
   return BL_OK;
@@ -880,7 +1022,25 @@ void bl_decoder_destroy(bl_decoder* d) {
 
 int bl_decode(bl_decoder* d, int n, const bl_utt* utts, int on_device,
               bl_results** out) {
-  return guarded([&] { return decode_impl(d, n, utts, on_device, out); });
+  return guarded([&] {
+    d->memory = nullptr;
+    d->mem_frames = 0;
+    return decode_impl(d, n, utts, on_device, out);
+  });
+}
+
+int bl_decode_memory(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
+                     const void* memory, int mem_frames, bl_results** out) {
+  return guarded([&] {
+    if (!d->net) throw std::invalid_argument("bl_decode_memory needs a transformer scorer");
+    if (!memory || mem_frames < 1) throw std::invalid_argument("memory frames must be >= 1");
+    d->memory = memory;
+    d->mem_frames = mem_frames;
+    d->rec.clear();
+    const int r = decode_impl(d, n, utts, grids_on_device, out);
+    d->memory = nullptr;
+    return r;
+  });
 }
 
 int bl_results_count(const bl_results* r) { return (int)r->r.size(); }
@@ -1033,7 +1193,24 @@ int bl_encoder_forward(bl_encoder* e, int n, int frames_in, const float* fbank,
                                   " frames (need >= 7)");
     CK(cudaSetDevice(e->device));
     CK(bl::enc_forward(e->impl, n, frames_in, fbank, fbank_on_device != 0, grid, e->chunk,
-                       &e->launches));
+                       &e->launches, nullptr));
+    if (sync) CK(cudaStreamSynchronize(bl::enc_stream(e->impl)));
+    return BL_OK;
+  });
+}
+
+int bl_encoder_forward_mem(bl_encoder* e, int n, int frames_in, const float* fbank,
+                           int fbank_on_device, float* grid, void* memory, int sync) {
+  return guarded([&] {
+    if (n < 0) throw std::invalid_argument("segment count must be >= 0");
+    if (n == 0) return BL_OK;
+    if (!fbank || !grid) throw std::invalid_argument("null fbank or grid");
+    if (bl::enc_frames_out(frames_in) < 1)
+      throw std::invalid_argument("segment too short: " + std::to_string(frames_in) +
+                                  " frames (need >= 7)");
+    CK(cudaSetDevice(e->device));
+    CK(bl::enc_forward(e->impl, n, frames_in, fbank, fbank_on_device != 0, grid, e->chunk,
+                       &e->launches, static_cast<__nv_bfloat16*>(memory)));
     if (sync) CK(cudaStreamSynchronize(bl::enc_stream(e->impl)));
     return BL_OK;
   });

@@ -101,6 +101,8 @@ struct KParams {
   // per-hypothesis scorer rows (network scorer): hypothesis k of utterance u
   // reads row u * B + k of sc_rows / sc_rowsf at every step
   int net_rows;
+  int* rec_nb;  // optional [U][S+2]: live beam size at the start of each step
+  int* nb_out;  // optional [U]: live beam size entering the next step (0 once finished)
 };
 
 // Dynamic shared-memory plan (identical on host and device).

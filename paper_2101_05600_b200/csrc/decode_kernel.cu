@@ -476,7 +476,10 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
   // ---------------------------------------------------------- step loop
   for (int l = stepm ? P.step_l : 1;; ++l) {
     const int cur = (l - 1) & 1, nxt = l & 1;
-    if (l > ud.max_steps) break;  // batched.cpp:125-128
+    if (l > ud.max_steps) {  // batched.cpp:125-128
+      if (P.nb_out && tid == 0) P.nb_out[u] = 0;
+      break;
+    }
     const int nb = sh.nb;
 
     // ---- P1: windows, eos candidates, offsets (warp 0) ----
@@ -518,6 +521,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       const int r0 = sh.b_row[cur][0];
       const bool same = __all_sync(0xffffffffu, j >= nb || sh.b_row[cur][j] == r0);
       if (lane == 0) {
+        if (P.rec_nb) P.rec_nb[(size_t)u * (P.S + 2) + l] = nb;
         sh.row_same = same ? r0 : -1;
         sh.s = ws;
         sh.e = we;
@@ -1208,6 +1212,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       if (sh.nchild == 0) stop = true;
       sh.nb = sh.nchild;
       sh.done = stop ? 1 : 0;
+      if (P.nb_out) P.nb_out[u] = stop ? 0 : sh.nchild;
     }
     __syncthreads();
     PROF_MARK(10);

@@ -1,0 +1,699 @@
+// decoder_net.cu — the Transformer attention decoder as a device scorer
+// (SURVEY §8 a'2), batched over every hypothesis of every utterance and run
+// once per decode step between launches of the step-granular search kernel.
+//
+// Step l for hypothesis slot k of utterance u (row R = u*B + k):
+//   token   = sos (= |C|) at l = 1, else hist[u][l-1][k].token
+//   anc[p]  = the slot, in beam p+1, of the ancestor whose KV entry holds
+//             position p (walk of the search's back-pointers; anc[l-1] = k)
+//   x = emb[token] * sqrt(d) + PE[l-1]
+//   per layer:  x += O(SelfAttn(LN1 x))   keys/values: cache[p][anc[p]], p < l
+//               x += O2(SrcAttn(LN2 x))   memory K/V precomputed per group
+//               x += FFN(LN3 x)
+//   att = log_softmax(out(LN x)) with an fp64 normaliser -> att / attf rows
+//
+// HBM layout (group of U utterances, S step positions):
+//   kvc  bf16 [L][U][S][B][2d]   self-attention K|V per (position, slot)
+//   kv2  bf16 [L][U*T2][2d]      source-attention K|V of the encoder memory
+//   X f32 / Y, QKV, AO bf16 / H bf16 [U*B][...]; logits f32, att f64, attf f32 [U*B][V]
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "decoder_net.cuh"
+#include "encoder.cuh"
+#include "gemm.cuh"
+
+namespace bl {
+namespace {
+
+constexpr int kDk = 64;
+
+uint16_t to_bf16(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+// tokens and ancestor slots of every hypothesis row. The ancestry is built
+// incrementally: row R = (u, k) at step l inherits its parent's row of the
+// previous step's table (anc_prev) and appends its own slot at position l-1,
+// so each step is one parallel gather instead of a pointer chase.
+__global__ void dec_tok_kernel(int l, const HistRec* __restrict__ hist, int hstride, int U, int B,
+                               int V, int* __restrict__ tok, int* __restrict__ par) {
+  const int R = blockIdx.x * blockDim.x + threadIdx.x;
+  if (R >= U * B) return;
+  const int u = R / B, k = R - u * B;
+  int t = V - 1, pj = 0;
+  if (l > 1) {
+    const HistRec h = hist[(size_t)u * hstride + (size_t)(l - 1) * B + k];
+    t = (h.token >= 0 && h.token < V) ? h.token : V - 1;  // dead slot: any valid row
+    pj = (h.parent >= 0 && h.parent < B) ? h.parent : 0;
+  }
+  tok[R] = t;
+  par[R] = pj;
+}
+
+__global__ void dec_anc_kernel(int l, int U, int B, int S, const int* __restrict__ par,
+                               const int* __restrict__ anc_prev, int* __restrict__ anc) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (size_t)U * B * l) return;
+  const int R = (int)(i / l), p = (int)(i - (size_t)R * l);
+  const int u = R / B, k = R - u * B;
+  anc[(size_t)R * S + p] =
+      p == l - 1 ? k : anc_prev[((size_t)u * B + par[R]) * S + p];
+}
+
+// x = emb[token] * sqrt(d) + pe[l-1]; one warp per row
+__global__ void dec_embed_kernel(const int* __restrict__ tok, const float* __restrict__ emb,
+                                 const float* __restrict__ pe_row, int d, float scale,
+                                 float* __restrict__ X, int M) {
+  const int R = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (R >= M) return;
+  const float* e = emb + (size_t)tok[R] * d;
+  float* x = X + (size_t)R * d;
+  for (int c = lane; c < d; c += 32) x[c] = e[c] * scale + pe_row[c];
+}
+
+// Self-attention of the new position over each hypothesis' own prefix.
+// Grid (U, heads), one warp per slot: the warps of one CTA are the beam of
+// one utterance, so ancestor entries shared by several hypotheses are served
+// from L1 (the live beam's union of entries is ~12% of nb*l on the bench
+// model). The step's K/V go to the cache at position l-1; scores use 4 lanes
+// per position (16 dims each), 8 positions per pass; the weighted sum has each
+// lane own two dims. Finished utterances and dead slots (k >= nb) return at
+// once.
+__global__ void dec_self_attn_kernel(int l, const __nv_bfloat16* __restrict__ qkv, int d, int B,
+                                     const int* __restrict__ anc, int S,
+                                     const int* __restrict__ nb_in,
+                                     __nv_bfloat16* __restrict__ cache,
+                                     __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float sa_sm[];
+  const int u = blockIdx.x, h = blockIdx.y;
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nb = l == 1 ? 1 : nb_in[u];
+  if (k >= nb) return;
+  float* sc = sa_sm + (size_t)k * S;                                        // [S] scores
+  int* sl = reinterpret_cast<int*>(sa_sm + (size_t)B * S) + (size_t)k * S;  // [S] slots
+  const int R = u * B + k;
+  const __nv_bfloat16* row = qkv + (size_t)R * 3 * d;
+  const size_t d2 = 2 * (size_t)d;
+  auto kv_at = [&](int p, int slot) {
+    return cache + (((size_t)u * S + p) * B + slot) * d2 + h * kDk;
+  };
+  {  // this step's K and V into the cache (position l-1, own slot)
+    const uint32_t kc = reinterpret_cast<const uint32_t*>(row + d + h * kDk)[lane];
+    const uint32_t vc = reinterpret_cast<const uint32_t*>(row + 2 * d + h * kDk)[lane];
+    __nv_bfloat16* dst = kv_at(l - 1, k);
+    reinterpret_cast<uint32_t*>(dst)[lane] = kc;
+    reinterpret_cast<uint32_t*>(dst + d)[lane] = vc;
+  }
+  for (int p = lane; p < l; p += 32) sl[p] = (p == l - 1) ? k : anc[(size_t)R * S + p];
+  __syncwarp();  // cache writes and slot list visible to the warp
+  const int qd = lane & 3, pp = lane >> 2;
+  float q[16];
+  {
+    const uint4* qs = reinterpret_cast<const uint4*>(row + h * kDk + qd * 16);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const uint4 w = qs[i];
+      const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(b2[j]);
+        q[i * 8 + 2 * j] = f.x;
+        q[i * 8 + 2 * j + 1] = f.y;
+      }
+    }
+  }
+  const float scale = rsqrtf((float)kDk);
+  float m = -INFINITY;
+  for (int p0 = 0; p0 < l; p0 += 8) {
+    const int p = p0 + pp;
+    float s = 0.f;
+    if (p < l) {
+      const uint4* ks = reinterpret_cast<const uint4*>(kv_at(p, sl[p]) + qd * 16);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const uint4 w = ks[i];
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __bfloat1622float2(b2[j]);
+          s = fmaf(q[i * 8 + 2 * j], f.x, s);
+          s = fmaf(q[i * 8 + 2 * j + 1], f.y, s);
+        }
+      }
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    if (p < l) {
+      s *= scale;
+      if (qd == 0) sc[p] = s;
+      m = fmaxf(m, s);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __syncwarp();
+  float sum = 0.f;
+  for (int p = lane; p < l; p += 32) {
+    const float e = expf(sc[p] - m);
+    sc[p] = e;
+    sum += e;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  __syncwarp();
+  float a0 = 0.f, a1 = 0.f;
+  for (int p = 0; p < l; ++p) {
+    const float w = sc[p];
+    const float2 v = __bfloat1622float2(
+        reinterpret_cast<const __nv_bfloat162*>(kv_at(p, sl[p]) + d)[lane]);
+    a0 = fmaf(w, v.x, a0);
+    a1 = fmaf(w, v.y, a1);
+  }
+  const float inv = 1.f / sum;
+  reinterpret_cast<__nv_bfloat162*>(out + (size_t)R * d + h * kDk)[lane] =
+      __floats2bfloat162_rn(a0 * inv, a1 * inv);
+}
+
+// Source attention on the warp-level tensor path. Per (utterance, head) the
+// B hypotheses' queries share the memory K/V, so the op is bound by reading
+// K/V once (HBM); the products are tiny (16 x 64 x T) and use
+// mma.sync.m16n8k16 bf16 with fp32 accumulation. Grid (U, heads, ceil(B/16)),
+// 4 warps; K/V staged in shared memory (144-byte rows: conflict-free
+// ldmatrix); each warp takes 64-key chunks with an online softmax, and the
+// warps' partial (max, sum, O) are merged at the end.
+constexpr int kXW = 4, kXKPitch = 72;  // bf16 elements per staged row
+
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t& b0, uint32_t& b1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(b0), "=r"(b1)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& b0, uint32_t& b1) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];"
+               : "=r"(b0), "=r"(b1)
+               : "r"(addr));
+}
+__device__ __forceinline__ uint32_t pk_bf16(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(kXW * 32)
+    dec_cross_attn_mma_kernel(int l, const int* __restrict__ nb_in,
+                              const __nv_bfloat16* __restrict__ q,
+                              const __nv_bfloat16* __restrict__ kv2, int T, int d, int B,
+                              __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char xm_sm[];
+  if (l > 1 && nb_in[blockIdx.x] <= (int)blockIdx.z * 16) return;  // finished utterance
+  const int Tp = (T + 63) & ~63;
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(xm_sm);
+  __nv_bfloat16* Vs = Ks + (size_t)Tp * kXKPitch;
+  float* mrg = reinterpret_cast<float*>(Vs + (size_t)Tp * kXKPitch);  // [warps][16*64 + 32]
+  const int u = blockIdx.x, h = blockIdx.y, q0 = blockIdx.z * 16;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t ld = 2 * (size_t)d;
+  const __nv_bfloat16* base = kv2 + (size_t)u * T * ld + h * kDk;
+  for (int i = threadIdx.x; i < Tp * 8; i += blockDim.x) {  // 8 x 16 B per row
+    const int t = i >> 3, c = i & 7;
+    uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
+    if (t < T) {
+      kk = reinterpret_cast<const uint4*>(base + t * ld)[c];
+      vv = reinterpret_cast<const uint4*>(base + t * ld + d)[c];
+    }
+    reinterpret_cast<uint4*>(Ks + (size_t)t * kXKPitch)[c] = kk;
+    reinterpret_cast<uint4*>(Vs + (size_t)t * kXKPitch)[c] = vv;
+  }
+  // query fragments: rows q0 + lane/4 (+8), dims kc*16 + 2*(lane%4) (+8)
+  uint32_t qa[4][4];
+  {
+    const int r0 = q0 + (lane >> 2), r1 = r0 + 8, c = 2 * (lane & 3);
+    const __nv_bfloat16* p0 = q + ((size_t)u * B + r0) * d + h * kDk + c;
+    const __nv_bfloat16* p1 = q + ((size_t)u * B + r1) * d + h * kDk + c;
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      qa[kc][0] = r0 < B ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16) : 0u;
+      qa[kc][1] = r1 < B ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16) : 0u;
+      qa[kc][2] = r0 < B ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16 + 8) : 0u;
+      qa[kc][3] = r1 < B ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16 + 8) : 0u;
+    }
+  }
+  __syncthreads();
+  const float sc = 1.4426950408889634f * rsqrtf((float)kDk);  // log2(e) / sqrt(dk)
+  float o[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // rows lane/4, lane/4 + 8
+  const uint32_t ks_base = (uint32_t)__cvta_generic_to_shared(Ks);
+  const uint32_t vs_base = (uint32_t)__cvta_generic_to_shared(Vs);
+  const int lr = lane & 7, lm = (lane >> 3) & 1;  // ldmatrix row / matrix of this lane
+  for (int key0 = warp * 64; key0 < T; key0 += kXW * 64) {
+    float s[8][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        uint32_t b0, b1;
+        ldsm_x2(ks_base + (uint32_t)(((key0 + nt * 8 + lr) * kXKPitch + kc * 16 + lm * 8) * 2),
+                b0, b1);
+        mma16816(s[nt], qa[kc], b0, b1);
+      }
+    }
+    float c0 = -INFINITY, c1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const int key = key0 + nt * 8 + 2 * (lane & 3);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const bool ok = key + j < T;
+        s[nt][j] = ok ? s[nt][j] * sc : -INFINITY;
+        s[nt][2 + j] = ok ? s[nt][2 + j] * sc : -INFINITY;
+        c0 = fmaxf(c0, s[nt][j]);
+        c1 = fmaxf(c1, s[nt][2 + j]);
+      }
+    }
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 1));
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 2));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 1));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 2));
+    const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
+    const float a0 = exp2f(m0 - n0), a1 = exp2f(m1 - n1);
+    m0 = n0;
+    m1 = n1;
+    l0 *= a0;
+    l1 *= a1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i][0] *= a0; o[i][1] *= a0; o[i][2] *= a1; o[i][3] *= a1;
+    }
+    uint32_t pa[4][4];
+#pragma unroll
+    for (int nt = 0; nt < 8; ++nt) {
+      const float p0 = exp2f(s[nt][0] - n0), p1 = exp2f(s[nt][1] - n0);
+      const float p2 = exp2f(s[nt][2] - n1), p3 = exp2f(s[nt][3] - n1);
+      l0 += p0 + p1;
+      l1 += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2] = pk_bf16(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pk_bf16(p2, p3);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        uint32_t b0, b1;
+        ldsm_x2_t(vs_base + (uint32_t)(((key0 + kk * 16 + lm * 8 + lr) * kXKPitch + dt * 8) * 2),
+                  b0, b1);
+        mma16816(o[dt], pa[kk], b0, b1);
+      }
+    }
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  // merge the warps: O = sum_w O_w 2^(m_w - M), L = sum_w l_w 2^(m_w - M)
+  float* mw = mrg + warp * (16 * 64 + 32);
+  {
+    const int r0 = lane >> 2, c = 2 * (lane & 3);
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      mw[r0 * 64 + dt * 8 + c] = o[dt][0];
+      mw[r0 * 64 + dt * 8 + c + 1] = o[dt][1];
+      mw[(r0 + 8) * 64 + dt * 8 + c] = o[dt][2];
+      mw[(r0 + 8) * 64 + dt * 8 + c + 1] = o[dt][3];
+    }
+    if ((lane & 3) == 0) {
+      mw[1024 + r0] = m0;
+      mw[1024 + r0 + 8] = m1;
+      mw[1040 + r0] = l0;
+      mw[1040 + r0 + 8] = l1;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 16 * 32; i += blockDim.x) {  // (row, dim pair)
+    const int r = i >> 5, c = (i & 31) * 2;
+    if (q0 + r >= B) continue;
+    float M = -INFINITY;
+    for (int w = 0; w < kXW; ++w) M = fmaxf(M, mrg[w * (16 * 64 + 32) + 1024 + r]);
+    float L = 0.f, x0 = 0.f, x1 = 0.f;
+    for (int w = 0; w < kXW; ++w) {
+      const float* pw = mrg + w * (16 * 64 + 32);
+      const float mwv = pw[1024 + r];
+      if (mwv == -INFINITY) continue;  // warp saw no keys
+      const float f = exp2f(mwv - M);
+      L += pw[1040 + r] * f;
+      x0 += pw[r * 64 + c] * f;
+      x1 += pw[r * 64 + c + 1] * f;
+    }
+    reinterpret_cast<__nv_bfloat162*>(out + ((size_t)u * B + q0 + r) * d + h * kDk)[c / 2] =
+        __floats2bfloat162_rn(x0 / L, x1 / L);
+  }
+}
+
+// att = logits - logsumexp(logits) with the normaliser in fp64 (rows then
+// satisfy the reference's check_normalized to ~1e-15); attf for the
+// certified fp32 bulk keys. One CTA per row.
+__global__ void __launch_bounds__(256)
+    dec_log_softmax64_kernel(const float* __restrict__ logits, int V, double lam,
+                             double* __restrict__ att, float* __restrict__ attf) {
+  __shared__ double red[8];
+  const float* x = logits + (size_t)blockIdx.x * V;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float mf = -INFINITY;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) mf = fmaxf(mf, x[i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, o));
+  if (lane == 0) red[warp] = mf;
+  __syncthreads();
+  double m = red[0];
+  for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
+  __syncthreads();
+  double s = 0.0;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) s += exp((double)x[i] - m);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) red[warp] = s;
+  __syncthreads();
+  s = 0.0;
+  for (int w = 0; w < 8; ++w) s += red[w];
+  const double lse = m + log(s);
+  double* a = att + (size_t)blockIdx.x * V;
+  float* af = attf + (size_t)blockIdx.x * V;
+  const double w1 = lam <= 0.0 ? 1.0 : 1.0 - lam;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const double v = (double)x[i] - lse;
+    a[i] = v;
+    af[i] = lam >= 1.0 ? 0.f : (float)(w1 * v);
+  }
+}
+
+size_t xm_smem(int T) {
+  const size_t Tp = (size_t)((T + 63) & ~63);
+  return 2 * Tp * kXKPitch * 2 + (size_t)kXW * (16 * 64 + 32) * 4;
+}
+
+}  // namespace
+
+struct DecLayer {
+  float *ln1g, *ln1b, *bqkv, *bo, *ln2g, *ln2b, *bq2, *bkv2, *bo2, *ln3g, *ln3b, *b1, *b2;
+  __nv_bfloat16 *wqkv, *wo, *wq2, *wkv2, *wo2, *w1, *w2;
+};
+
+struct DecoderNet {
+  DecSpec s;
+  void* wbuf = nullptr;
+  float* emb = nullptr;
+  std::vector<DecLayer> L;
+  float *ang, *anb, *bout;
+  __nv_bfloat16* wout;
+  float* pe = nullptr;
+  int pe_rows = 0;
+  // group state
+  int U = 0, B = 0, S = 0, T2 = 0;
+  void* ws = nullptr;
+  size_t ws_bytes = 0;
+  __nv_bfloat16 *kvc = nullptr, *kv2 = nullptr, *Y = nullptr, *QKV = nullptr, *AO = nullptr,
+                *H = nullptr;
+  float *X = nullptr, *logits = nullptr, *attf = nullptr;
+  double* att = nullptr;
+  int *anc2[2] = {nullptr, nullptr}, *tok = nullptr, *par = nullptr;
+
+  ~DecoderNet() {
+    if (wbuf) cudaFree(wbuf);
+    if (ws) cudaFree(ws);
+    if (pe) cudaFree(pe);
+  }
+
+  cudaError_t load(const float* w) {
+    const size_t d = s.d, ff = s.dff, V = s.vocab;
+    std::vector<float> f32;
+    std::vector<uint16_t> b16;
+    std::vector<std::pair<bool, size_t>> slots;
+    auto put32 = [&](const float* p, size_t n) {
+      slots.push_back({false, f32.size()});
+      f32.insert(f32.end(), p, p + n);
+      while (f32.size() % 32) f32.push_back(0.f);
+    };
+    auto put16 = [&](const float* p, size_t n) {
+      slots.push_back({true, b16.size()});
+      for (size_t i = 0; i < n; ++i) b16.push_back(to_bf16(p[i]));
+      while (b16.size() % 64) b16.push_back(0);
+    };
+    const float* p = w;
+    put32(p, V * d); p += V * d;  // embed.w (fp32, gathered)
+    for (int l = 0; l < s.layers; ++l) {
+      // self-attention block: ln1, q, k, v, o
+      put32(p, d); p += d;
+      put32(p, d); p += d;
+      {
+        std::vector<float> wq(3 * d * d), bq(3 * d);
+        for (int j = 0; j < 3; ++j) {
+          std::memcpy(&wq[j * d * d], p, d * d * 4); p += d * d;
+          std::memcpy(&bq[j * d], p, d * 4); p += d;
+        }
+        put16(wq.data(), wq.size());
+        put32(bq.data(), bq.size());
+      }
+      put16(p, d * d); p += d * d;  // wo
+      put32(p, d); p += d;          // bo
+      // source attention block: ln2, q2, k2, v2, o2
+      put32(p, d); p += d;
+      put32(p, d); p += d;
+      put16(p, d * d); p += d * d;  // wq2
+      put32(p, d); p += d;          // bq2
+      {
+        std::vector<float> wkv(2 * d * d), bkv(2 * d);
+        for (int j = 0; j < 2; ++j) {
+          std::memcpy(&wkv[j * d * d], p, d * d * 4); p += d * d;
+          std::memcpy(&bkv[j * d], p, d * 4); p += d;
+        }
+        put16(wkv.data(), wkv.size());
+        put32(bkv.data(), bkv.size());
+      }
+      put16(p, d * d); p += d * d;  // wo2
+      put32(p, d); p += d;          // bo2
+      put32(p, d); p += d;          // ln3.g
+      put32(p, d); p += d;          // ln3.b
+      put16(p, ff * d); p += ff * d;  // w1
+      put32(p, ff); p += ff;          // b1
+      put16(p, d * ff); p += d * ff;  // w2
+      put32(p, d); p += d;            // b2
+    }
+    put32(p, d); p += d;          // after_norm.g
+    put32(p, d); p += d;          // after_norm.b
+    put16(p, V * d); p += V * d;  // out.w
+    put32(p, V);                  // out.b
+    const size_t n32 = f32.size() * 4, n16 = b16.size() * 2;
+    cudaError_t e = cudaMalloc(&wbuf, n32 + n16);
+    if (e != cudaSuccess) return e;
+    float* d32 = static_cast<float*>(wbuf);
+    auto* d16 = reinterpret_cast<__nv_bfloat16*>(static_cast<char*>(wbuf) + n32);
+    if ((e = cudaMemcpy(d32, f32.data(), n32, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    if ((e = cudaMemcpy(d16, b16.data(), n16, cudaMemcpyHostToDevice)) != cudaSuccess) return e;
+    size_t k = 0;
+    auto f = [&]() { return d32 + slots[k++].second; };
+    auto h = [&]() { return d16 + slots[k++].second; };
+    emb = f();
+    L.resize(s.layers);
+    for (auto& y : L) {
+      y.ln1g = f(); y.ln1b = f(); y.wqkv = h(); y.bqkv = f(); y.wo = h(); y.bo = f();
+      y.ln2g = f(); y.ln2b = f(); y.wq2 = h(); y.bq2 = f(); y.wkv2 = h(); y.bkv2 = f();
+      y.wo2 = h(); y.bo2 = f(); y.ln3g = f(); y.ln3b = f(); y.w1 = h(); y.b1 = f();
+      y.w2 = h(); y.b2 = f();
+    }
+    ang = f(); anb = f(); wout = h(); bout = f();
+    return cudaSuccess;
+  }
+
+  cudaError_t ensure_pe(int rows) {
+    if (pe_rows >= rows) return cudaSuccess;
+    if (pe) cudaFree(pe);
+    pe = nullptr;
+    std::vector<float> hp((size_t)rows * s.d);
+    const float kf = -std::log(10000.0f) / s.d;
+    for (int t = 0; t < rows; ++t)
+      for (int i = 0; i < s.d; i += 2) {
+        const float a = (float)t * std::exp((float)i * kf);
+        hp[(size_t)t * s.d + i] = std::sin(a);
+        hp[(size_t)t * s.d + i + 1] = std::cos(a);
+      }
+    cudaError_t e = cudaMalloc(&pe, hp.size() * 4);
+    if (e != cudaSuccess) return e;
+    pe_rows = rows;
+    return cudaMemcpy(pe, hp.data(), hp.size() * 4, cudaMemcpyHostToDevice);
+  }
+
+  cudaError_t gemm(int M, int N, int K, const __nv_bfloat16* A, const __nv_bfloat16* Bw,
+                   int mode, const float* bias, float* of, __nv_bfloat16* ob, int ldo,
+                   cudaStream_t st) {
+    GemmDesc g;
+    g.M = M; g.N = N; g.K = K; g.A = A; g.lda = K; g.B = Bw; g.ldb = K;
+    g.mode = mode; g.bias = bias; g.out_f32 = of; g.out_bf16 = ob; g.ldo = ldo;
+    return gemm_bf16(g, st);
+  }
+};
+
+size_t dec_num_weights(const DecSpec& s) {
+  const size_t d = s.d, ff = s.dff, V = s.vocab;
+  size_t n = V * d;
+  n += (size_t)s.layers * (2 * (2 * d + 4 * (d * d + d)) + 2 * d + ff * d + ff + d * ff + d);
+  n += 2 * d + V * d + V;
+  return n;
+}
+
+std::string dec_validate(const DecSpec& s) {
+  if (s.d < 64 || s.d > 1024 || s.d % 64) return "decoder d_model must be a multiple of 64 in [64, 1024]";
+  if (s.heads < 1 || s.d != s.heads * kDk) return "decoder heads must give a head width of 64";
+  if (s.dff < 8 || s.dff % 8) return "decoder d_ff must be a positive multiple of 8";
+  if (s.layers < 1) return "decoder layers must be >= 1";
+  if (s.vocab < 2 || s.vocab % 4) return "decoder vocab must be >= 2 and a multiple of 4";
+  return "";
+}
+
+cudaError_t dec_create(const DecSpec& s, const float* weights, DecoderNet** out) {
+  auto* n = new DecoderNet;
+  n->s = s;
+  cudaError_t e = n->load(weights);
+  if (e != cudaSuccess) {
+    delete n;
+    return e;
+  }
+  *out = n;
+  return cudaSuccess;
+}
+
+void dec_destroy(DecoderNet* n) { delete n; }
+const DecSpec& dec_spec(const DecoderNet* n) { return n->s; }
+const double* dec_att(const DecoderNet* n) { return n->att; }
+const float* dec_attf(const DecoderNet* n) { return n->attf; }
+int dec_launches_per_step(const DecoderNet* n) { return 6 + 11 * n->s.layers; }
+
+cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16* memory, int T2,
+                        cudaStream_t st) {
+  const DecSpec& s = n->s;
+  const size_t d = s.d, M = (size_t)U * B, Lc = s.layers;
+  auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+  const size_t b_kvc = al(Lc * U * S * B * 2 * d * 2), b_kv2 = al(Lc * U * T2 * 2 * d * 2);
+  const size_t need = b_kvc + b_kv2 + al(M * d * 4) + 3 * al(M * d * 2) + al(M * 3 * d * 2) +
+                      al(M * s.dff * 2) + al(M * s.vocab * 4) * 2 + al(M * s.vocab * 8) +
+                      2 * al(M * S * 4) + 2 * al(M * 4);
+  cudaError_t e;
+  if (need > n->ws_bytes) {
+    if (n->ws) cudaFree(n->ws);
+    n->ws = nullptr;
+    n->ws_bytes = 0;
+    if ((e = cudaMalloc(&n->ws, need)) != cudaSuccess) return e;
+    n->ws_bytes = need;
+  }
+  char* p = static_cast<char*>(n->ws);
+  auto take = [&](size_t b) {
+    char* r = p;
+    p += al(b);
+    return r;
+  };
+  n->kvc = reinterpret_cast<__nv_bfloat16*>(take(Lc * U * S * B * 2 * d * 2));
+  n->kv2 = reinterpret_cast<__nv_bfloat16*>(take(Lc * U * T2 * 2 * d * 2));
+  n->X = reinterpret_cast<float*>(take(M * d * 4));
+  n->Y = reinterpret_cast<__nv_bfloat16*>(take(M * d * 2));
+  n->AO = reinterpret_cast<__nv_bfloat16*>(take(M * d * 2));
+  take(M * d * 2);  // spare
+  n->QKV = reinterpret_cast<__nv_bfloat16*>(take(M * 3 * d * 2));
+  n->H = reinterpret_cast<__nv_bfloat16*>(take(M * s.dff * 2));
+  n->logits = reinterpret_cast<float*>(take(M * s.vocab * 4));
+  n->attf = reinterpret_cast<float*>(take(M * s.vocab * 4));
+  n->att = reinterpret_cast<double*>(take(M * s.vocab * 8));
+  n->anc2[0] = reinterpret_cast<int*>(take(M * S * 4));
+  n->anc2[1] = reinterpret_cast<int*>(take(M * S * 4));
+  n->tok = reinterpret_cast<int*>(take(M * 4));
+  n->par = reinterpret_cast<int*>(take(M * 4));
+  n->U = U; n->B = B; n->S = S; n->T2 = T2;
+  if ((e = n->ensure_pe(S + 1)) != cudaSuccess) return e;
+  // source-attention K|V of the memory, once per group
+  for (int l = 0; l < s.layers; ++l) {
+    if ((e = n->gemm(U * T2, 2 * s.d, s.d, memory, n->L[l].wkv2, kPlain, n->L[l].bkv2, nullptr,
+                     n->kv2 + (size_t)l * U * T2 * 2 * d, 2 * s.d, st)) != cudaSuccess)
+      return e;
+  }
+  const size_t sa = (size_t)B * S * 8;
+  if (sa > 227 * 1024) return cudaErrorInvalidValue;
+  if ((e = cudaFuncSetAttribute(dec_self_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sa)) != cudaSuccess)
+    return e;
+  const size_t xm = xm_smem(T2);
+  if (xm > 227 * 1024) return cudaErrorInvalidValue;
+  return cudaFuncSetAttribute(dec_cross_attn_mma_kernel,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xm);
+}
+
+cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, const int* nb_live,
+                     double lambda, cudaStream_t st) {
+  const DecSpec& s = n->s;
+  const int U = n->U, B = n->B, S = n->S, T2 = n->T2, d = s.d, M = U * B;
+  if (l < 1 || l > S) return cudaErrorInvalidValue;
+  cudaError_t e;
+  dec_tok_kernel<<<(M + 127) / 128, 128, 0, st>>>(l, hist, hstride, U, B, s.vocab, n->tok,
+                                                  n->par);
+  int* anc = n->anc2[l & 1];
+  const size_t na = (size_t)M * l;
+  dec_anc_kernel<<<(unsigned)((na + 255) / 256), 256, 0, st>>>(l, U, B, S, n->par,
+                                                               n->anc2[(l - 1) & 1], anc);
+  dec_embed_kernel<<<(M * 32 + 255) / 256, 256, 0, st>>>(n->tok, n->emb,
+                                                         n->pe + (size_t)(l - 1) * d, d,
+                                                         std::sqrt((float)d), n->X, M);
+  const size_t sa = (size_t)B * S * 8;
+  const size_t xm = xm_smem(T2);
+  for (int li = 0; li < s.layers; ++li) {
+    const DecLayer& y = n->L[li];
+    layer_norm_bf16(d, n->X, M, y.ln1g, y.ln1b, n->Y, st);
+    if ((e = n->gemm(M, 3 * d, d, n->Y, y.wqkv, kPlain, y.bqkv, nullptr, n->QKV, 3 * d, st)) !=
+        cudaSuccess)
+      return e;
+    dec_self_attn_kernel<<<dim3(U, s.heads), 32 * B, sa, st>>>(
+        l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, n->AO);
+    if ((e = n->gemm(M, d, d, n->AO, y.wo, kResidual, y.bo, n->X, nullptr, d, st)) != cudaSuccess)
+      return e;
+    layer_norm_bf16(d, n->X, M, y.ln2g, y.ln2b, n->Y, st);
+    if ((e = n->gemm(M, d, d, n->Y, y.wq2, kPlain, y.bq2, nullptr, n->QKV, d, st)) != cudaSuccess)
+      return e;
+    dec_cross_attn_mma_kernel<<<dim3(U, s.heads, (B + 15) / 16), kXW * 32, xm, st>>>(
+        l, nb_live, n->QKV, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, d, B, n->AO);
+    if ((e = n->gemm(M, d, d, n->AO, y.wo2, kResidual, y.bo2, n->X, nullptr, d, st)) !=
+        cudaSuccess)
+      return e;
+    layer_norm_bf16(d, n->X, M, y.ln3g, y.ln3b, n->Y, st);
+    if ((e = n->gemm(M, s.dff, d, n->Y, y.w1, kRelu, y.b1, nullptr, n->H, s.dff, st)) !=
+        cudaSuccess)
+      return e;
+    if ((e = n->gemm(M, d, s.dff, n->H, y.w2, kResidual, y.b2, n->X, nullptr, d, st)) !=
+        cudaSuccess)
+      return e;
+  }
+  layer_norm_bf16(d, n->X, M, n->ang, n->anb, n->Y, st);
+  if ((e = n->gemm(M, s.vocab, d, n->Y, n->wout, kPlain, n->bout, n->logits, nullptr, s.vocab,
+                   st)) != cudaSuccess)
+    return e;
+  dec_log_softmax64_kernel<<<M, 256, 0, st>>>(n->logits, s.vocab, lambda, n->att, n->attf);
+  return cudaGetLastError();
+}
+
+}  // namespace bl

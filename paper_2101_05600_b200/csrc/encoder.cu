@@ -632,7 +632,7 @@ struct EncoderImpl {
   // n segments of T_in frames; fbank [n][T_in][idim] (host or device);
   // grid [n][T2][vocab] device fp32.
   cudaError_t forward(int n, int T_in, const float* fbank, bool on_device, float* grid,
-                      int chunk) {
+                      int chunk, __nv_bfloat16* memory = nullptr) {
     cur_tin = T_in;
     const int T1 = (T_in - 3) / 2 + 1, T2 = enc_frames_out(T_in), d = s.d;
     cudaError_t e = ensure_pe(T2);
@@ -753,6 +753,10 @@ struct EncoderImpl {
           return e;
       }
       ln(ang, anb);
+      if (memory &&
+          (e = cudaMemcpyAsync(memory + (size_t)s0 * T2 * d, Y, (size_t)M * d * 2,
+                               cudaMemcpyDeviceToDevice, st)) != cudaSuccess)
+        return e;
       if ((e = gemm(M, s.vocab, d, Y, cw, kPlain, cb, out, nullptr, s.vocab)) != cudaSuccess)
         return e;
       log_softmax_kernel<<<M, 256, 0, st>>>(out, s.vocab);
@@ -777,11 +781,15 @@ cudaError_t enc_create(const EncSpec& s, const float* w, EncoderImpl** out) {
   return cudaSuccess;
 }
 void enc_destroy(EncoderImpl* e) { delete e; }
+void layer_norm_bf16(int d, const float* X, int rows, const float* g, const float* b,
+                     __nv_bfloat16* Y, cudaStream_t st) {
+  launch_layernorm(d, X, rows, g, b, Y, st);
+}
 void enc_set_stream(EncoderImpl* e, cudaStream_t st) { e->st = st; }
 cudaStream_t enc_stream(EncoderImpl* e) { return e->st; }
 cudaError_t enc_forward(EncoderImpl* e, int n, int T_in, const float* fb, bool on_device,
-                        float* grid, int chunk, int* launches) {
-  cudaError_t r = e->forward(n, T_in, fb, on_device, grid, chunk);
+                        float* grid, int chunk, int* launches, __nv_bfloat16* memory) {
+  cudaError_t r = e->forward(n, T_in, fb, on_device, grid, chunk, memory);
   if (launches) *launches = e->launches;
   return r;
 }

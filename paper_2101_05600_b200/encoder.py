@@ -22,6 +22,7 @@ from typing import Dict, List, Tuple
 
 import numpy as np
 
+from . import api as _api
 from .api import _check, lib
 
 
@@ -127,9 +128,10 @@ class Encoder:
         _check(L.bl_encoder_set_chunk(h, chunk))
 
     def close(self) -> None:
-        if getattr(self, "_h", None):
-            lib().bl_encoder_destroy(self._h)
-            self._h = None
+        L = getattr(_api, "_lib", None) if _api is not None else None
+        if getattr(self, "_h", None) and L is not None:
+            L.bl_encoder_destroy(self._h)
+        self._h = None
 
     __del__ = close
 
@@ -148,19 +150,27 @@ class Encoder:
                                         1 if on_device else 0, C.c_void_p(grid_ptr),
                                         1 if sync else 0))
 
-    def forward(self, fbank):
+    def forward(self, fbank, memory: bool = False):
         """torch: fbank [n, frames, idim] float32 (CPU or CUDA) -> CUDA grid
-        [n, frames_out, vocab] float32."""
+        [n, frames_out, vocab] float32 (and, with memory=True, the encoder
+        output bf16 [n, frames_out, d_model] for the attention decoder)."""
         import torch
         n, T, idim = fbank.shape
         if idim != self.spec.idim:
             raise ValueError(f"fbank has {idim} features, encoder expects {self.spec.idim}")
         fb = fbank.contiguous().float()
-        grid = torch.empty((n, frames_out(T), self.spec.vocab), dtype=torch.float32,
-                           device="cuda")
+        T2 = frames_out(T)
+        grid = torch.empty((n, T2, self.spec.vocab), dtype=torch.float32, device="cuda")
         self.set_stream(torch.cuda.current_stream().cuda_stream)
-        self.forward_raw(n, T, fb.data_ptr(), fb.is_cuda, grid.data_ptr(), sync=True)
-        return grid
+        if not memory:
+            self.forward_raw(n, T, fb.data_ptr(), fb.is_cuda, grid.data_ptr(), sync=True)
+            return grid
+        mem = torch.empty((n, T2, self.spec.d_model), dtype=torch.bfloat16, device="cuda")
+        _check(lib().bl_encoder_forward_mem(self._h, n, T, C.c_void_p(fb.data_ptr()),
+                                            1 if fb.is_cuda else 0,
+                                            C.c_void_p(grid.data_ptr()),
+                                            C.c_void_p(mem.data_ptr()), 1))
+        return grid, mem
 
 
 def gemm_bf16(A, B, mode: int = 0, bias=None, out=None, out_bf16=None, scale: float = 1.0,
