@@ -237,6 +237,74 @@ def run_pipeline(args, torch, dist, bl, dec, ids, n, world, dev, local):
             "launches_per_step": enc.launches + dec.last_stats["launches"]}
 
 
+def run_pipeline_attn(args, torch, dist, bl, ids, n, world, dev, local):
+    """The full model end to end: pinned host fbank -> device encoder (grid +
+    memory) -> joint CTC/attention decode with the device Transformer decoder
+    scorer (3 layers, d=256, 4 heads, ff 2048, vocab 500; BASELINE cfg 2's
+    '6 enc/3 dec' model, random-init) -> results on the host."""
+    from paper_2101_05600_b200 import encoder as benc
+    from paper_2101_05600_b200 import transformer as btr
+    from paper_2101_05600_b200.api import _check, lib
+    import ctypes as C
+    espec, dspec = benc.SMALL, btr.SMALL
+    enc = benc.Encoder(espec, benc.random_weights(espec, seed=0), device=local, chunk=64)
+    sc = btr.TransformerScorer(dspec, btr.random_weights(dspec, seed=1), device=local)
+    cfg = bl.DecoderConfig(beam_width=BEAM, ctc_weight=LAMBDA, margin_m1=M1, margin_m2=M2,
+                           eos_mode="both")
+    dec = bl.Decoder(sc, cfg, device=local)
+    fb = torch.from_numpy(benc.synthetic_fbank(n, 1000, espec.idim, seed=17 + local))
+    fb = fb.pin_memory()
+    grid = torch.empty((n, T_ENC, VOCAB), dtype=torch.float32, device=dev)
+    mem = torch.empty((n, T_ENC, espec.d_model), dtype=torch.bfloat16, device=dev)
+    st = torch.cuda.Stream(device=dev)
+    enc.set_stream(st.cuda_stream)
+    dec.set_stream(st.cuda_stream)
+    stride = T_ENC * VOCAB * 4
+    descs = [(ids[i], T_ENC, VOCAB, grid.data_ptr() + i * stride) for i in range(n)]
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+
+    def pstep():
+        e0.record(st)
+        _check(lib().bl_encoder_forward_mem(enc._h, n, 1000, C.c_void_p(fb.data_ptr()), 0,
+                                            C.c_void_p(grid.data_ptr()),
+                                            C.c_void_p(mem.data_ptr()), 0))
+        e1.record(st)
+        res = dec.decode_raw(descs, on_device=True, memory=mem.data_ptr(), mem_frames=T_ENC)
+        e2.record(st)
+        return res
+
+    res = pstep()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_enc, t_all = [], []
+    for _ in range(max(1, args.attn_steps)):
+        res = pstep()
+        st.synchronize()
+        t_enc.append(e0.elapsed_time(e1))
+        t_all.append(e0.elapsed_time(e2))
+    ms = torch.tensor([statistics.mean(t_all)], device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    enc_ms = statistics.mean(t_enc)
+    lens = [len(r.tokens) for r in res]
+    audio = world * n * T_ENC * FRAME_SHIFT_MS / 1000.0
+    out = {"value": audio / (ms / 1000.0), "unit": "audio-s/s", "ms_per_step": ms,
+           "steps": max(1, args.attn_steps), "encoder_ms": enc_ms, "decode_ms": ms - enc_ms,
+           "decode_steps_max": max(r.steps_taken for r in res),
+           "mean_hyp_tokens": statistics.mean(lens),
+           "h2d_bytes_per_step": n * 1000 * espec.idim * 4,
+           "d2h_bytes_per_step": dec.last_stats.get("d2h_bytes", 0),
+           "launches_per_step": enc.launches + dec.last_stats["launches"],
+           "model": "encoder 6 x d256 + Transformer decoder scorer 3 x d256 (4 heads, ff "
+                    "2048, vocab 500), random-init; the near-uniform random decoder keeps "
+                    "hypotheses ~T long (worst case for the per-step decoder)"}
+    del dec, sc
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -248,7 +316,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true",
-                    help="skip the fbank -> encoder -> decoder leg")
+                    help="skip the fbank -> encoder -> decoder legs")
+    ap.add_argument("--attn-steps", type=int, default=2,
+                    help="timed steps of the full-model (Transformer scorer) leg")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -339,9 +409,10 @@ def main():
                "ms_per_step": ems, "h2d_bytes_per_step": n * stride,
                "d2h_bytes_per_step": dec.last_stats.get("d2h_bytes", 0)}
 
-    pipeline = None
+    pipeline = pipeline_attn = None
     if not args.no_pipeline:
         pipeline = run_pipeline(args, torch, dist, bl, dec, ids, n, world, dev, local)
+        pipeline_attn = run_pipeline_attn(args, torch, dist, bl, ids, n, world, dev, local)
 
     peak, peak_kind = peaks()
     kernel_ms = statistics.mean(kms)
@@ -359,6 +430,7 @@ def main():
                          "kernel_ms": kernel_ms},
             "clocks": clk.summary(),
             "pipeline": pipeline,
+            "pipeline_attn": pipeline_attn,
             "counters": {k: dec.last_stats[k] for k in
                          ("steps", "scorer_queries", "ctc_frames_evaluated", "contenders",
                           "fallback_steps")}}
