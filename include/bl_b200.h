@@ -83,6 +83,13 @@ int bl_config_validate(const bl_config* cfg);
  * writes up to `cap` half-open [start,end) pairs, *n_out = segment count. */
 int bl_hard_segments(int num_frames, int min_len, int max_len, int* starts,
                      int* ends, int cap, int* n_out);
+/* VAD segmentation, segmentation.hpp:49-60 composed (frame_llr ->
+ * smooth_and_decide -> vad_segments): outputs [T][num_nodes] raw VAD model
+ * values; speech/noise node sets; threshold (nats), smoothing window,
+ * min_len/max_len in frames. Writes up to cap segments; *n_out = total. */
+int bl_vad_segments(const float* outputs, int T, int num_nodes, const int* speech, int n_speech,
+                    const int* noise, int n_noise, double threshold, int smooth_window,
+                    int min_len, int max_len, int* starts, int* ends, int cap, int* n_out);
 /* make_batches (batched.hpp:20-21, batched.cpp:12-30): stable ascending
  * sort by true_frames; order[n] receives the sorted input indices, batches
  * are consecutive chunks of batch_size. */

@@ -260,6 +260,10 @@ class Ref:
                                        C.POINTER(C.c_double)]
         L.ref_verify.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int,
                                  C.c_uint64]
+        L.ref_vad_segments.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                       C.c_void_p, C.c_int, C.c_double, C.c_int, C.c_int,
+                                       C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_char_p,
+                                       C.c_int]
         L.ref_replay_misses.restype = C.c_longlong
         L.ref_replay_misses.argtypes = [C.c_int]
 
@@ -302,6 +306,24 @@ class Ref:
             raise ValueError(err.value.decode())
         return _collect(self.lib, "ref_", h, ids), (cnt.steps, cnt.scorer_queries,
                                                      cnt.ctc_frames_evaluated)
+
+    def vad_segments(self, outputs, speech, noise, threshold, smooth_window, min_len,
+                     max_len):
+        """segmentation.cpp frame_llr -> smooth_and_decide -> vad_segments."""
+        o = np.ascontiguousarray(outputs, np.float32)
+        sp = np.asarray(speech, np.int32)
+        no = np.asarray(noise, np.int32)
+        cap = o.shape[0] + 1
+        st = np.zeros(cap, np.int32)
+        en = np.zeros(cap, np.int32)
+        err = C.create_string_buffer(512)
+        n = self.lib.ref_vad_segments(o.ctypes.data, o.shape[0], o.shape[1], sp.ctypes.data,
+                                      len(sp), no.ctypes.data, len(no), threshold,
+                                      smooth_window, min_len, max_len, st.ctypes.data,
+                                      en.ctypes.data, cap, err, 512)
+        if n < 0:
+            raise ValueError(err.value.decode())
+        return list(zip(st[:n].tolist(), en[:n].tolist()))
 
     def replay_misses(self, reset=True) -> int:
         """Queries the replay scorer could not answer since the last reset."""

@@ -291,6 +291,33 @@ int ref_verify(const char* suite, int trials, int max_frames, int max_vocab,
   return r.failures;
 }
 
+int ref_vad_segments(const float* outputs, int T, int num_nodes, const int* speech,
+                     int n_speech, const int* noise, int n_noise, double threshold,
+                     int smooth_window, int min_len, int max_len, int* starts, int* ends,
+                     int cap, char* err, int errlen) {
+  try {
+    NodeMap nm;
+    nm.speech_nodes.assign(speech, speech + n_speech);
+    nm.noise_nodes.assign(noise, noise + n_noise);
+    std::vector<double> llr(T);
+    for (int t = 0; t < T; ++t) {
+      std::vector<double> row(outputs + (size_t)t * num_nodes,
+                              outputs + (size_t)(t + 1) * num_nodes);
+      llr[t] = frame_llr(row, nm);
+    }
+    auto flags = smooth_and_decide(llr, threshold, smooth_window);
+    auto segs = vad_segments(flags, min_len, max_len, "r");
+    for (size_t i = 0; i < segs.size() && (int)i < cap; ++i) {
+      starts[i] = segs[i].start;
+      ends[i] = segs[i].end;
+    }
+    return (int)segs.size();
+  } catch (const std::exception& e) {
+    set_err(err, errlen, e.what());
+    return -1;
+  }
+}
+
 long long ref_replay_misses(int reset) {
   const long long m = g_replay_misses.load();
   if (reset) g_replay_misses = 0;

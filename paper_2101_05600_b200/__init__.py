@@ -11,4 +11,4 @@ from .api import (  # noqa: F401
     LoopScorer, PosteriorGrid, Scorer, Segment, TableScorer, UniformScorer,
     Utterance, batched_beam_search, beam_search, eos_mode_from_string,
     hard_segments, lib, make_batches, make_scorer, read_grid, result_json,
-    save_table_scorer, write_grid, write_results)
+    save_table_scorer, vad_segments, write_grid, write_results)

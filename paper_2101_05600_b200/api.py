@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
     L.bl_config_default.argtypes = [C.POINTER(_Config)]
     L.bl_config_validate.argtypes = [C.POINTER(_Config)]
     L.bl_hard_segments.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip, C.c_int, ip]
+    L.bl_vad_segments.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, C.c_double,
+                                  C.c_int, C.c_int, C.c_int, vp, vp, C.c_int, ip]
     L.bl_make_batches.argtypes = [C.c_int, C.POINTER(C.c_uint32), C.c_int, ip, ip]
     L.bl_scorer_create.argtypes = [C.c_char_p, C.c_int, C.POINTER(vp)]
     L.bl_scorer_create_table.argtypes = [C.c_int, C.c_int, C.c_int, ip, ip, dp,
@@ -289,6 +291,26 @@ def hard_segments(num_frames: int, min_len: int, max_len: int,
     _check(lib().bl_hard_segments(num_frames, min_len, max_len, s, e, cap,
                                   C.byref(n)))
     return [Segment(utterance_id, s[k], e[k], "hard") for k in range(n.value)]
+
+
+def vad_segments(outputs, speech_nodes: Sequence[int], noise_nodes: Sequence[int],
+                 threshold: float = 0.0, smooth_window: int = 5, min_len: int = 1500,
+                 max_len: int = 2000, utterance_id: str = "") -> List[Segment]:
+    """VAD segmentation (segmentation.hpp:49-60, VadConfig defaults): raw VAD
+    model outputs [T][num_nodes] -> speech segments (source "vad")."""
+    o = np.ascontiguousarray(outputs, np.float32)
+    if o.ndim != 2:
+        raise InvalidArgument("VAD outputs must be [frames, nodes]")
+    sp = np.ascontiguousarray(speech_nodes, np.int32)
+    no = np.ascontiguousarray(noise_nodes, np.int32)
+    cap = o.shape[0] + 1
+    st = np.zeros(cap, np.int32)
+    en = np.zeros(cap, np.int32)
+    n = C.c_int()
+    _check(lib().bl_vad_segments(o.ctypes.data, o.shape[0], o.shape[1], sp.ctypes.data, len(sp),
+                                 no.ctypes.data, len(no), threshold, smooth_window, min_len,
+                                 max_len, st.ctypes.data, en.ctypes.data, cap, C.byref(n)))
+    return [Segment(utterance_id, int(st[k]), int(en[k]), "vad") for k in range(n.value)]
 
 
 # ------------------------------------------------------------------ scorers

@@ -820,6 +820,83 @@ int bl_hard_segments(int T, int min_len, int max_len, int* starts, int* ends,
   });
 }
 
+// VAD segmentation (segmentation.cpp:13-119): per-frame LLR = max noise
+// output - max speech output (frame_llr), centred moving average by prefix
+// sums and threshold with ties as speech (smooth_and_decide), maximal speech
+// runs merged left to right until >= min_len, then near-uniform splits of at
+// most max_len (vad_segments). Same operation order, so same decisions.
+int bl_vad_segments(const float* outputs, int T, int num_nodes, const int* speech, int n_speech,
+                    const int* noise, int n_noise, double threshold, int smooth_window,
+                    int min_len, int max_len, int* starts, int* ends, int cap, int* n_out) {
+  return guarded([&] {
+    if (n_speech < 1 || n_noise < 1)
+      throw std::invalid_argument("nodemap: speech and noise sets must be non-empty");
+    for (int i = 0; i < n_noise; ++i)
+      for (int j = 0; j < n_speech; ++j)
+        if (noise[i] == speech[j])
+          throw std::invalid_argument("nodemap: speech and noise sets overlap");
+    for (int j = 0; j < n_speech; ++j)
+      if (speech[j] < 0 || speech[j] >= num_nodes)
+        throw std::invalid_argument("nodemap: speech node out of range");
+    for (int i = 0; i < n_noise; ++i)
+      if (noise[i] < 0 || noise[i] >= num_nodes)
+        throw std::invalid_argument("nodemap: noise node out of range");
+    if (smooth_window < 1) throw std::invalid_argument("vad: smoothing window must be >= 1");
+    if (!(min_len > 0 && min_len <= max_len))
+      throw std::invalid_argument("vad: need 0 < min_len <= max_len");
+    if (T < 0) throw std::invalid_argument("vad: T < 0");
+    std::vector<double> llr(T);
+    for (int t = 0; t < T; ++t) {
+      const float* row = outputs + (size_t)t * num_nodes;
+      double sp = -HUGE_VAL, no = -HUGE_VAL;
+      for (int j = 0; j < n_speech; ++j) sp = std::max(sp, (double)row[speech[j]]);
+      for (int i = 0; i < n_noise; ++i) no = std::max(no, (double)row[noise[i]]);
+      llr[t] = no - sp;
+    }
+    std::vector<double> prefix(T + 1, 0.0);
+    for (int t = 0; t < T; ++t) prefix[t + 1] = prefix[t] + llr[t];
+    const int half_lo = (smooth_window - 1) / 2, half_hi = smooth_window / 2;
+    std::vector<char> sp(T);
+    for (int t = 0; t < T; ++t) {
+      const int lo = std::max(0, t - half_lo), hi = std::min(T - 1, t + half_hi);
+      const double mean = (prefix[hi + 1] - prefix[lo]) / (hi - lo + 1);
+      sp[t] = mean <= threshold;
+    }
+    std::vector<std::pair<int, int>> runs, merged;
+    for (int t = 0; t < T;) {
+      if (!sp[t]) {
+        ++t;
+        continue;
+      }
+      const int a = t;
+      while (t < T && sp[t]) ++t;
+      runs.emplace_back(a, t);
+    }
+    for (size_t r = 0; r < runs.size();) {
+      int a = runs[r].first, b = runs[r].second;
+      ++r;
+      while (b - a < min_len && r < runs.size()) b = runs[r++].second;
+      merged.emplace_back(a, b);
+    }
+    int n = 0;
+    for (auto [a, b] : merged) {
+      const int len = b - a, pieces = (len + max_len - 1) / max_len;
+      int off = a;
+      for (int k = 0; k < pieces; ++k) {
+        const int piece = len / pieces + (k < len % pieces ? 1 : 0);
+        if (n < cap) {
+          starts[n] = off;
+          ends[n] = off + piece;
+        }
+        ++n;
+        off += piece;
+      }
+    }
+    *n_out = n;
+    return BL_OK;
+  });
+}
+
 // make_batches (batched.cpp:12-30)
 int bl_make_batches(int n, const uint32_t* frames, int batch_size, int* order,
                     int* n_batches) {

@@ -163,3 +163,44 @@ def test_decoder_needs_gpu_or_fails_loudly():
         pytest.skip("GPU present")
     with pytest.raises(bl.CudaError):
         bl.Decoder(bl.UniformScorer(3))
+
+
+# ------------------------------------------------------------ VAD segmentation
+def _vad_outputs(seed, T, nodes=4):
+    rng = np.random.default_rng(seed)
+    # slowly varying speech/noise evidence with bursts, some exact ties
+    base = np.cumsum(rng.normal(0, 0.6, T))
+    out = rng.normal(0, 0.3, (T, nodes)).astype(np.float32)
+    out[:, 0] += base.astype(np.float32)
+    out[:, 2] -= base.astype(np.float32)
+    out[::17, 1] = out[::17, 3]
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_vad_segments_match_reference(ref, seed):
+    """bl_vad_segments == reference frame_llr/smooth_and_decide/vad_segments."""
+    import paper_2101_05600_b200 as bl
+    rng = np.random.default_rng(100 + seed)
+    T = int(rng.integers(50, 4000))
+    outs = _vad_outputs(seed, T)
+    for thr, win, mn, mx in ((0.0, 5, 150, 200), (0.5, 1, 1, 7), (-0.3, 12, 40, 40),
+                             (0.0, 3, 1000, 2000)):
+        want = ref.vad_segments(outs, [0, 1], [2, 3], thr, win, mn, mx)
+        got = bl.vad_segments(outs, [0, 1], [2, 3], thr, win, mn, mx, "x")
+        assert [(g.start, g.end) for g in got] == want
+        assert all(g.source == "vad" for g in got)
+
+
+def test_vad_segments_errors():
+    import paper_2101_05600_b200 as bl
+    o = np.zeros((10, 3), np.float32)
+    with pytest.raises(ValueError):
+        bl.vad_segments(o, [0], [0])           # overlapping node sets
+    with pytest.raises(ValueError):
+        bl.vad_segments(o, [0], [5])           # node out of range
+    with pytest.raises(ValueError):
+        bl.vad_segments(o, [0], [1], smooth_window=0)
+    with pytest.raises(ValueError):
+        bl.vad_segments(o, [0], [1], min_len=5, max_len=4)
+    assert bl.vad_segments(np.zeros((0, 3), np.float32), [0], [1]) == []
