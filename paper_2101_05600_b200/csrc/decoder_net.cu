@@ -213,6 +213,12 @@ __device__ __forceinline__ void ldsm_x2_t(uint32_t addr, uint32_t& b0, uint32_t&
                : "=r"(b0), "=r"(b1)
                : "r"(addr));
 }
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, unsigned src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
 __device__ __forceinline__ uint32_t pk_bf16(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<const uint32_t*>(&h);
@@ -228,21 +234,22 @@ __global__ void __launch_bounds__(kXW * 32)
   const int Tp = (T + 63) & ~63;
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(xm_sm);
   __nv_bfloat16* Vs = Ks + (size_t)Tp * kXKPitch;
-  float* mrg = reinterpret_cast<float*>(Vs + (size_t)Tp * kXKPitch);  // [warps][16*64 + 32]
+  // after the key loop the K/V tiles are dead: the warps' partials reuse them
+  float* mrg = reinterpret_cast<float*>(xm_sm);  // [warps][16*64 + 32]
   const int u = blockIdx.x, h = blockIdx.y, q0 = blockIdx.z * 16;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t ld = 2 * (size_t)d;
   const __nv_bfloat16* base = kv2 + (size_t)u * T * ld + h * kDk;
+  // K/V rows straight into shared memory (cp.async, 16 B each, zero fill
+  // past T): every thread keeps all its copies in flight
   for (int i = threadIdx.x; i < Tp * 8; i += blockDim.x) {  // 8 x 16 B per row
     const int t = i >> 3, c = i & 7;
-    uint4 kk = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-    if (t < T) {
-      kk = reinterpret_cast<const uint4*>(base + t * ld)[c];
-      vv = reinterpret_cast<const uint4*>(base + t * ld + d)[c];
-    }
-    reinterpret_cast<uint4*>(Ks + (size_t)t * kXKPitch)[c] = kk;
-    reinterpret_cast<uint4*>(Vs + (size_t)t * kXKPitch)[c] = vv;
+    const int tt = t < T ? t : 0;
+    const unsigned nbytes = t < T ? 16u : 0u;
+    cp_async16(Ks + (size_t)t * kXKPitch + c * 8, base + tt * ld + c * 8, nbytes);
+    cp_async16(Vs + (size_t)t * kXKPitch + c * 8, base + tt * ld + d + c * 8, nbytes);
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
   // query fragments: rows q0 + lane/4 (+8), dims kc*16 + 2*(lane%4) (+8)
   uint32_t qa[4][4];
   {
@@ -331,6 +338,7 @@ __global__ void __launch_bounds__(kXW * 32)
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  __syncthreads();  // every warp is done with Ks/Vs
   // merge the warps: O = sum_w O_w 2^(m_w - M), L = sum_w l_w 2^(m_w - M)
   float* mw = mrg + warp * (16 * 64 + 32);
   {
@@ -409,7 +417,7 @@ __global__ void __launch_bounds__(256)
 
 size_t xm_smem(int T) {
   const size_t Tp = (size_t)((T + 63) & ~63);
-  return 2 * Tp * kXKPitch * 2 + (size_t)kXW * (16 * 64 + 32) * 4;
+  return std::max(2 * Tp * kXKPitch * 2, (size_t)kXW * (16 * 64 + 32) * 4);
 }
 
 }  // namespace
