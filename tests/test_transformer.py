@@ -123,6 +123,27 @@ def test_transformer_search_vs_reference_replay(ref, espec, dspec, n, frames, be
 
 
 @pytest.mark.gpu
+def test_transformer_large_vocab_tma_step_mode_vs_reference(ref):
+    """Librispeech-size model (d=512, 8 heads, vocab 5000): the search runs its
+    TMA-streamed slab path in step mode with per-hypothesis network rows."""
+    import pyoracle as po
+    grid, mem, w = _setup(enc.LARGE, tr.LARGE, 2, 300, seed=13)
+    kw = dict(beam_width=4, margin_m1=5, margin_m2=10)
+    dec, res, ids = _decode(grid, mem, tr.TransformerScorer(tr.LARGE, w), bl.DecoderConfig(**kw))
+    recs = dec.records()
+    spec = po.ScorerSpec("replay", tr.LARGE.vocab - 1, replay_ids=ids,
+                         entries=[(u, p, r) for u, p, r in recs])
+    host = grid.cpu().numpy()
+    ref.replay_misses(reset=True)
+    want, _ = ref.decode([host[i] for i in range(grid.shape[0])], spec, po.config(**kw), ids=ids)
+    assert ref.replay_misses() == 0
+    for g, r in zip(res, want):
+        assert g.tokens == r.tokens and g.label_times == r.label_times
+        assert g.steps_taken == r.steps and g.eos_trigger == r.eos_trigger
+        assert abs(g.joint_logp - r.joint_logp) <= 1e-9
+
+
+@pytest.mark.gpu
 def test_transformer_scorer_needs_memory():
     torch = pytest.importorskip("torch")
     w = tr.random_weights(TINY_DEC, seed=1)
