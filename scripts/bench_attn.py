@@ -20,18 +20,20 @@ ap.add_argument("--n", type=int, default=256)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--beam", type=int, default=10)
 ap.add_argument("--profile", action="store_true")
+ap.add_argument("--spec", default="small", choices=["small", "large"])
 a = ap.parse_args()
-espec, dspec = enc.SMALL, tr.SMALL
+espec, dspec = (enc.SMALL, tr.SMALL) if a.spec == "small" else (enc.LARGE, tr.LARGE)
+V, D = espec.vocab, espec.d_model
 e = enc.Encoder(espec, enc.random_weights(espec, seed=0), chunk=64)
 sc = tr.TransformerScorer(dspec, tr.random_weights(dspec, seed=1))
 dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=a.beam, margin_m1=5, margin_m2=20))
 fb = torch.from_numpy(enc.synthetic_fbank(a.n, 1000, seed=2)).pin_memory()
-grid = torch.empty(a.n, 249, 500, device="cuda")
-mem = torch.empty(a.n, 249, 256, device="cuda", dtype=torch.bfloat16)
+grid = torch.empty(a.n, 249, V, device="cuda")
+mem = torch.empty(a.n, 249, D, device="cuda", dtype=torch.bfloat16)
 st = torch.cuda.Stream()
 e.set_stream(st.cuda_stream)
 dec.set_stream(st.cuda_stream)
-descs = [(f"s{i}", 249, 500, grid[i].data_ptr()) for i in range(a.n)]
+descs = [(f"s{i}", 249, V, grid[i].data_ptr()) for i in range(a.n)]
 from paper_2101_05600_b200.api import _check, lib  # noqa: E402
 import ctypes as C  # noqa: E402
 
@@ -53,7 +55,7 @@ t = [step() for _ in range(a.steps)]
 enc_ms = statistics.mean(x[1] for x in t)
 dec_ms = statistics.mean(x[2] for x in t)
 lens = [len(r.tokens) for r in t[-1][0]]
-out = {"n": a.n, "encoder_ms": round(enc_ms, 2), "decode_ms": round(dec_ms, 2),
+out = {"spec": a.spec, "n": a.n, "encoder_ms": round(enc_ms, 2), "decode_ms": round(dec_ms, 2),
        "audio_s_per_s": round(a.n * 9.96 / ((enc_ms + dec_ms) / 1e3), 1),
        "steps_max": max(r.steps_taken for r in t[-1][0]),
        "mean_tokens": statistics.mean(lens), "stats": dec.last_stats}
