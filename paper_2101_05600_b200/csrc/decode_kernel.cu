@@ -110,6 +110,15 @@ __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned
                "r"(bytes)
                : "memory");
 }
+// Barrier over the step's decision group, warps [gw0, kNWarp): the whole
+// block when gw0 == 0, else named barrier 1 (the serial-chain warps run on).
+__device__ __forceinline__ void group_sync(int gw0) {
+  if (gw0 == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync 1, %0;" ::"r"((kNWarp - gw0) * 32) : "memory");
+  }
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -154,6 +163,7 @@ struct Shared {
   int s, e, W, nb, n_cont, nsel, nchild, n_fin, n_fin_new, count_long, best_fin;
   int done, trigger, steps, fallback;
   int row_same;  // scorer row shared by every live parent, or -1
+  int child_q[BMAX];  // contender index of each child (deferred tau fix-up)
   double best_all, best_fin_val, off;
   float theta, theta2;
   int n_list;
@@ -901,6 +911,12 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       PROF_MARK(5);
     }
 
+    // Decision group of this step: warps [gw0, kNWarp) run P7-P9. On the
+    // staged path the contender chains (warps [0, nser)) only produce the
+    // children's gamma states and tau, which nothing in P7-P9 reads, so
+    // they overlap with ranking, walk and end detection; tau is patched in
+    // after the join.
+    int gw0 = 0;
     if (!sh.fallback) {
       const int nc = sh.n_cont;
       const long long ts0 = clock64();
@@ -987,11 +1003,13 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           }
         }
       }
-      __syncthreads();
-      PROF_MARK(6);
+      gw0 = staged ? nser : 0;
+      if (warp >= gw0) {
+      group_sync(gw0);
+      if (gw0 == 0) PROF_MARK(6);
       // ---- P7: exact order over contenders + eos (warp-ballot ranks) ----
       const int ni = nc + nb;
-      for (int i = warp; i < ni; i += kNWarp) {
+      for (int i = warp - gw0; i < ni; i += kNWarp - gw0) {
         const Item me = items[i < nc ? i : caps + (i - nc)];
         int rank = 0;
         for (int q0 = 0; q0 < ni; q0 += 32) {
@@ -1009,14 +1027,15 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           x.parent = me.parent;
           x.token = me.token;
           x.slot = i < nc ? i : -1;
-          x.tau = me.tau;
-          x.taut = me.taut;
+          x.tau = gw0 ? 0 : me.tau;  // chains may still run: patched after the join
+          x.taut = gw0 ? 0 : me.taut;
           sh.sel[rank] = x;
         }
       }
-      if (tid == 0) sh.nsel = min(ni, B + nb);
-      __syncthreads();
-      PROF_MARK(7);
+      if (tid == gw0 * 32) sh.nsel = min(ni, B + nb);
+      group_sync(gw0);
+      if (gw0 == 0) PROF_MARK(7);
+      }  // decision group
     } else {
       // ---- fallback: fp64 scores for every candidate + exact selection ----
       double* xs = P.xs + (size_t)u * B * (C + 1);
@@ -1098,12 +1117,14 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       PROF_MARK(8);
     }
 
+    if (warp >= gw0) {
+    const int gtid = tid - gw0 * 32;
     // ---- P8: walk (parallel): finished entries and children ----
     const int nsel = sh.nsel;
-    if (tid < nsel) {
-      const SelE x = sh.sel[tid];
+    if (gtid < nsel) {
+      const SelE x = sh.sel[gtid];
       int non_eos_before = 0, eos_before = 0;
-      for (int q = 0; q < tid; ++q) {
+      for (int q = 0; q < gtid; ++q) {
         if (sh.sel[q].token < C) ++non_eos_before;
         else ++eos_before;
       }
@@ -1131,6 +1152,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
                                        P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
           sh.b_joint[nxt][k] = x.score;
           sh.b_row[nxt][k] = P.net_rows ? u * B + k : lookup_row(P, hist_c, l, l - 1, j, c);
+          sh.child_q[k] = x.slot;
           HistRec h;
           h.token = c;
           h.parent = j;
@@ -1140,7 +1162,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
         }
       }
     }
-    if (tid == 0) {
+    if (gtid == 0) {
       int ne = 0, ee2 = 0;
       for (int q = 0; q < nsel; ++q) {
         if (ne >= B) break;
@@ -1150,11 +1172,11 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       sh.nchild = ne;
       sh.n_fin_new = ee2;
     }
-    __syncthreads();
-    PROF_MARK(9);
-    if (sh.fallback && tid < sh.nchild) {
+    group_sync(gw0);
+    if (gw0 == 0) PROF_MARK(9);
+    if (sh.fallback && gtid < sh.nchild) {
       // children states for the fallback path (slot k of area nxt)
-      int k = tid, cnt = 0, q = 0;
+      int k = gtid, cnt = 0, q = 0;
       for (; q < nsel; ++q) {
         if (sh.sel[q].token < C) {
           if (cnt == k) break;
@@ -1174,7 +1196,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     }
 
     // ---- P9: end detection (batched.cpp:215-228) ----
-    if (tid == 0) {
+    if (gtid == 0) {
       const int n0 = sh.n_fin, nn = sh.n_fin_new;
       for (int q = n0; q < n0 + nn; ++q) {
         const FinEntry f = fin_u[q];
@@ -1214,7 +1236,15 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       sh.done = stop ? 1 : 0;
       if (P.nb_out) P.nb_out[u] = stop ? 0 : sh.nchild;
     }
-    __syncthreads();
+    }  // decision group
+    __syncthreads();  // join: contender chains and decisions both done
+    if (gw0 > 0 && tid < sh.nchild) {  // children's tau from their chains
+      const Item& it = items[sh.child_q[tid]];
+      sh.b_tau[nxt][tid] = it.tau;
+      sh.b_taut[nxt][tid] = it.taut;
+      hist_u[(size_t)l * B + tid].tau = it.tau;
+    }
+    if (gw0 > 0) __syncthreads();
     PROF_MARK(10);
     if (sh.done) break;
     if (stepm) {

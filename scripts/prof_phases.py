@@ -3,7 +3,7 @@ os.environ["BL_PROFILE"] = "1"
 sys.path.insert(0, ".")
 import numpy as np
 import paper_2101_05600_b200 as bl
-names = ["init+Ftab", "P1 window/eos", "P2 phi/PhiF", "P3 bulk(+P4a)", "P4 theta", "P5 collect", "P6 contenders", "P7 rank", "fallback", "P8 walk", "P9 end", "finalize", "t0:P3 frames", "t0:P3 keys", "t0:P6 serial", "t0:P6 staging"]
+names = ["init+Ftab", "P1 window/eos", "P2 phi/PhiF", "P3 bulk(+P4a)", "P4 theta", "P5 collect", "P6 contenders", "P7 rank (fb)", "fallback", "P8 walk (fb)", "P6-P9 overlap", "finalize", "t0:P3 frames", "t0:P3 keys", "t0:P6 serial", "t0:P6 staging"]
 rng = np.random.default_rng(1)
 for (V, B, M2, U) in [(500, 10, 20, 64)]:
     G = []
