@@ -470,12 +470,20 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     // F[k][c]: label c held from frame k to some k' then blank to T
     // (the eos tail of ctc_prefix.cpp:88-104 in closed form).
     for (int t = tid; t <= T; t += kNT) Gt[t] = Gs[t];
-    for (int c = tid; c < C; c += kNT) {
-      double f = 0.0;
-      Ft[(size_t)T * C + c] = f;
+    // two columns per pass, their serial chains interleaved (log_add2)
+    for (int c0 = tid; c0 < C; c0 += 2 * kNT) {
+      const int c1 = c0 + kNT;
+      const bool two = c1 < C;
+      const int c1r = two ? c1 : c0;
+      double f0 = 0.0, f1 = 0.0;
+      Ft[(size_t)T * C + c0] = f0;
+      if (two) Ft[(size_t)T * C + c1] = f1;
       for (int k = T - 1; k >= 0; --k) {
-        f = log_add(log_mul((double)grid[(size_t)k * V + c], f), Gs[k], tb);
-        Ft[(size_t)k * C + c] = f;
+        const double g = Gs[k];
+        log_add2(log_mul((double)grid[(size_t)k * V + c0], f0), g,
+                 log_mul((double)grid[(size_t)k * V + c1r], f1), g, tb, &f0, &f1);
+        Ft[(size_t)k * C + c0] = f0;
+        if (two) Ft[(size_t)k * C + c1] = f1;
       }
     }
   }
@@ -492,7 +500,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     }
     const int nb = sh.nb;
 
-    // ---- P1: windows, eos candidates, offsets (warp 0) ----
+    // ---- P1: windows and offsets (warp 0). The eos candidates (two fp64
+    // log_adds per hypothesis) are only read by P7: they are computed by a
+    // spare warp during P6 (eos_items below), off the critical path. ----
     if (warp == 0) {
       const int j = lane;
       int ws = INT_MAX, we = INT_MIN;
@@ -501,24 +511,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       if (j < nb) {
         window_for(sh.b_tau[cur][j], sh.b_taut[cur][j], P.m1, P.m2, l, T, &ws, &we);
         const int cov = sh.b_cov[cur][j];
-        const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
-        const double* gbp = gnp + P.Tp;
-        double ee;
-        if (cov >= T) {
-          ee = log_add(gnp[T], gbp[T], tb);
-        } else {
-          const int last = sh.b_last[cur][j];
-          const double fl = last >= 0 ? Ft[(size_t)cov * C + last] : Gt[cov];
-          ee = log_add(log_mul(gnp[cov], fl), log_mul(gbp[cov], Gt[cov]), tb);
-          tail = (unsigned long long)(T - cov);
-        }
-        const double* row = P.sc_rows + (size_t)sh.b_row[cur][j] * V;
-        Item it;
-        it.score = mix_joint(lam, ee, __dadd_rn(sh.b_att[cur][j], row[C]));
-        it.parent = j;
-        it.token = C;
-        it.tau = it.taut = 0;
-        items[caps + j] = it;  // eos candidates live past the contender slots
+        if (cov < T) tail = (unsigned long long)(T - cov);
         jm = sh.b_joint[cur][j];
       }
 #pragma unroll
@@ -548,6 +541,31 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     __syncthreads();
     PROF_MARK(1);
     const int s = sh.s, e = sh.e, W = sh.W;
+    // eos candidates of the beam (eos_score_extended, ctc_prefix.cpp:88-104,
+    // via the tail tables), one lane per hypothesis
+    auto eos_items = [&]() {
+      const int j = lane;
+      if (j < nb) {
+        const int cov = sh.b_cov[cur][j];
+        const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
+        const double* gbp = gnp + P.Tp;
+        double ee;
+        if (cov >= T) {
+          ee = log_add(gnp[T], gbp[T], tb);
+        } else {
+          const int last = sh.b_last[cur][j];
+          const double fl = last >= 0 ? Ft[(size_t)cov * C + last] : Gt[cov];
+          ee = log_add(log_mul(gnp[cov], fl), log_mul(gbp[cov], Gt[cov]), tb);
+        }
+        const double* row = P.sc_rows + (size_t)sh.b_row[cur][j] * V;
+        Item it;
+        it.score = mix_joint(lam, ee, __dadd_rn(sh.b_att[cur][j], row[C]));
+        it.parent = j;
+        it.token = C;
+        it.tau = it.taut = 0;
+        items[caps + j] = it;  // eos candidates live past the contender slots
+      }
+    };
 
     // ---- P2: phi_j[t] (fp64, reference log_add) and the fp32 factors ----
     for (int idx = tid; idx < nb * W; idx += kNT) {
@@ -974,7 +992,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           items[q].taut = taut;
           if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - tr0;
         }
-      } else if (staged) {
+      } else {
+        if (warp == kNWarp - 1) eos_items();
+        if (staged) {
         for (int q = warp - nser; q < nc; q += kNWarp - nser) {
           const int j = items[q].parent, c = items[q].token;
           const bool repeat = sh.b_last[cur][j] == c;
@@ -1001,6 +1021,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
                                          P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
             items[q].score = mix_joint(lam, psi, att);
           }
+        }
         }
       }
       gw0 = staged ? nser : 0;
@@ -1038,6 +1059,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       }  // decision group
     } else {
       // ---- fallback: fp64 scores for every candidate + exact selection ----
+      if (warp == 0) eos_items();
+      __syncthreads();
       double* xs = P.xs + (size_t)u * B * (C + 1);
       unsigned char* taken = P.taken + (size_t)u * B * (C + 1);
       const int total = nb * (C + 1);
