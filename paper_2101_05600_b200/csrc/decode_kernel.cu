@@ -567,49 +567,62 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       }
     };
 
-    // ---- P2: phi_j[t] (fp64, reference log_add) and the fp32 factors ----
-    for (int idx = tid; idx < nb * W; idx += kNT) {
-      const int j = idx / W, i = idx - j * W, t = s + i;
-      const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
-      const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
-      const double* gbp = gnp + P.Tp;
-      const double gb = gread(gbp, t - 1, vlo, cov);
-      phi[(size_t)j * P.Tmax + i] = log_add(gb, gread(gnp, t - 1, vlo, cov), tb);
+    // ---- P2: phi_j[t] (fp64, reference log_add), the per-parent max M_j
+    // and the fp32 factors in one pass: a half-warp per parent (16 parents
+    // per pass), the max by half-warp shuffles, one block barrier ----
+    {
+      const int hl = lane & 15;  // lane within the half-warp
+      for (int jb = 2 * warp; jb < nb; jb += kNT / 16) {  // warp-uniform
+        const int j = jb + (lane >> 4);
+        const bool act = j < nb;
+        double m = -HUGE_VAL;
+        if (act) {
+          const int vlo = sh.b_vlo[cur][j], cov = sh.b_cov[cur][j];
+          const double* gnp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 0);
+          const double* gbp = gnp + P.Tp;
+          for (int i = hl; i < W; i += 16) {
+            const int t = s + i;
+            const double v =
+                log_add(gread(gbp, t - 1, vlo, cov), gread(gnp, t - 1, vlo, cov), tb);
+            phi[(size_t)j * P.Tmax + i] = v;
+            if (!is_zero(v) && v > m) m = v;
+          }
+        }
+        if (!P.exact) {
+#pragma unroll
+          for (int o = 8; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+          const double Mj = (m == -HUGE_VAL) ? kLogZero : m;
+          if (act && hl == 0) {
+            sh.M[j] = Mj;
+            sh.mzero[j] = is_zero(Mj) ? 1 : 0;
+            // per-parent float base of the joint key, relative to `off`
+            const double base = (lam >= 1.0)   ? Mj
+                                : (lam <= 0.0) ? sh.b_att[cur][j]
+                                               : lam * Mj + (1.0 - lam) * sh.b_att[cur][j];
+            sh.kb[j] = (float)(base - sh.off);
+          }
+          if (act) {
+            for (int i = hl; i < W; i += 16) {  // this lane's own phi entries
+              const double pv = phi[(size_t)j * P.Tmax + i];
+              PhiF[(size_t)i * BMAX + j] =
+                  (!is_zero(Mj) && !is_zero(pv)) ? __expf((float)(pv - Mj)) : 0.f;
+            }
+          }
+        }
+      }
+      if (!P.exact) {
+        const int pad = BMAX - nb;  // factor columns of absent parents are zero
+        for (int idx = tid; idx < W * pad; idx += kNT) {
+          const int i = idx / pad, j = nb + (idx - i * pad);
+          PhiF[(size_t)i * BMAX + j] = 0.f;
+        }
+        for (int idx = tid; idx < ub_words; idx += kNT) ubits[idx] = 0u;
+      }
     }
     __syncthreads();
 
+    bool step_fallback = P.exact != 0;  // fp64 decisions for this step
     if (!P.exact) {
-      for (int j = warp; j < nb; j += kNWarp) {
-        double m = -HUGE_VAL;
-        for (int i = lane; i < W; i += 32) {
-          const double v = phi[(size_t)j * P.Tmax + i];
-          if (!is_zero(v) && v > m) m = v;
-        }
-        m = warp_max_d(m);
-        if (lane == 0) {
-          const double Mj = (m == -HUGE_VAL) ? kLogZero : m;
-          sh.M[j] = Mj;
-          sh.mzero[j] = is_zero(Mj) ? 1 : 0;
-          // per-parent float base of the joint key, relative to `off`
-          const double base = (lam >= 1.0)   ? Mj
-                              : (lam <= 0.0) ? sh.b_att[cur][j]
-                                             : lam * Mj + (1.0 - lam) * sh.b_att[cur][j];
-          sh.kb[j] = (float)(base - sh.off);
-        }
-      }
-      __syncthreads();
-      for (int idx = tid; idx < W * BMAX; idx += kNT) {
-        const int i = idx / BMAX, j = idx - i * BMAX;
-        float v = 0.f;
-        if (j < nb) {
-          const double Mj = sh.M[j];
-          const double p = phi[(size_t)j * P.Tmax + i];
-          if (!is_zero(Mj) && !is_zero(p)) v = __expf((float)(p - Mj));
-        }
-        PhiF[(size_t)i * BMAX + j] = v;
-      }
-      for (int idx = tid; idx < ub_words; idx += kNT) ubits[idx] = 0u;
-      __syncthreads();
       PROF_MARK(2);
 
       // ---- P3: K1 bulk prefix score + certified fp32 joint keys ----
@@ -912,8 +925,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           }
         }
       }
-      __syncthreads();
-      if (warp == 0 && lane < nb && sh.b_last[cur][lane] >= 0) {
+      if (warp == kNWarp - 1 && lane < nb && sh.b_last[cur][lane] >= 0) {
         const int idx = atomicAdd(&sh.n_cont, 1);  // repeat column: always exact
         if (idx < caps) {
           items[idx].parent = lane;
@@ -921,11 +933,13 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
         }
       }
       __syncthreads();
+      // every thread derives the same decision; thread 0 records it (what
+      // other threads may still read is the same value)
+      step_fallback = sh.fallback || sh.n_cont > P.caps;
       if (tid == 0) {
         sh.c_cont += sh.n_cont;
-        if (sh.n_cont > P.caps) sh.fallback = 1;
+        sh.fallback = step_fallback;
       }
-      __syncthreads();
       PROF_MARK(5);
     }
 
@@ -935,7 +949,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     // they overlap with ranking, walk and end detection; tau is patched in
     // after the join.
     int gw0 = 0;
-    if (!sh.fallback) {
+    if (!step_fallback) {
       const int nc = sh.n_cont;
       const long long ts0 = clock64();
       // ---- P6a: stage the contenders' grid columns, the blank column and the
@@ -1197,7 +1211,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     }
     group_sync(gw0);
     if (gw0 == 0) PROF_MARK(9);
-    if (sh.fallback && gtid < sh.nchild) {
+    if (step_fallback && gtid < sh.nchild) {
       // children states for the fallback path (slot k of area nxt)
       int k = gtid, cnt = 0, q = 0;
       for (; q < nsel; ++q) {
