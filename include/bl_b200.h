@@ -266,6 +266,15 @@ int bl_scorer_create_transformer(int device, const bl_transformer_spec* spec,
  * i's rows at memory + i*mem_frames*d_model. */
 int bl_decode_memory(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
                      const void* memory, int mem_frames, bl_results** out);
+/* Bulk form for large batches: decodes like bl_decode / bl_decode_memory
+ * (memory may be NULL) and writes the 1-best results straight into caller
+ * arrays — n_tokens/steps/trigger/joint [n], tokens/label_times [n][cap] —
+ * without per-utterance result objects. *stats receives a bl_results holding
+ * only the counters/stats/transfer figures (count 0); destroy it as usual. */
+int bl_decode_into(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
+                   const void* memory, int mem_frames, int cap, int* n_tokens, int* steps,
+                   int* trigger, double* joint, int* tokens, int* label_times,
+                   bl_results** stats);
 /* Record mode (parity tests): keep every scorer row the network produced for
  * a live hypothesis, with the utterance index and the token prefix, so a
  * host replay scorer can drive the reference decoder with identical rows. */

@@ -124,6 +124,8 @@ def lib() -> C.CDLL:
     L.bl_scorer_create_transformer.argtypes = [C.c_int, vp, vp, C.c_size_t, C.POINTER(vp)]
     L.bl_decode_memory.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.c_int, vp, C.c_int,
                                    C.POINTER(vp)]
+    L.bl_decode_into.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.c_int, vp, C.c_int, C.c_int,
+                                 vp, vp, vp, vp, vp, vp, C.POINTER(vp)]
     L.bl_encoder_forward_mem.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, C.c_int]
     L.bl_gemm_bf16.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int,
                                vp, vp, vp, C.c_int, C.c_float, vp, C.c_int, vp]
@@ -528,6 +530,25 @@ class Decoder:
             self._desc_cache = (key, descs, arr)
         rec = arr[0]
         h = C.c_void_p()
+        if self.nbest == 1 and n > 0:
+            # bulk path: 1-best results written straight into numpy arrays
+            cap = max(1, int(rec["num_frames"][:n].max()))
+            nt = np.empty(n, np.int32)
+            st = np.empty(n, np.int32)
+            tr = np.empty(n, np.int32)
+            jt = np.empty(n, np.float64)
+            tok = np.empty((n, cap), np.int32)
+            lt = np.empty((n, cap), np.int32)
+            _check(lib().bl_decode_into(
+                self._h, n, rec.ctypes.data_as(C.POINTER(_Utt)), 1 if on_device else 0,
+                C.c_void_p(memory) if memory is not None else None, mem_frames, cap,
+                nt.ctypes.data, st.ctypes.data, tr.ctypes.data, jt.ctypes.data,
+                tok.ctypes.data, lt.ctypes.data, C.byref(h)))
+            try:
+                self._stats(h, counters)
+            finally:
+                lib().bl_results_destroy(h)
+            return ResultSet(ids, nt, st, tr, jt, tok, lt, None)
         if memory is not None:
             _check(lib().bl_decode_memory(self._h, n, rec.ctypes.data_as(C.POINTER(_Utt)),
                                           1 if on_device else 0, C.c_void_p(memory),
@@ -574,6 +595,11 @@ class Decoder:
                                 [l_[q] for q in range(m_.value)]))
                 nbest.append(lst)
         out = ResultSet(ids, nt, st, tr, jt, tok, lt, nbest)
+        self._stats(h, counters)
+        return out
+
+    def _stats(self, h, counters) -> None:
+        L = lib()
         s, q, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
         L.bl_results_counters(h, C.byref(s), C.byref(q), C.byref(f))
         if counters is not None:
@@ -594,7 +620,6 @@ class Decoder:
             prof = (C.c_double * 16)()
             L.bl_results_profile(h, prof)
             self.last_stats["profile_cycles"] = [round(x) for x in prof]
-        return out
 
 
 _decoders: Dict[tuple, Decoder] = {}

@@ -442,8 +442,16 @@ int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
   return launches;
 }
 
+// Bulk result destination (bl_decode_into): results written straight from
+// the pinned D2H buffer into caller arrays, no per-utterance objects.
+struct IntoArgs {
+  int cap;
+  int *n_tokens, *steps, *trigger, *tokens, *label_times;
+  double* joint;
+};
+
 int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
-                bl_results** out) {
+                bl_results** out, const IntoArgs* into = nullptr) {
   validate_cfg(d->cfg);  // batched.cpp:97
   auto res = std::make_unique<bl_results>();
   if (n == 0) {  // batched.cpp:99
@@ -729,6 +737,30 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
 
   const int* hr = static_cast<const int*>(d->h_res.p);
   const unsigned long long* hc = static_cast<const unsigned long long*>(d->h_cnt.p);
+  if (into) {
+    for (int i = 0; i < n; ++i) {
+      const int* r = hr + (size_t)i * rs;
+      const int nt = r[0];
+      if (nt > into->cap) throw std::invalid_argument("result longer than the export capacity");
+      into->n_tokens[i] = nt;
+      into->steps[i] = r[1];
+      into->trigger[i] = r[2];
+      std::memcpy(into->joint + i, r + 4, sizeof(double));
+      std::memcpy(into->tokens + (size_t)i * into->cap, r + bl::kResHdr, sizeof(int) * nt);
+      std::memcpy(into->label_times + (size_t)i * into->cap, r + bl::kResHdr + S,
+                  sizeof(int) * nt);
+      res->max_tokens = std::max(res->max_tokens, nt);
+      const unsigned long long* c = hc + (size_t)i * 8;
+      res->steps += c[0];
+      res->queries += c[1];
+      res->frames += c[2];
+      res->k1 += c[3];
+      res->fallback += c[4];
+      res->contenders += c[5];
+    }
+    *out = res.release();  // counters and stats only
+    return BL_OK;
+  }
   res->r.resize(n);
   for (int i = 0; i < n; ++i) {
     const int* r = hr + (size_t)i * rs;
@@ -1103,6 +1135,25 @@ int bl_decode(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     d->memory = nullptr;
     d->mem_frames = 0;
     return decode_impl(d, n, utts, on_device, out);
+  });
+}
+
+int bl_decode_into(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
+                   const void* memory, int mem_frames, int cap, int* n_tokens, int* steps,
+                   int* trigger, double* joint, int* tokens, int* label_times,
+                   bl_results** stats) {
+  return guarded([&] {
+    if (cap < 1 || !n_tokens || !steps || !trigger || !joint || !tokens || !label_times)
+      throw std::invalid_argument("bl_decode_into: null output or cap < 1");
+    if (memory && !d->net) throw std::invalid_argument("memory needs a transformer scorer");
+    d->memory = memory;
+    d->mem_frames = memory ? mem_frames : 0;
+    if (memory && mem_frames < 1) throw std::invalid_argument("memory frames must be >= 1");
+    d->rec.clear();
+    IntoArgs ia{cap, n_tokens, steps, trigger, tokens, label_times, joint};
+    const int r = decode_impl(d, n, utts, grids_on_device, stats, &ia);
+    d->memory = nullptr;
+    return r;
   });
 }
 
