@@ -186,7 +186,7 @@ def run_pipeline(args, torch, dist, bl, dec, ids, n, world, dev, local):
     the host. Same segments, decoder and config as the headline."""
     from paper_2101_05600_b200 import encoder as benc
     spec = benc.SMALL
-    enc = benc.Encoder(spec, benc.random_weights(spec, seed=0), device=local, chunk=64)
+    enc = benc.Encoder(spec, benc.random_weights(spec, seed=0), device=local, chunk=148)
     fb = torch.from_numpy(benc.synthetic_fbank(n, 1000, spec.idim, seed=17 + local))
     fb = fb.pin_memory()
     grid = torch.empty((n, T_ENC, VOCAB), dtype=torch.float32, device=dev)
@@ -277,7 +277,7 @@ def run_pipeline_attn(args, torch, dist, bl, ids, n, world, dev, local):
     from paper_2101_05600_b200.api import _check, lib
     import ctypes as C
     espec, dspec = benc.SMALL, btr.SMALL
-    enc = benc.Encoder(espec, benc.random_weights(espec, seed=0), device=local, chunk=64)
+    enc = benc.Encoder(espec, benc.random_weights(espec, seed=0), device=local, chunk=148)
     sc = btr.TransformerScorer(dspec, btr.random_weights(dspec, seed=1), device=local)
     cfg = bl.DecoderConfig(beam_width=BEAM, ctc_weight=LAMBDA, margin_m1=M1, margin_m2=M2,
                            eos_mode="both")

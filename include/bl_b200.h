@@ -208,7 +208,8 @@ int bl_encoder_create(int device, const bl_encoder_spec* spec, const float* weig
 /* Stream used verbatim (NULL = the legacy default stream); the encoder starts
  * on a private non-blocking stream. */
 int bl_encoder_set_stream(bl_encoder* e, void* stream);
-/* Segments processed per internal chunk (workspace ~ chunk x 50 MB at d=512). */
+/* Segments processed per internal chunk (default 148: 148 x 249 rows is two waves of
+ * 128-row GEMM tiles on 148 SMs; workspace ~ chunk x 50 MB at d=512). */
 int bl_encoder_set_chunk(bl_encoder* e, int segments);
 /* n equal-length segments, fbank [n][frames_in][idim] fp32 (host or device),
  * grid [n][frames_out][vocab] fp32 DEVICE memory. Enqueued on the encoder's

@@ -1258,7 +1258,7 @@ struct bl_encoder {
   int device = 0;
   bl::EncoderImpl* impl = nullptr;
   cudaStream_t own = nullptr;
-  int chunk = 64;
+  int chunk = 148;  // 148 x 249 rows = 2 waves of 128-row tiles on 148 SMs
   int launches = 0;
 };
 

@@ -115,7 +115,7 @@ class Encoder:
     """Device encoder; ``forward`` writes log-posterior grids to device memory."""
 
     def __init__(self, spec: EncoderSpec, weights: np.ndarray, device: int = 0,
-                 chunk: int = 64):
+                 chunk: int = 148):
         self.spec = spec
         w = np.ascontiguousarray(weights, dtype=np.float32)
         L = lib()

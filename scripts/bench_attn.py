@@ -24,7 +24,7 @@ ap.add_argument("--spec", default="small", choices=["small", "large"])
 a = ap.parse_args()
 espec, dspec = (enc.SMALL, tr.SMALL) if a.spec == "small" else (enc.LARGE, tr.LARGE)
 V, D = espec.vocab, espec.d_model
-e = enc.Encoder(espec, enc.random_weights(espec, seed=0), chunk=64)
+e = enc.Encoder(espec, enc.random_weights(espec, seed=0), chunk=148)
 sc = tr.TransformerScorer(dspec, tr.random_weights(dspec, seed=1))
 dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=a.beam, margin_m1=5, margin_m2=20))
 fb = torch.from_numpy(enc.synthetic_fbank(a.n, 1000, seed=2)).pin_memory()
