@@ -11,8 +11,15 @@
 
 #include <cstdint>
 #include <algorithm>
+#include <charconv>
+#include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <fstream>
 #include <map>
+#include <optional>
+#include <ostream>
+#include <sstream>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -284,6 +291,144 @@ inline DecodeResult beam_search(const Utterance& utt, const Scorer& scorer,
   b.utterances = {utt};
   b.padded_frames = utt.true_frames;
   return batched_beam_search(b, scorer, cfg, counters).front();
+}
+
+// ---------------------------------------------------------------- grid I/O
+// grid.hpp:53-62 (grid.cpp): validation, padding, CTCG container
+// ("CTCG", u32 version=1, T, vocab, frame_shift_ms, T*vocab f32, little-endian).
+inline std::optional<std::string> validate_grid(const PosteriorGrid& grid) {
+  constexpr double kRowTol = 1e-6;
+  if (grid.num_frames < 1) return std::string("empty grid");
+  if (grid.vocab < 2) return std::string("vocab must be >= 2 (one token plus blank)");
+  if (grid.logp.size() != static_cast<size_t>(grid.num_frames) * grid.vocab)
+    return std::string("logp size does not match T*vocab");
+  for (uint32_t t = 0; t < grid.num_frames; ++t) {
+    const float* row = grid.logp.data() + static_cast<size_t>(t) * grid.vocab;
+    double m = -HUGE_VAL;
+    for (uint32_t k = 0; k < grid.vocab; ++k) {
+      if (std::isnan(row[k])) return "row " + std::to_string(t) + " has NaN";
+      if (row[k] > kRowTol)
+        return "row " + std::to_string(t) + " entry " + std::to_string(k) +
+               " is a positive log-prob";
+      m = std::max(m, static_cast<double>(row[k]));
+    }
+    double lse = kLogZero;
+    if (m > -1e29) {
+      double sum = 0.0;
+      for (uint32_t k = 0; k < grid.vocab; ++k) sum += std::exp(row[k] - m);
+      lse = m + std::log(sum);
+    }
+    if (std::abs(lse) > kRowTol) {
+      std::ostringstream os;
+      os.setf(std::ios::showpos);
+      os << "row " << t << " logsumexp=" << lse;
+      return os.str();
+    }
+  }
+  return std::nullopt;
+}
+
+inline PosteriorGrid pad_to_length(const PosteriorGrid& grid, uint32_t target_frames) {
+  if (target_frames < grid.num_frames)
+    throw std::invalid_argument("pad_to_length: target shorter than grid");
+  PosteriorGrid out = grid;
+  out.num_frames = target_frames;
+  out.logp.resize(static_cast<size_t>(target_frames) * grid.vocab, static_cast<float>(kLogZero));
+  for (uint32_t t = grid.num_frames; t < target_frames; ++t)  // blank-only frames
+    out.logp[static_cast<size_t>(t) * grid.vocab + grid.vocab - 1] = 0.0f;
+  return out;
+}
+
+namespace detail {
+inline void put_u32(std::ostream& os, uint32_t v) {
+  const unsigned char b[4] = {static_cast<unsigned char>(v), static_cast<unsigned char>(v >> 8),
+                              static_cast<unsigned char>(v >> 16),
+                              static_cast<unsigned char>(v >> 24)};
+  os.write(reinterpret_cast<const char*>(b), 4);
+}
+inline uint32_t get_u32(std::istream& is) {
+  unsigned char b[4] = {0, 0, 0, 0};
+  is.read(reinterpret_cast<char*>(b), 4);
+  return static_cast<uint32_t>(b[0]) | (static_cast<uint32_t>(b[1]) << 8) |
+         (static_cast<uint32_t>(b[2]) << 16) | (static_cast<uint32_t>(b[3]) << 24);
+}
+// shortest round-trip double, JSON style (integral values keep ".0")
+inline std::string json_double(double v) {
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof(buf), v);
+  std::string s(buf, r.ptr);
+  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
+  return s;
+}
+inline std::string json_string(const std::string& v) {
+  std::string o = "\"";
+  for (const char ch : v) {
+    const unsigned char c = static_cast<unsigned char>(ch);
+    if (c == '"' || c == '\\') {
+      o += '\\';
+      o += ch;
+    } else if (c < 0x20) {
+      char e[8];
+      std::snprintf(e, sizeof(e), "\\u%04x", c);
+      o += e;
+    } else {
+      o += ch;
+    }
+  }
+  return o + "\"";
+}
+inline std::string json_ints(const std::vector<int>& v) {
+  std::string o = "[";
+  for (size_t i = 0; i < v.size(); ++i) {
+    if (i) o += ',';
+    o += std::to_string(v[i]);
+  }
+  return o + "]";
+}
+}  // namespace detail
+
+inline void write_grid(const std::string& path, const PosteriorGrid& grid) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw std::runtime_error("cannot write grid file: " + path);
+  os.write("CTCG", 4);
+  detail::put_u32(os, 1);
+  detail::put_u32(os, grid.num_frames);
+  detail::put_u32(os, grid.vocab);
+  detail::put_u32(os, grid.frame_shift_ms);
+  os.write(reinterpret_cast<const char*>(grid.logp.data()),
+           static_cast<std::streamsize>(grid.logp.size() * sizeof(float)));
+  if (!os) throw std::runtime_error("short write: " + path);
+}
+
+inline PosteriorGrid read_grid(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw std::runtime_error("cannot open grid file: " + path);
+  char magic[4];
+  is.read(magic, 4);
+  if (!is || std::memcmp(magic, "CTCG", 4) != 0)
+    throw std::runtime_error("bad magic in grid file: " + path);
+  if (detail::get_u32(is) != 1) throw std::runtime_error("unsupported grid version in " + path);
+  PosteriorGrid g;
+  g.num_frames = detail::get_u32(is);
+  g.vocab = detail::get_u32(is);
+  g.frame_shift_ms = detail::get_u32(is);
+  g.logp.resize(static_cast<size_t>(g.num_frames) * g.vocab);
+  is.read(reinterpret_cast<char*>(g.logp.data()),
+          static_cast<std::streamsize>(g.logp.size() * sizeof(float)));
+  if (!is) throw std::runtime_error("truncated grid file: " + path);
+  return g;
+}
+
+// io.hpp:32 (io.cpp:81-92): one JSON object per result, keys in sorted order
+inline void write_results(std::ostream& os, const std::vector<DecodeResult>& results) {
+  for (const auto& r : results) {
+    os << "{\"eos_trigger\":" << detail::json_string(to_string(r.eos_trigger))
+       << ",\"id\":" << detail::json_string(r.id)
+       << ",\"joint_logp\":" << detail::json_double(r.joint_logp)
+       << ",\"label_times\":" << detail::json_ints(r.label_times)
+       << ",\"steps\":" << r.steps_taken << ",\"tokens\":" << detail::json_ints(r.tokens)
+       << "}\n";
+  }
 }
 
 }  // namespace beamlattice
