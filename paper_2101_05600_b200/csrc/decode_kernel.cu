@@ -4,20 +4,23 @@
 // /root/reference/proj/src/batched.cpp:94-237) with every step on device:
 //
 //   P1  windows + per-utterance envelope       ctc_prefix.cpp:106-125, batched.cpp:129-135
-//       eos candidates (exact fp64)            ctc_prefix.cpp:88-104 via precomputed tail tables
 //   P2  phi_j[t] = gb[t-1] (+) gn[t-1]  (fp64)  ctc_prefix.cpp:50-51
+//       + per-parent max and fp32 factors (one half-warp per parent)
 //   P3  K1 bulk prefix score, all (j, c):       ctc_prefix.cpp:47-59 (psi term)
 //       psi ~= M_j + m_c + log sum_t exp(phi_j-M_j) exp(L[t,c]-m_c)  (fp32 FMA)
 //       -> certified fp32 joint keys            beam_search.cpp:60-66, logmath.hpp:34-39
 //   P4  theta = B-th largest certified lower bound
 //   P5  contenders = candidates whose upper bound reaches theta (+ repeats)
-//   P6  contenders re-scored by the reference-order fp64 recursion from
-//       shared-memory staged inputs; it also yields their child state
-//       (gamma_n', gamma_b', tau, tau~)
+//   P6  contenders: psi by a parallel fp64 log-sum-exp (score), and the
+//       serial reference-order gamma_n'/gamma_b' chains (one warp) that
+//       yield their child state (gamma, tau, tau~); a spare warp computes
+//       the eos candidates (exact fp64, ctc_prefix.cpp:88-104 via tail tables)
 //   P7  exact total order (score desc, parent asc, token asc) incl. eos
 //                                               batched.cpp:172-186
 //   P8  walk: finished entries / children       batched.cpp:188-212
 //   P9  end detection                           batched.cpp:215-228
+//       P7-P9 run on the non-chain warps (named barrier) while the chains
+//       finish; the children's tau is patched in after the join
 //   fin finalize + n-best                       batched.cpp:70-90
 //
 // If the contender set overflows (degenerate ties) or exact mode is on, the
