@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // m starts at the log-zero guard (not -inf): a log-zero grid entry then
       // never triggers a rescale and contributes exp(-1e30 - m) = 0, so the
       // per-element guard test disappears (an all-zero column keeps m == gf).
-      auto acc = [&](float(&Sx)[BMAX], float& m, float x, const float4* ph) {
+      auto acc = [&](float(&Sx)[BMAX], float& m, float x, const float* ph) {
         if (x > m + 8.f) {
           const float r = __expf(m - x);
 #pragma unroll
@@ -649,13 +649,22 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           m = x;
         }
         const float pe = __expf(x - m);
+        if constexpr (BMAX % 4 == 0) {  // 16-byte factor rows
 #pragma unroll
-        for (int q = 0; q < BMAX / 4; ++q) {
-          const float4 f = ph[q];
-          Sx[4 * q + 0] = fmaf(f.x, pe, Sx[4 * q + 0]);
-          Sx[4 * q + 1] = fmaf(f.y, pe, Sx[4 * q + 1]);
-          Sx[4 * q + 2] = fmaf(f.z, pe, Sx[4 * q + 2]);
-          Sx[4 * q + 3] = fmaf(f.w, pe, Sx[4 * q + 3]);
+          for (int q = 0; q < BMAX / 4; ++q) {
+            const float4 f = reinterpret_cast<const float4*>(ph)[q];
+            Sx[4 * q + 0] = fmaf(f.x, pe, Sx[4 * q + 0]);
+            Sx[4 * q + 1] = fmaf(f.y, pe, Sx[4 * q + 1]);
+            Sx[4 * q + 2] = fmaf(f.z, pe, Sx[4 * q + 2]);
+            Sx[4 * q + 3] = fmaf(f.w, pe, Sx[4 * q + 3]);
+          }
+        } else {  // BMAX = 10: 8-byte rows
+#pragma unroll
+          for (int q = 0; q < BMAX / 2; ++q) {
+            const float2 f = reinterpret_cast<const float2*>(ph)[q];
+            Sx[2 * q + 0] = fmaf(f.x, pe, Sx[2 * q + 0]);
+            Sx[2 * q + 1] = fmaf(f.y, pe, Sx[2 * q + 1]);
+          }
         }
       };
       long long tq_frames = 0, tq_keys = 0;
@@ -663,8 +672,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       const int W4 = W & ~(kCh - 1);
       // certified keys: joint(j, c) - off in [key - h, key + h]; parent-major
       // so each parent's constants are read once for both columns
-      const float4* phr = reinterpret_cast<const float4*>(PhiF);
-      const int phs = BMAX / 4;  // float4 per PhiF row
+      const float* phr = PhiF;
+      constexpr int phs = BMAX;  // floats per PhiF row
       auto emit_keys = [&](int c0, bool two, const float(&S0)[BMAX], const float(&S1)[BMAX],
                            float m0, float m1, float r0s, float r1s) {
 #pragma unroll
@@ -1444,6 +1453,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
 int bmax_for(int B) {
   if (B <= 4) return 4;
   if (B <= 8) return 8;
+  if (B <= 10) return 10;  // the bench / paper beam: no padded parents in P3
   if (B <= 12) return 12;
   if (B <= 16) return 16;
   if (B <= 24) return 24;
@@ -1457,6 +1467,7 @@ size_t step_state_bytes(int B, int S) {
   switch (bmax_for(B)) {
     case 4: sh = sizeof(Shared<4>); break;
     case 8: sh = sizeof(Shared<8>); break;
+    case 10: sh = sizeof(Shared<10>); break;
     case 12: sh = sizeof(Shared<12>); break;
     case 16: sh = sizeof(Shared<16>); break;
     case 24: sh = sizeof(Shared<24>); break;
@@ -1498,6 +1509,7 @@ cudaError_t launch_decode(const KParams& p, cudaStream_t st) {
   switch (bmax_for(p.B)) {
     case 4: return launch_t<4>(p, st);
     case 8: return launch_t<8>(p, st);
+    case 10: return launch_t<10>(p, st);
     case 12: return launch_t<12>(p, st);
     case 16: return launch_t<16>(p, st);
     case 24: return launch_t<24>(p, st);
