@@ -29,6 +29,7 @@ namespace bl {
 cudaError_t launch_decode(const KParams& p, cudaStream_t st);
 size_t step_state_bytes(int B, int S);
 size_t decode_smem_bytes(const KParams& p);
+size_t decode_static_smem(const KParams& p);
 int bmax_for(int B);
 }  // namespace bl
 
@@ -513,7 +514,19 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     }
     use_tma = use_tma && (reinterpret_cast<uintptr_t>(gbase) & 15) == 0;
   }
-  const int tma_stages = use_tma ? (U <= 148 ? bl::kTmaStagesMax : 4) : 0;
+  int tma_stages = use_tma ? (U <= 148 ? bl::kTmaStagesMax : 4) : 0;
+  {
+    // long utterances: fewer TMA stages (down to 2), then the non-TMA path,
+    // before the plan is rejected (12 KB left for static shared memory)
+    const size_t lim = (227 - 12) * 1024;
+    const size_t fixed0 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).total;
+    auto need = [&](int st) { return fixed0 + bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0, st).region_need; };
+    while (use_tma && tma_stages > 2 && need(tma_stages) > lim) --tma_stages;
+    if (use_tma && need(tma_stages) > lim) {
+      use_tma = false;
+      tma_stages = 0;
+    }
+  }
   // shared-memory plan: the aliased region (P3-P5 keys, P6 staging) is sized
   // so the whole plan fits 3 CTAs/SM (~71 KB) when the fixed parts allow it;
   // the upper keys move to HBM when they do not fit.
@@ -659,8 +672,16 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     desc[i].row0 = (int)(goff[i] / V);
   }
   std::memcpy(d->h_utts.p, desc.data(), sizeof(bl::UttDesc) * U);
-  if (bl::decode_smem_bytes(p) > 227 * 1024)
-    throw std::invalid_argument("utterance too long for the device decoder's shared memory plan");
+  {
+    // dynamic plan + the variant's static shared memory against the opt-in limit
+    int optin = 227 * 1024;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d->device);
+    if (bl::decode_smem_bytes(p) + bl::decode_static_smem(p) > (size_t)optin)
+      throw std::invalid_argument(
+          "utterance too long for the device decoder's shared memory plan (" +
+          std::to_string(Tmax) + " frames, vocab " + std::to_string(V) +
+          "): hard-segment it (bl_hard_segments)");
+  }
 
   CK(cudaMemcpyAsync(d->utts.p, d->h_utts.p, sizeof(bl::UttDesc) * U,
                      cudaMemcpyHostToDevice, st));

@@ -1501,6 +1501,27 @@ static cudaError_t launch_v(const KParams& p, cudaStream_t st) {
 }
 
 template <int BMAX>
+static size_t static_smem_t(const KParams& p) {
+  cudaFuncAttributes fa{};
+  if (p.use_tma) cudaFuncGetAttributes(&fa, decode_kernel<BMAX, true>);
+  else cudaFuncGetAttributes(&fa, decode_kernel<BMAX, false>);
+  return fa.sharedSizeBytes;
+}
+
+// static shared memory of the kernel variant `p` selects
+size_t decode_static_smem(const KParams& p) {
+  switch (bmax_for(p.B)) {
+    case 4: return static_smem_t<4>(p);
+    case 8: return static_smem_t<8>(p);
+    case 10: return static_smem_t<10>(p);
+    case 12: return static_smem_t<12>(p);
+    case 16: return static_smem_t<16>(p);
+    case 24: return static_smem_t<24>(p);
+    default: return static_smem_t<32>(p);
+  }
+}
+
+template <int BMAX>
 static cudaError_t launch_t(const KParams& p, cudaStream_t st) {
   return p.use_tma ? launch_v<BMAX, true>(p, st) : launch_v<BMAX, false>(p, st);
 }
