@@ -226,6 +226,97 @@ inline std::vector<Segment> hard_segments(int num_frames, int min_len, int max_l
   return out;
 }
 
+// segmentation.hpp:10-60 — VAD segmentation (host code, same op order as
+// segmentation.cpp:13-119, so threshold ties decide identically)
+struct NodeMap {
+  std::vector<int> speech_nodes;
+  std::vector<int> noise_nodes;
+  void validate(int output_width) const {
+    if (speech_nodes.empty() || noise_nodes.empty())
+      throw std::invalid_argument("nodemap: speech and noise sets must be non-empty");
+    for (int n : noise_nodes)
+      if (std::find(speech_nodes.begin(), speech_nodes.end(), n) != speech_nodes.end())
+        throw std::invalid_argument("nodemap: speech and noise sets overlap");
+    for (int n : speech_nodes)
+      if (n < 0 || n >= output_width) throw std::invalid_argument("nodemap: speech node out of range");
+    for (int n : noise_nodes)
+      if (n < 0 || n >= output_width) throw std::invalid_argument("nodemap: noise node out of range");
+  }
+};
+
+struct VadConfig {
+  double threshold = 0.0;  // LLR cut, nats
+  int smooth_window = 5;   // frames
+  int min_len = 1500;      // frames
+  int max_len = 2000;      // frames
+  void validate() const {
+    if (smooth_window < 1) throw std::invalid_argument("vad: smoothing window must be >= 1");
+    if (!(min_len > 0 && min_len <= max_len))
+      throw std::invalid_argument("vad: need 0 < min_len <= max_len");
+  }
+};
+
+// log P_noise - log P_speech, each the max output over its node set
+inline double frame_llr(const std::vector<double>& outputs, const NodeMap& nodemap) {
+  nodemap.validate(static_cast<int>(outputs.size()));
+  double speech = -HUGE_VAL, noise = -HUGE_VAL;
+  for (int k : nodemap.speech_nodes) speech = std::max(speech, outputs[k]);
+  for (int k : nodemap.noise_nodes) noise = std::max(noise, outputs[k]);
+  return noise - speech;
+}
+
+// centred W-frame moving average (truncated at the edges); speech iff <= theta
+inline std::vector<bool> smooth_and_decide(const std::vector<double>& llr, double threshold,
+                                           int smooth_window) {
+  if (smooth_window < 1) throw std::invalid_argument("smoothing window must be >= 1");
+  const int n = static_cast<int>(llr.size());
+  std::vector<double> prefix(n + 1, 0.0);
+  for (int t = 0; t < n; ++t) prefix[t + 1] = prefix[t] + llr[t];
+  const int half_lo = (smooth_window - 1) / 2, half_hi = smooth_window / 2;
+  std::vector<bool> speech(n);
+  for (int t = 0; t < n; ++t) {
+    const int lo = std::max(0, t - half_lo), hi = std::min(n - 1, t + half_hi);
+    speech[t] = (prefix[hi + 1] - prefix[lo]) / (hi - lo + 1) <= threshold;
+  }
+  return speech;
+}
+
+// maximal speech runs, merged left to right until >= min_len, then split into
+// near-uniform pieces of at most max_len
+inline std::vector<Segment> vad_segments(const std::vector<bool>& speech_flags, int min_len,
+                                         int max_len, const std::string& utterance_id) {
+  if (!(min_len > 0 && min_len <= max_len))
+    throw std::invalid_argument("vad_segments: need 0 < min_len <= max_len");
+  const int n = static_cast<int>(speech_flags.size());
+  std::vector<std::pair<int, int>> runs, merged;
+  for (int t = 0; t < n;) {
+    if (!speech_flags[t]) {
+      ++t;
+      continue;
+    }
+    const int a = t;
+    while (t < n && speech_flags[t]) ++t;
+    runs.emplace_back(a, t);
+  }
+  for (size_t r = 0; r < runs.size();) {
+    int a = runs[r].first, b = runs[r].second;
+    ++r;
+    while (b - a < min_len && r < runs.size()) b = runs[r++].second;
+    merged.emplace_back(a, b);
+  }
+  std::vector<Segment> out;
+  for (auto [a, b] : merged) {
+    const int len = b - a, pieces = (len + max_len - 1) / max_len;
+    int off = a;
+    for (int k = 0; k < pieces; ++k) {
+      const int piece = len / pieces + (k < len % pieces ? 1 : 0);
+      out.push_back({utterance_id, off, off + piece, "vad"});
+      off += piece;
+    }
+  }
+  return out;
+}
+
 // batched.hpp:13-38
 struct Batch {
   std::vector<Utterance> utterances;

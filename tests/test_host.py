@@ -4,6 +4,7 @@ Mirrors test_segmentation.cpp, test_batched.cpp, test_beam_search.cpp,
 test_scorer.cpp and test_grid.cpp of the reference."""
 import io
 import json
+import os
 import math
 import random
 
@@ -204,3 +205,26 @@ def test_vad_segments_errors():
     with pytest.raises(ValueError):
         bl.vad_segments(o, [0], [1], min_len=5, max_len=4)
     assert bl.vad_segments(np.zeros((0, 3), np.float32), [0], [1]) == []
+
+
+def test_cpp_header_vad_matches_reference(ref, tmp_path):
+    """The drop-in header's VAD functions (host C++) equal the reference."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "vad"
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tests", "cpp", "vad_check.cpp"), "-o", str(exe)],
+                   check=True)
+    for seed in range(3):
+        outs = _vad_outputs(seed, 1500 + 300 * seed).astype(np.float64)
+        path = tmp_path / f"v{seed}.txt"
+        with open(path, "w") as fh:
+            fh.write(f"{outs.shape[0]} {outs.shape[1]}\n")
+            for row in outs:
+                fh.write(" ".join(repr(float(np.float32(x))) for x in row) + "\n")
+        for thr, win, mn, mx in ((0.0, 5, 150, 200), (0.5, 1, 1, 7), (-0.3, 12, 40, 40)):
+            got = subprocess.run([str(exe), str(path), repr(thr), str(win), str(mn), str(mx), "r"],
+                                 capture_output=True, text=True, check=True).stdout.split()
+            got = [(int(got[i]), int(got[i + 1])) for i in range(0, len(got), 2)]
+            want = ref.vad_segments(outs.astype(np.float32), [0, 1], [2, 3], thr, win, mn, mx)
+            assert got == want
