@@ -257,38 +257,32 @@ __device__ double child_recursion_smem(const double* ph, const float* lc,
   return psi;
 }
 
-// gamma_n'/gamma_b' chains only (psi is computed in parallel by other warps),
-// same operation order as ctc_prefix.cpp:47-57, argmax as :63-77.
-__device__ void child_state_smem(const double* ph, const float* lc, const float* lb, int s,
-                                 int W, int tau_p, double* gnc, double* gbc, int* tau_out,
-                                 int* taut_out, const SpTables& tb) {
+// The same recursion with two lanes per contender: the even lane runs the
+// gamma_n' chain, the odd lane the gamma_b' chain, which takes the partner's
+// previous gamma_n' by a shuffle. Each frame then costs one log_add per lane
+// instead of two interleaved ones; the operations per value are the
+// reference's (ctc_prefix.cpp:47-57), so the results are bit-identical.
+// Called by whole warps (the shuffle); `live` lanes store.
+__device__ void child_state_lanes(const double* ph, const float* lc, const float* lb, int s,
+                                  int W, int tau_p, double* gout, int role, bool live,
+                                  int* best_out, const SpTables& tb) {
   const int lo = tau_p > 1 ? tau_p : 1;
-  int best_n = lo, best_b = lo;
-  double val_n = kLogZero, val_b = kLogZero;
-  double gn_prev = kLogZero, gb_prev = kLogZero;
+  int best = lo;
+  double val = kLogZero, g_prev = kLogZero;
   for (int i = 0; i < W; ++i) {
     const int t = s + i;
-    double an, ab;
-    log_add2(gn_prev, ph[i], gb_prev, gn_prev, tb, &an, &ab);
-    const double gn = log_mul(an, (double)lc[i]);
-    const double gb = log_mul(ab, (double)lb[i]);
-    gnc[t] = gn;
-    gbc[t] = gb;
-    if (t >= lo) {
-      if (gn > val_n) {
-        val_n = gn;
-        best_n = t;
-      }
-      if (gb > val_b) {
-        val_b = gb;
-        best_b = t;
-      }
+    const double gn_partner = __shfl_xor_sync(0xffffffffu, g_prev, 1);
+    const double b = role == 0 ? ph[i] : gn_partner;
+    const double x = role == 0 ? (double)lc[i] : (double)lb[i];
+    const double g = log_mul(log_add(g_prev, b, tb), x);
+    if (live) gout[t] = g;
+    if (t >= lo && g > val) {
+      val = g;
+      best = t;
     }
-    gn_prev = gn;
-    gb_prev = gb;
+    g_prev = g;
   }
-  *tau_out = best_n;
-  *taut_out = best_b;
+  *best_out = best;
 }
 
 // Same recursion reading the grid and the parent from global memory
@@ -992,28 +986,41 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // ---- P6: contenders re-scored exactly. Warps [0, nser): the serial
       // gamma_n'/gamma_b' chains (one thread per contender, reference op
       // order); the other warps: psi by a parallel fp64 log-sum-exp. ----
-      const int nser = (nc + 31) >> 5;
-      if (warp < nser) {
+      // staged: two lanes per contender (16 per warp); otherwise one
+      const int nser = staged ? (nc + 15) >> 4 : (nc + 31) >> 5;
+      if (warp < nser && staged) {
+        const int q0 = tid >> 1, role = tid & 1;
+        const bool live = q0 < nc;
+        const int q = live ? q0 : nc - 1;  // idle lanes shadow a real chain
+        const int j = items[q].parent, c = items[q].token;
+        const bool repeat = sh.b_last[cur][j] == c;
+        double* gnc = gam_ptr(P, u, nxt, q, 0);
+        int best;
+        const long long tr0 = clock64();
+        child_state_lanes(repeat ? stR + (size_t)j * W : phi + (size_t)j * P.Tmax,
+                          stL + (size_t)q * W, stB, s, W, sh.b_tau[cur][j],
+                          role == 0 ? gnc : gnc + P.Tp, role, live, &best, tb);
+        if (live) {
+          if (role == 0) items[q].tau = best;
+          else items[q].taut = best;
+        }
+        if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - tr0;
+      } else if (warp < nser) {
+        // inputs not staged (window too wide for the region): one lane per
+        // contender runs the chains and psi from global memory
         const int q = tid;
         if (q < nc) {
           const int j = items[q].parent, c = items[q].token;
-          const bool repeat = sh.b_last[cur][j] == c;
           double* gnc = gam_ptr(P, u, nxt, q, 0);
           double* gbc = gnc + P.Tp;
           int tau, taut;
           const long long tr0 = clock64();
-          if (staged) {
-            child_state_smem(repeat ? stR + (size_t)j * W : phi + (size_t)j * P.Tmax,
-                             stL + (size_t)q * W, stB, s, W, sh.b_tau[cur][j], gnc, gbc, &tau,
-                             &taut, tb);
-          } else {
-            const double psi = child_recursion_global<BMAX>(
-                P, sh, u, cur, j, c, s, e, grid, phi + (size_t)j * P.Tmax, gnc, gbc, &tau,
-                &taut, tb);
-            const double att = __dadd_rn(sh.b_att[cur][j],
-                                         P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
-            items[q].score = mix_joint(lam, psi, att);
-          }
+          const double psi = child_recursion_global<BMAX>(
+              P, sh, u, cur, j, c, s, e, grid, phi + (size_t)j * P.Tmax, gnc, gbc, &tau, &taut,
+              tb);
+          const double att = __dadd_rn(sh.b_att[cur][j],
+                                       P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+          items[q].score = mix_joint(lam, psi, att);
           items[q].tau = tau;
           items[q].taut = taut;
           if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - tr0;
