@@ -87,6 +87,17 @@ __device__ __forceinline__ double gread(const double* a, int i, int vlo, int cov
   return (i < vlo || i > cov) ? kLogZero : a[i];
 }
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ double warp_max_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
@@ -635,30 +646,33 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // m starts at the log-zero guard (not -inf): a log-zero grid entry then
       // never triggers a rescale and contributes exp(-1e30 - m) = 0, so the
       // per-element guard test disappears (an all-zero column keeps m == gf).
-      auto acc = [&](float(&Sx)[BMAX], float& m, float x, const float* ph) {
+      // Accumulators are packed pairs of parents: fma.rn.f32x2 does two
+      // fp32 FMAs per instruction with the same rounding as two fmaf. The
+      // exp is ex2.approx.ftz
+      // (terms below 2^-126 of the column max flush to zero: at most
+      // W * 2^-126 absolute, covered by the W * 1e-6 key half-width).
+      constexpr int kP = BMAX / 2;
+      auto acc = [&](float2(&Sx)[kP], float& m, float x, const float* ph) {
         if (x > m + 8.f) {
           const float r = __expf(m - x);
+          const float2 r2 = make_float2(r, r);
 #pragma unroll
-          for (int q = 0; q < BMAX; ++q) Sx[q] *= r;
+          for (int q = 0; q < kP; ++q) Sx[q] = __fmul2_rn(Sx[q], r2);
           m = x;
         }
-        const float pe = __expf(x - m);
+        const float pe = ex2_ftz((x - m) * 1.44269504088896341f);
+        const float2 p2 = make_float2(pe, pe);
         if constexpr (BMAX % 4 == 0) {  // 16-byte factor rows
 #pragma unroll
           for (int q = 0; q < BMAX / 4; ++q) {
             const float4 f = reinterpret_cast<const float4*>(ph)[q];
-            Sx[4 * q + 0] = fmaf(f.x, pe, Sx[4 * q + 0]);
-            Sx[4 * q + 1] = fmaf(f.y, pe, Sx[4 * q + 1]);
-            Sx[4 * q + 2] = fmaf(f.z, pe, Sx[4 * q + 2]);
-            Sx[4 * q + 3] = fmaf(f.w, pe, Sx[4 * q + 3]);
+            Sx[2 * q + 0] = __ffma2_rn(make_float2(f.x, f.y), p2, Sx[2 * q + 0]);
+            Sx[2 * q + 1] = __ffma2_rn(make_float2(f.z, f.w), p2, Sx[2 * q + 1]);
           }
         } else {  // BMAX = 10: 8-byte rows
 #pragma unroll
-          for (int q = 0; q < BMAX / 2; ++q) {
-            const float2 f = reinterpret_cast<const float2*>(ph)[q];
-            Sx[2 * q + 0] = fmaf(f.x, pe, Sx[2 * q + 0]);
-            Sx[2 * q + 1] = fmaf(f.y, pe, Sx[2 * q + 1]);
-          }
+          for (int q = 0; q < kP; ++q)
+            Sx[q] = __ffma2_rn(reinterpret_cast<const float2*>(ph)[q], p2, Sx[q]);
         }
       };
       long long tq_frames = 0, tq_keys = 0;
@@ -668,7 +682,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // so each parent's constants are read once for both columns
       const float* phr = PhiF;
       constexpr int phs = BMAX;  // floats per PhiF row
-      auto emit_keys = [&](int c0, bool two, const float(&S0)[BMAX], const float(&S1)[BMAX],
+      const bool lam_pos = lam > 0.0;
+      auto emit_keys = [&](int c0, bool two, const float2(&S0)[kP], const float2(&S1)[kP],
                            float m0, float m1, float r0s, float r1s) {
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) {
@@ -681,31 +696,27 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
               const int c = c0 + cc;
               if (cc == 1 && !two) break;
               const float m = cc ? m1 : m0;
-              const float Sq = cc ? S1[q] : S0[q];
+              const float2 Sp = cc ? S1[q >> 1] : S0[q >> 1];
+              const float Sq = (q & 1) ? Sp.y : Sp.x;
               float klo = -INFINITY, kub_v = -INFINITY;
               bool under = false;
               if (c != last) {
                 const float r = row_same >= 0 ? (cc ? r1s : r0s)
                                               : P.sc_rowsf[(size_t)sh.b_row[cur][q] * V + c];
-                if (r == -INFINITY) {
-                  klo = kub_v = kZeroKey;  // att is log-zero: joint exactly kLogZero
-                } else if (lam <= 0.0) {
-                  const float key = kbq + r;
-                  const float h = hw + fabsf(key) * 2.4e-7f;
-                  klo = key - h;
-                  kub_v = key + h;
-                } else if (mz || m == gf) {
-                  klo = kub_v = kZeroKey;  // psi exactly kLogZero
-                } else if (Sq >= 7.888609052210118e-31f) {  // 2^-100
-                  const float key = kbq + lamf * (m + __logf(Sq)) + r;
-                  const float h = hw + fabsf(key) * 2.4e-7f;
-                  klo = key - h;
-                  kub_v = key + h;
-                } else {  // fp32 underflow: certified upper bound only
-                  const float key = kbq + lamf * (m - 68.62157f) + r;
-                  klo = -INFINITY;
-                  kub_v = key + hw + fabsf(key) * 2.4e-7f;
-                  under = true;
+                // same arithmetic as kbq + lamf * (m + __logf(Sq)) + r for a
+                // normal Sq; below 2^-100 only the certified upper bound
+                // with log(Sq) <= log(2^-99) is kept
+                under = lam_pos && !(Sq >= 7.888609052210118e-31f);  // 2^-100
+                const float lg = under ? -68.62157f : lg2_ftz(Sq) * 0.693147180559945309f;
+                const float key = lam_pos ? kbq + lamf * (m + lg) + r : kbq + r;
+                const float h = hw + fabsf(key) * 2.4e-7f;
+                klo = under ? -INFINITY : key - h;
+                kub_v = key + h;
+                // joint exactly kLogZero: att log-zero, or psi log-zero
+                const bool zero = r == -INFINITY || (lam_pos && (mz || m == gf));
+                if (zero) {
+                  klo = kub_v = kZeroKey;
+                  under = false;
                 }
                 if (klo > l2) {
                   if (klo > l1) {
@@ -746,7 +757,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           for (int j = 0; j < NST && j < J; ++j) issue(j, tma_jobs + j);
         }
-        float S0[BMAX], S1[BMAX];
+        float2 S0[kP], S1[kP];
         float m0 = gf, m1 = gf, r0s = 0.f, r1s = 0.f;
         const int colb = ((2 * tid) >= kTmaBoxCols ? kTmaRows * kTmaBoxCols : 0) +
                          ((2 * tid) & (kTmaBoxCols - 1));
@@ -758,7 +769,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           const bool active = c0 < C, two = c0 + 1 < C;
           if (k == 0) {
 #pragma unroll
-            for (int q = 0; q < BMAX; ++q) S0[q] = S1[q] = 0.f;
+            for (int q = 0; q < kP; ++q) S0[q] = S1[q] = make_float2(0.f, 0.f);
             m0 = m1 = gf;
             r0s = (row_same >= 0 && active) ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
             r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
@@ -786,9 +797,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       for (int c0 = 2 * tid; c0 < C; c0 += 2 * kNT) {
         const long long tq1 = clock64();
         const bool two = c0 + 1 < C;
-        float S0[BMAX], S1[BMAX];
+        float2 S0[kP], S1[kP];
 #pragma unroll
-        for (int q = 0; q < BMAX; ++q) S0[q] = S1[q] = 0.f;
+        for (int q = 0; q < kP; ++q) S0[q] = S1[q] = make_float2(0.f, 0.f);
         float m0 = gf, m1 = gf;
         const float r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
         const float r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;

@@ -15,7 +15,7 @@ names = {0: "init", 1: "P1", 2: "P2", 3: "P3", 4: "P4", 5: "P5", 6: "P6", 7: "P7
 
 
 SRC_LINES = open(src).read().split("\n")
-KSTART = next(i for i, l in enumerate(SRC_LINES, 1) if "decode_kernel(const KParams P)" in l)
+KSTART = next(i for i, l in enumerate(SRC_LINES, 1) if "decode_kernel(const" in l)
 FUNCS = [(i, re.search(r"(\w+)\(", l).group(1)) for i, l in enumerate(SRC_LINES, 1)
          if re.match(r"^(__device__|template|static|SP_HD)", l) is None and
          re.match(r"^__device__.*\(|^(\w+ )+\w+\(.*", l) and i < KSTART and "(" in l]
