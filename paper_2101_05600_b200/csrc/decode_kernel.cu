@@ -1039,33 +1039,28 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       } else {
         if (warp == kNWarp - 1) eos_items();
         if (staged) {
-        for (int q = warp - nser; q < nc; q += kNWarp - nser) {
-          const int j = items[q].parent, c = items[q].token;
-          const bool repeat = sh.b_last[cur][j] == c;
-          const double* ph = repeat ? stR + (size_t)j * W : phi + (size_t)j * P.Tmax;
-          const float* lc = stL + (size_t)q * W;
-          double mloc = -HUGE_VAL;
-          for (int i = lane; i < W; i += 32) {
-            const double term = log_mul(ph[i], (double)lc[i]);
-            if (!is_zero(term) && term > mloc) mloc = term;
-          }
-          const double M = warp_max_d(mloc);
-          double sum = 0.0;
-          if (M != -HUGE_VAL) {
-            for (int i = lane; i < W; i += 32) {
+          // psi by an online fp64 log-sum-exp, one lane per contender (the
+          // sum runs in a different order from ctc_prefix.cpp:58; ~1e-15
+          // relative)
+          for (int q = (warp - nser) * 32 + lane; q < nc; q += (kNWarp - nser) * 32) {
+            const int j = items[q].parent, c = items[q].token;
+            const bool repeat = sh.b_last[cur][j] == c;
+            const double* ph = repeat ? stR + (size_t)j * W : phi + (size_t)j * P.Tmax;
+            const float* lc = stL + (size_t)q * W;
+            double M = -HUGE_VAL, S = 0.0;
+            for (int i = 0; i < W; ++i) {
               const double term = log_mul(ph[i], (double)lc[i]);
-              if (!is_zero(term)) sum += exp(term - M);
+              if (!is_zero(term)) {
+                const double ex = exp_neg(-fabs(term - M), tb);  // M = -inf: 0
+                S = term > M ? fma(S, ex, 1.0) : S + ex;
+                M = fmax(M, term);
+              }
             }
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-          if (lane == 0) {
-            const double psi = M == -HUGE_VAL ? kLogZero : M + log(sum);
+            const double psi = M == -HUGE_VAL ? kLogZero : M + log_pos(S, tb);
             const double att = __dadd_rn(sh.b_att[cur][j],
                                          P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
             items[q].score = mix_joint(lam, psi, att);
           }
-        }
         }
       }
       gw0 = staged ? nser : 0;

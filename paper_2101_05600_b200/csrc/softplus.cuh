@@ -99,6 +99,47 @@ SP_HD double softplus_neg(double d, const SpTables& tb) {
   return hi + lo;
 }
 
+// exp(d) for d <= 0 (the first half of softplus_neg; 0 below ~-745).
+SP_HD double exp_neg(double d, const SpTables& tb) {
+  const double dd = d < -800.0 ? -800.0 : d;
+  const double n = rint(dd * SP_64_OVER_LN2);
+  double r = fma(-n, SP_LN2_64_HI, dd);
+  r = fma(-n, SP_LN2_64_LO, r);
+  const int ni = (int)n;
+  const double th = tb.thi[ni & 63];
+  const double tl = tb.tlo[ni & 63];
+  const double r2 = r * r;
+  const double a01 = fma(r, 0.5, 1.0);
+  const double a23 = fma(r, 1.0 / 24.0, 1.0 / 6.0);
+  const double a45 = fma(r, 1.0 / 720.0, 1.0 / 120.0);
+  const double r4 = r2 * r2;
+  const double q = r * fma(r4, a45, fma(r2, a23, a01));
+  return (th + fma(th, q, tl)) * sp_pow2(ni >> 6);
+}
+
+// log(x) for a positive normal x (the second half of softplus_neg).
+SP_HD double log_pos(double x, const SpTables& tb) {
+  const long long bits = sp_double_to_bits(x);
+  const int E = (int)(bits >> 52) - 1023;
+  const int jj = (int)((bits >> 46) & 63);
+  const double m = sp_bits_to_double((bits & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+  const double iv = tb.inv[jj];
+  const double rr = fma(m, iv, -1.0);
+  const double s2 = rr * rr;
+  const double b0 = fma(rr, 1.0 / 3.0, -0.5);
+  const double b1 = fma(rr, 1.0 / 5.0, -1.0 / 4.0);
+  const double b2 = fma(rr, 1.0 / 7.0, -1.0 / 6.0);
+  const double b3 = fma(rr, 1.0 / 9.0, -1.0 / 8.0);
+  const double s4 = s2 * s2;
+  const double c0 = fma(s2, b1, b0);
+  const double c1 = fma(s2, -1.0 / 10.0, b3);
+  const double c2 = fma(s4, fma(s2, c1, b2), c0);
+  const double pl = fma(s2, c2, rr);
+  const double hi = fma((double)E, SP_LN2_HI, tb.lh[jj]);
+  const double lo = fma((double)E, SP_LN2_LO, tb.ll[jj]) + pl;
+  return hi + lo;
+}
+
 // log_add (logmath.hpp:19-23) with the reference's exact zero semantics:
 // a zero operand returns the other operand bit-exactly, two zeros return
 // kLogZero exactly.

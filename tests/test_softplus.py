@@ -23,7 +23,7 @@ def spc(tmp_path_factory):
 def run(spc, pairs):
     inp = "\n".join(f"{a!r} {b!r}" for a, b in pairs)
     out = subprocess.run([spc], input=inp, capture_output=True, text=True).stdout.split()
-    return [(float.fromhex(out[2 * i]), float.fromhex(out[2 * i + 1])) for i in range(len(pairs))]
+    return [tuple(float.fromhex(out[4 * i + k]) for k in range(4)) for i in range(len(pairs))]
 
 
 def test_softplus_accuracy(spc):
@@ -38,7 +38,7 @@ def test_softplus_accuracy(spc):
         pairs.append((a, a + d))
     worst = 0.0
     same = 0
-    for (a, b), (sp, la) in zip(pairs, run(spc, pairs)):
+    for (a, b), (sp, la, _, _) in zip(pairs, run(spc, pairs)):
         d = min(a, b) - max(a, b)
         ex = mp.log1p(mp.exp(mp.mpf(d)))
         worst = max(worst, float(abs((mp.mpf(sp) - ex) / ex)) / 2 ** -53)
@@ -54,3 +54,24 @@ def test_log_add_zero_semantics(spc):
     assert res[0][1] == -3.25 and res[1][1] == -3.25
     assert res[2][1] == -1e30 and res[3][1] == -1e30
     assert res[4][1] == math.log(2.0)
+
+
+def test_exp_log_accuracy(spc):
+    """exp_neg / log_pos (the two halves of the softplus, used for the
+    contenders' parallel psi): within 3 ulp of 40-digit values."""
+    mp = pytest.importorskip("mpmath")
+    mp.mp.dps = 40
+    rng = random.Random(11)
+    pairs = [(0.0, -rng.choice([rng.uniform(0, 1), rng.uniform(0, 40), rng.uniform(0, 700),
+                                10 ** rng.uniform(-12, 0)])) for _ in range(4000)]
+    we = wl = 0.0
+    for (_, d), (_, _, e, lg) in zip(pairs, run(spc, pairs)):
+        ex = mp.exp(mp.mpf(d))
+        if ex > mp.mpf(2) ** -1000:
+            we = max(we, float(abs((mp.mpf(e) - ex) / ex)) / 2 ** -53)
+        lx = mp.log(1 - mp.mpf(d))
+        if lx > 0:
+            wl = max(wl, float(abs(mp.mpf(lg) - lx) / max(lx, mp.mpf(1))) / 2 ** -53)
+    assert we <= 3.0 and wl <= 3.0, (we, wl)
+    z = run(spc, [(0.0, 0.0), (0.0, -1e30)])
+    assert z[0][2] == 1.0 and z[0][3] == 0.0 and z[1][2] == 0.0
