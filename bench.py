@@ -44,7 +44,7 @@ def workload_config(n_seg):
                         "-> 2880 x 10 s segments per GPU; CTC grids T_enc=249 x vocab 500 "
                         "flat random posteriors (random-init proxy); batch 64, beam 10, "
                         "lambda 0.3, M1=5, M2=20, eos both; uniform attention scorer "
-                        "(device mock: the Transformer scorer is not built yet)",
+                        "(the Transformer decoder scorer is timed in pipeline_attn)",
             "segments_per_gpu": n_seg, "T_enc": T_ENC, "vocab": VOCAB, "batch": 64,
             "beam": BEAM, "margin_m1": M1, "margin_m2": M2, "ctc_weight": LAMBDA,
             "eos_mode": "both", "scorer": "uniform",
