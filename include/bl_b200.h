@@ -271,11 +271,16 @@ int bl_decode_memory(bl_decoder* d, int n, const bl_utt* utts, int grids_on_devi
  * (memory may be NULL) and writes the 1-best results straight into caller
  * arrays — n_tokens/steps/trigger/joint [n], tokens/label_times [n][cap] —
  * without per-utterance result objects. *stats receives a bl_results holding
- * only the counters/stats/transfer figures (count 0); destroy it as usual. */
+ * only the counters/stats/transfer figures (count 0); destroy it as usual.
+ * When tokens and label_times are page-locked (bl_host_alloc) and cap >= the
+ * step cap, those rows are copied device -> caller directly (no host pass). */
 int bl_decode_into(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
                    const void* memory, int mem_frames, int cap, int* n_tokens, int* steps,
                    int* trigger, double* joint, int* tokens, int* label_times,
                    bl_results** stats);
+/* Page-locked host memory for bl_decode_into's outputs (cudaMallocHost). */
+int bl_host_alloc(size_t bytes, void** out);
+void bl_host_free(void* p);
 /* Record mode (parity tests): keep every scorer row the network produced for
  * a live hypothesis, with the utterance index and the token prefix, so a
  * host replay scorer can drive the reference decoder with identical rows. */

@@ -110,6 +110,9 @@ def lib() -> C.CDLL:
     L.bl_results_export.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p, C.c_void_p, C.c_void_p]
     L.bl_results_destroy.argtypes = [vp]
+    L.bl_host_alloc.argtypes = [C.c_size_t, C.POINTER(vp)]
+    L.bl_host_free.argtypes = [vp]
+    L.bl_host_free.restype = None
     L.bl_encoder_frames_out.argtypes = [C.c_int]
     L.bl_encoder_num_weights.argtypes = [vp]
     L.bl_encoder_num_weights.restype = C.c_size_t
@@ -424,6 +427,58 @@ def save_table_scorer(path: str, scorer: TableScorer) -> None:
         f.write(json.dumps(j) + "\n")
 
 
+class _HostBlock:
+    """A page-locked host buffer leased from _HostPool; returns to the pool
+    when the last numpy view of it (and the block) is gone."""
+
+    def __init__(self, pool, ptr, nbytes):
+        self.pool, self.ptr, self.nbytes = pool, ptr, nbytes
+
+    def array(self, offset, shape, dtype):
+        dt = np.dtype(dtype)
+        view = _BlockView(self, self.ptr + offset, shape, dt.str)
+        return np.asarray(view)
+
+    def __del__(self):
+        try:
+            self.pool.give(self.ptr, self.nbytes)
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class _BlockView:
+    def __init__(self, block, addr, shape, typestr):
+        self.block = block  # keeps the lease alive while a view exists
+        self.__array_interface__ = {"data": (addr, False), "shape": tuple(shape),
+                                    "typestr": typestr, "version": 3}
+
+
+class _HostPool:
+    """Page-locked result blocks (bl_host_alloc), reused across decode calls
+    by size."""
+
+    def __init__(self):
+        self.free = {}
+
+    def take(self, nbytes):
+        lst = self.free.get(nbytes)
+        if lst:
+            return _HostBlock(self, lst.pop(), nbytes)
+        p = C.c_void_p()
+        _check(lib().bl_host_alloc(nbytes, C.byref(p)))
+        return _HostBlock(self, p.value, nbytes)
+
+    def give(self, ptr, nbytes):
+        lst = self.free.setdefault(nbytes, [])
+        if len(lst) < 4:
+            lst.append(ptr)
+        else:
+            lib().bl_host_free(ptr)
+
+
+_HOST_POOL = _HostPool()
+
+
 class ResultSet(_Seq):
     """Results of one decode call as flat arrays (one bulk export from the
     C ABI); indexing materialises DecodeResult objects lazily."""
@@ -533,12 +588,15 @@ class Decoder:
         if self.nbest == 1 and n > 0:
             # bulk path: 1-best results written straight into numpy arrays
             cap = max(1, int(rec["num_frames"][:n].max()))
-            nt = np.empty(n, np.int32)
-            st = np.empty(n, np.int32)
-            tr = np.empty(n, np.int32)
-            jt = np.empty(n, np.float64)
-            tok = np.empty((n, cap), np.int32)
-            lt = np.empty((n, cap), np.int32)
+            # page-locked, reused result block: the library copies token and
+            # label-time rows straight into it (no first-touch page faults)
+            blk = _HOST_POOL.take(n * (24 + 8 * cap))
+            jt = blk.array(0, (n,), np.float64)
+            nt = blk.array(8 * n, (n,), np.int32)
+            st = blk.array(12 * n, (n,), np.int32)
+            tr = blk.array(16 * n, (n,), np.int32)
+            tok = blk.array(24 * n, (n, cap), np.int32)
+            lt = blk.array(24 * n + 4 * n * cap, (n, cap), np.int32)
             _check(lib().bl_decode_into(
                 self._h, n, rec.ctypes.data_as(C.POINTER(_Utt)), 1 if on_device else 0,
                 C.c_void_p(memory) if memory is not None else None, mem_frames, cap,

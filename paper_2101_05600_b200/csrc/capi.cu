@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -453,6 +454,9 @@ struct IntoArgs {
 
 int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
                 bl_results** out, const IntoArgs* into = nullptr) {
+  using clk = std::chrono::steady_clock;
+  static const bool host_timing = std::getenv("BL_HOST_TIMING") != nullptr;
+  const auto t_in = clk::now();
   validate_cfg(d->cfg);  // batched.cpp:97
   auto res = std::make_unique<bl_results>();
   if (n == 0) {  // batched.cpp:99
@@ -702,6 +706,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       d->ev_copy.push_back(e);
     }
   }
+  const auto t_launch = clk::now();
   CK(cudaEventRecord(d->ev0, st));  // timing start; copies start after the descriptors
   if (!on_device) CK(cudaStreamWaitEvent(d->copy, d->ev0, 0));
   if (nchunk > 1) CK(cudaStreamWaitEvent(d->alt, d->ev0, 0));
@@ -737,14 +742,39 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     CK(cudaStreamWaitEvent(st, d->ev_alt, 0));
   }
   CK(cudaEventRecord(d->ev1, st));
-  CK(cudaMemcpyAsync(d->h_res.p, d->res.p, sizeof(int) * (size_t)U * rs,
-                     cudaMemcpyDeviceToHost, st));
+  // 1-best export into page-locked caller arrays: headers, tokens and label
+  // times go straight to their final [n][cap] rows (three 2D copies, no
+  // host-side repacking); otherwise the whole result block is copied.
+  bool direct = false;
+  if (into && into->cap >= S) {
+    cudaPointerAttributes a{}, b{};
+    direct = cudaPointerGetAttributes(&a, into->tokens) == cudaSuccess &&
+             a.type == cudaMemoryTypeHost &&
+             cudaPointerGetAttributes(&b, into->label_times) == cudaSuccess &&
+             b.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+  }
+  const int* dres = static_cast<const int*>(d->res.p);
+  if (direct) {
+    const size_t sp = sizeof(int) * (size_t)rs, dp = sizeof(int) * (size_t)into->cap;
+    CK(cudaMemcpy2DAsync(d->h_res.p, sizeof(int) * bl::kResHdr, dres, sp,
+                         sizeof(int) * bl::kResHdr, U, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpy2DAsync(into->tokens, dp, dres + bl::kResHdr, sp, sizeof(int) * (size_t)S, U,
+                         cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpy2DAsync(into->label_times, dp, dres + bl::kResHdr + S, sp,
+                         sizeof(int) * (size_t)S, U, cudaMemcpyDeviceToHost, st));
+  } else {
+    CK(cudaMemcpyAsync(d->h_res.p, dres, sizeof(int) * (size_t)U * rs, cudaMemcpyDeviceToHost,
+                       st));
+  }
   CK(cudaMemcpyAsync(d->h_cnt.p, d->cnt.p, sizeof(unsigned long long) * (size_t)U * 8,
                      cudaMemcpyDeviceToHost, st));
   if (d->profile)
     CK(cudaMemcpyAsync(d->h_prof.p, d->prof.p, sizeof(long long) * (size_t)U * 16,
                        cudaMemcpyDeviceToHost, st));
+  const auto t_enq = clk::now();
   CK(cudaStreamSynchronize(st));
+  const auto t_sync = clk::now();
   if (d->profile) {
     const long long* hp = static_cast<const long long*>(d->h_prof.p);
     for (int i = 0; i < U; ++i)
@@ -754,22 +784,26 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
   res->kernel_ms = ms;
   res->launches = launches;
-  res->d2h = sizeof(int) * (size_t)U * rs + sizeof(unsigned long long) * (size_t)U * 8;
+  res->d2h = (direct ? sizeof(int) * (size_t)U * (bl::kResHdr + 2 * (size_t)S)
+                     : sizeof(int) * (size_t)U * rs) +
+             sizeof(unsigned long long) * (size_t)U * 8;
 
   const int* hr = static_cast<const int*>(d->h_res.p);
   const unsigned long long* hc = static_cast<const unsigned long long*>(d->h_cnt.p);
   if (into) {
     for (int i = 0; i < n; ++i) {
-      const int* r = hr + (size_t)i * rs;
+      const int* r = hr + (size_t)i * (direct ? bl::kResHdr : rs);
       const int nt = r[0];
       if (nt > into->cap) throw std::invalid_argument("result longer than the export capacity");
       into->n_tokens[i] = nt;
       into->steps[i] = r[1];
       into->trigger[i] = r[2];
       std::memcpy(into->joint + i, r + 4, sizeof(double));
-      std::memcpy(into->tokens + (size_t)i * into->cap, r + bl::kResHdr, sizeof(int) * nt);
-      std::memcpy(into->label_times + (size_t)i * into->cap, r + bl::kResHdr + S,
-                  sizeof(int) * nt);
+      if (!direct) {
+        std::memcpy(into->tokens + (size_t)i * into->cap, r + bl::kResHdr, sizeof(int) * nt);
+        std::memcpy(into->label_times + (size_t)i * into->cap, r + bl::kResHdr + S,
+                    sizeof(int) * nt);
+      }
       res->max_tokens = std::max(res->max_tokens, nt);
       const unsigned long long* c = hc + (size_t)i * 8;
       res->steps += c[0];
@@ -778,6 +812,14 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       res->k1 += c[3];
       res->fallback += c[4];
       res->contenders += c[5];
+    }
+    if (host_timing) {
+      auto ms = [](clk::time_point a, clk::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+      };
+      std::fprintf(stderr, "[bl host] plan %.3f  enqueue %.3f  wait %.3f (kernel %.3f)  export %.3f ms\n",
+                   ms(t_in, t_launch), ms(t_launch, t_enq), ms(t_enq, t_sync), res->kernel_ms,
+                   ms(t_sync, clk::now()));
     }
     *out = res.release();  // counters and stats only
     return BL_OK;
@@ -1157,6 +1199,19 @@ int bl_decode(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     d->mem_frames = 0;
     return decode_impl(d, n, utts, on_device, out);
   });
+}
+
+int bl_host_alloc(size_t bytes, void** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("bl_host_alloc: null out");
+    *out = nullptr;
+    CK(cudaMallocHost(out, bytes ? bytes : 1));
+    return BL_OK;
+  });
+}
+
+void bl_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 int bl_decode_into(bl_decoder* d, int n, const bl_utt* utts, int grids_on_device,
