@@ -256,6 +256,12 @@ struct bl_decoder {
   };
   std::vector<Rec> rec;
   DevBuf rec_nb, nb_live;
+  // streamed host input (see KParams::ready)
+  DevBuf ready, stream_err;
+  HostBuf h_epoch, h_err;
+  unsigned epoch = 0;
+  size_t ready_n = 0;
+  cudaEvent_t ev_copied = nullptr;
 };
 
 struct bl_results {
@@ -674,6 +680,43 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     desc[i].grid = on_device ? utts[i].logp
                              : static_cast<const float*>(d->grid.p) + goff[i];
     desc[i].row0 = (int)(goff[i] / V);
+    desc[i].chunk = 0;
+  }
+  // Streamed host input: ONE launch; the copy stream lands the grids chunk
+  // by chunk and flags each one, and every CTA starts as soon as its own
+  // chunk is in HBM.
+  const bool stepm0 = d->step_mode != 0 || d->net != nullptr;
+  const bool stream_in = !on_device && !stepm0 && U >= 296 &&
+                         std::getenv("BL_NO_STREAM_IN") == nullptr;
+  std::vector<int> bnd{0};
+  if (stream_in) {
+    // 32-utterance chunks while the first two waves of CTAs ramp up (each
+    // starts as soon as its own chunk lands), then doubling up to 1024
+    int want = 32;
+    while (bnd.back() < U) {
+      int b = std::min(U, bnd.back() + want);
+      while (b < U && ((goff[b] * sizeof(float)) & 127) != 0) ++b;  // no shared 128-B line
+      bnd.push_back(b);
+      if (b >= 888) want = std::min(2 * want, 1024);
+    }
+    for (size_t k = 0; k + 1 < bnd.size(); ++k)
+      for (int i = bnd[k]; i < bnd[k + 1]; ++i) desc[i].chunk = (int)k;
+    const size_t nck = bnd.size() - 1;
+    if (d->ready_n < nck) {
+      d->ready.ensure(sizeof(unsigned) * nck);
+      CK(cudaMemsetAsync(d->ready.p, 0, sizeof(unsigned) * nck, st));
+      d->ready_n = nck;
+    }
+    d->stream_err.ensure(sizeof(int));
+    d->h_epoch.ensure(sizeof(unsigned));
+    d->h_err.ensure(sizeof(int));
+    if (++d->epoch == 0) d->epoch = 1;
+    *static_cast<unsigned*>(d->h_epoch.p) = d->epoch;
+    CK(cudaMemsetAsync(d->stream_err.p, 0, sizeof(int), st));
+    if (!d->ev_copied) CK(cudaEventCreateWithFlags(&d->ev_copied, cudaEventDisableTiming));
+    p.ready = static_cast<const unsigned*>(d->ready.p);
+    p.ready_epoch = d->epoch;
+    p.stream_err = static_cast<int*>(d->stream_err.p);
   }
   std::memcpy(d->h_utts.p, desc.data(), sizeof(bl::UttDesc) * U);
   {
@@ -698,7 +741,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       throw std::invalid_argument("the transformer scorer needs the encoder memory "
                                   "(bl_decode_memory)");
   }
-  const int nchunk = (on_device || stepm) ? 1 : std::max(1, std::min(16, U / 360));
+  const int nchunk = (on_device || stepm || stream_in) ? 1 : std::max(1, std::min(16, U / 360));
   if ((int)d->ev_copy.size() < nchunk) {
     for (int k = (int)d->ev_copy.size(); k < nchunk; ++k) {
       cudaEvent_t e;
@@ -711,7 +754,29 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   if (!on_device) CK(cudaStreamWaitEvent(d->copy, d->ev0, 0));
   if (nchunk > 1) CK(cudaStreamWaitEvent(d->alt, d->ev0, 0));
   int launches = 0;
-  for (int k = 0; k < nchunk; ++k) {
+  if (stream_in) {
+    CK(cudaStreamWaitEvent(d->copy, d->ev0, 0));
+    CK(bl::launch_decode(p, st));
+    ++launches;
+    unsigned* rdy = static_cast<unsigned*>(d->ready.p);
+    for (size_t k = 0; k + 1 < bnd.size(); ++k) {
+      const int a = bnd[k], b = bnd[k + 1];
+      for (const auto& r : runs) {
+        const int i0 = std::max(r.i0, a), i1 = std::min(r.i1, b);
+        if (i0 >= i1) continue;
+        const size_t len = goff[i1 - 1] + (size_t)desc[i1 - 1].T * V - goff[i0];
+        CK(cudaMemcpyAsync(static_cast<float*>(d->grid.p) + goff[i0],
+                           r.src + (goff[i0] - goff[r.i0]), sizeof(float) * len,
+                           cudaMemcpyHostToDevice, d->copy));
+        res->h2d += sizeof(float) * len;
+      }
+      CK(cudaMemcpyAsync(rdy + k, d->h_epoch.p, sizeof(unsigned), cudaMemcpyHostToDevice,
+                         d->copy));
+    }
+    CK(cudaEventRecord(d->ev_copied, d->copy));
+    CK(cudaStreamWaitEvent(st, d->ev_copied, 0));
+  }
+  for (int k = 0; k < nchunk && !stream_in; ++k) {
     const int a = (int)((long long)U * k / nchunk), b = (int)((long long)U * (k + 1) / nchunk);
     if (!on_device) {
       for (const auto& r : runs) {
@@ -769,12 +834,16 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   }
   CK(cudaMemcpyAsync(d->h_cnt.p, d->cnt.p, sizeof(unsigned long long) * (size_t)U * 8,
                      cudaMemcpyDeviceToHost, st));
+  if (stream_in)
+    CK(cudaMemcpyAsync(d->h_err.p, d->stream_err.p, sizeof(int), cudaMemcpyDeviceToHost, st));
   if (d->profile)
     CK(cudaMemcpyAsync(d->h_prof.p, d->prof.p, sizeof(long long) * (size_t)U * 16,
                        cudaMemcpyDeviceToHost, st));
   const auto t_enq = clk::now();
   CK(cudaStreamSynchronize(st));
   const auto t_sync = clk::now();
+  if (stream_in && *static_cast<const int*>(d->h_err.p))
+    throw BlError{BL_CUDA_ERROR, "streamed input: a grid chunk never reached the device"};
   if (d->profile) {
     const long long* hp = static_cast<const long long*>(d->h_prof.p);
     for (int i = 0; i < U; ++i)
@@ -1188,6 +1257,7 @@ void bl_decoder_destroy(bl_decoder* d) {
   if (d->copy) cudaStreamDestroy(d->copy);
   if (d->alt) cudaStreamDestroy(d->alt);
   if (d->ev_alt) cudaEventDestroy(d->ev_alt);
+  if (d->ev_copied) cudaEventDestroy(d->ev_copied);
   if (d->own) cudaStreamDestroy(d->own);
   delete d;
 }

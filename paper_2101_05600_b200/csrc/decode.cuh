@@ -19,6 +19,7 @@ struct UttDesc {
   int max_steps;      // ceil(max_steps_ratio * T), batched.cpp:112-113
   int need_tail;      // margin_m2 < T: eos tails need the F/G tables
   int row0;           // first row of this utterance in the TMA tensor map
+  int chunk;          // streamed host input: the copy chunk holding this grid
 };
 
 // Finished (eos-ended) entry, FinishedEntry (beam_search.hpp:53-61) with a
@@ -103,6 +104,12 @@ struct KParams {
   int net_rows;
   int* rec_nb;  // optional [U][S+2]: live beam size at the start of each step
   int* nb_out;  // optional [U]: live beam size entering the next step (0 once finished)
+  // streamed host input: the CTA of utterance u starts once
+  // ready[utts[u].chunk] == ready_epoch (written by the copy stream after
+  // that chunk's grids); a chunk that never arrives sets *stream_err
+  const unsigned* ready;
+  unsigned ready_epoch;
+  int* stream_err;
 };
 
 // Dynamic shared-memory plan (identical on host and device).

@@ -415,6 +415,26 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
   }
   for (int i = tid; i < 320; i += kNT)
     reinterpret_cast<double*>(&tb)[i] = reinterpret_cast<const double*>(&c_sptab)[i];
+  if (P.ready) {
+    // streamed host input: wait for this utterance's copy chunk (acquire;
+    // chunk boundaries are 128-byte aligned, so no line of this grid was
+    // cached by a CTA of an earlier chunk)
+    if (tid == 0) {
+      const unsigned* f = P.ready + ud.chunk;
+      const long long t0 = clock64();
+      for (;;) {
+        unsigned v;
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v == P.ready_epoch) break;
+        if (clock64() - t0 > (1ll << 36)) {  // ~35 s: the copy never landed
+          atomicExch(P.stream_err, 1);
+          break;
+        }
+        __nanosleep(1000);
+      }
+    }
+    __syncthreads();
+  }
   if (stepm && P.step_l > 1) {
     // resume: the search state saved at the end of step l-1
     const int* src = reinterpret_cast<const int*>(st_u + 16);
