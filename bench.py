@@ -261,7 +261,7 @@ def run_prefix_c3(torch, bl, dev, peak, n=592):
     out = {"segments": n, "vocab": V, "kernel_ms": st["kernel_ms"], "k1_bytes": st["k1_bytes"],
            "k1_gbs": gbs, "peak_gbs": peak[0], "frac": gbs / peak[0],
            "audio_s_per_s": n * T_ENC * FRAME_SHIFT_MS / 1000.0 / (st["kernel_ms"] / 1000.0),
-           "kernel": "decode_kernel<12, TMA> (K1 slab streamed by cp.async.bulk.tensor)"}
+           "kernel": "decode_kernel<10, TMA> (K1 slab streamed by cp.async.bulk.tensor)"}
     del g, dec
     torch.cuda.empty_cache()
     return out

@@ -920,20 +920,39 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // list; the exact theta (B-th largest lower bound) is ranked inside it
       // and the contenders are the list entries that reach max(theta, theta0).
       const float theta0 = sh.theta;
-      for (int kidx = tid; kidx < nb * C; kidx += kNT) {
-        const float ku = kub[kidx];
-        if (ku >= theta0) {
-          const int q = kidx / C, c = kidx - q * C;
-          if (c != sh.b_last[cur][q]) {
-            const int idx = atomicAdd(&sh.n_list, 1);
-            if (idx < kListCap) {
-              const bool under = (ubits[kidx >> 5] >> (kidx & 31)) & 1u;
-              // derived lower bound: never above the key's true lower bound
-              clist[idx] = make_float4(
-                  under ? -INFINITY : ku - 2.000002f * (hw + (fabsf(ku) + hw) * 2.4e-7f), ku,
-                  __int_as_float(q), __int_as_float(c));
-            }
+      auto list_key = [&](int kidx, float ku) {
+        const int q = kidx / C, c = kidx - q * C;
+        if (c != sh.b_last[cur][q]) {
+          const int idx = atomicAdd(&sh.n_list, 1);
+          if (idx < kListCap) {
+            const bool under = (ubits[kidx >> 5] >> (kidx & 31)) & 1u;
+            // derived lower bound: never above the key's true lower bound
+            clist[idx] = make_float4(
+                under ? -INFINITY : ku - 2.000002f * (hw + (fabsf(ku) + hw) * 2.4e-7f), ku,
+                __int_as_float(q), __int_as_float(c));
           }
+        }
+      };
+      const int nkeys = nb * C;
+      if (P.kub_smem) {
+        for (int kidx = tid; kidx < nkeys; kidx += kNT) {
+          const float ku = kub[kidx];
+          if (ku >= theta0) list_key(kidx, ku);
+        }
+      } else {
+        // upper keys in HBM: kScan independent loads per thread before any
+        // test (one dependent load per key would serialise their latency)
+        constexpr int kScan = 8;
+        for (int k0 = tid; k0 < nkeys; k0 += kScan * kNT) {
+          float ku[kScan];
+#pragma unroll
+          for (int r = 0; r < kScan; ++r) {
+            const int kidx = k0 + r * kNT;
+            ku[r] = kidx < nkeys ? kub[kidx] : -INFINITY;
+          }
+#pragma unroll
+          for (int r = 0; r < kScan; ++r)
+            if (ku[r] >= theta0) list_key(k0 + r * kNT, ku[r]);
         }
       }
       __syncthreads();
