@@ -799,10 +799,26 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
             const float* sb = stages + (size_t)st * (kTmaStageBytes / 4) + colb;
             const int nrow = min(kTmaRows, W - k * kTmaRows);
             const int f0 = k * kTmaRows;
-            for (int i = 0; i < nrow; ++i) {
-              const float2 v = *reinterpret_cast<const float2*>(sb + i * kTmaBoxCols);
-              acc(S0, m0, v.x, phr + (f0 + i) * phs);
-              acc(S1, m1, v.y, phr + (f0 + i) * phs);
+            constexpr int kRu = 4;  // rows per unrolled group
+            if (nrow == kTmaRows) {  // full chunk: rows unrolled so their loads and exps overlap
+#pragma unroll
+              for (int i0 = 0; i0 < kTmaRows; i0 += kRu) {
+                float2 v[kRu];
+#pragma unroll
+                for (int k2 = 0; k2 < kRu; ++k2)
+                  v[k2] = *reinterpret_cast<const float2*>(sb + (i0 + k2) * kTmaBoxCols);
+#pragma unroll
+                for (int k2 = 0; k2 < kRu; ++k2) {
+                  acc(S0, m0, v[k2].x, phr + (f0 + i0 + k2) * phs);
+                  acc(S1, m1, v[k2].y, phr + (f0 + i0 + k2) * phs);
+                }
+              }
+            } else {
+              for (int i = 0; i < nrow; ++i) {
+                const float2 v = *reinterpret_cast<const float2*>(sb + i * kTmaBoxCols);
+                acc(S0, m0, v.x, phr + (f0 + i) * phs);
+                acc(S1, m1, v.y, phr + (f0 + i) * phs);
+              }
             }
             if (k == nch - 1) emit_keys(c0, two, S0, S1, m0, two ? m1 : gf, r0s, r1s);
           }
