@@ -136,15 +136,28 @@ __global__ void dec_self_attn_kernel(int l, const __nv_bfloat16* __restrict__ qk
   }
   const float scale = rsqrtf((float)kDk);
   float m = -INFINITY;
-  for (int p0 = 0; p0 < l; p0 += 8) {
-    const int p = p0 + pp;
-    float s = 0.f;
-    if (p < l) {
-      const uint4* ks = reinterpret_cast<const uint4*>(kv_at(p, sl[p]) + qd * 16);
+  // two 8-position passes per iteration: four 16-byte K loads per lane in
+  // flight before the dot products
+  for (int p0 = 0; p0 < l; p0 += 16) {
+    uint4 kw[2][2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int p = p0 + 8 * r + pp;
+      if (p < l) {
+        const uint4* ks = reinterpret_cast<const uint4*>(kv_at(p, sl[p]) + qd * 16);
+        kw[r][0] = ks[0];
+        kw[r][1] = ks[1];
+      } else {
+        kw[r][0] = kw[r][1] = make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int p = p0 + 8 * r + pp;
+      float s = 0.f;
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        const uint4 w = ks[i];
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&kw[r][i]);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float2 f = __bfloat1622float2(b2[j]);
@@ -152,13 +165,13 @@ __global__ void dec_self_attn_kernel(int l, const __nv_bfloat16* __restrict__ qk
           s = fmaf(q[i * 8 + 2 * j + 1], f.y, s);
         }
       }
-    }
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    if (p < l) {
-      s *= scale;
-      if (qd == 0) sc[p] = s;
-      m = fmaxf(m, s);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (p < l) {
+        s *= scale;
+        if (qd == 0) sc[p] = s;
+        m = fmaxf(m, s);
+      }
     }
   }
 #pragma unroll
@@ -173,17 +186,44 @@ __global__ void dec_self_attn_kernel(int l, const __nv_bfloat16* __restrict__ qk
 #pragma unroll
   for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
   __syncwarp();
-  float a0 = 0.f, a1 = 0.f;
-  for (int p = 0; p < l; ++p) {
+  // weighted V sum: 8 lanes x 8 dims (16-byte loads) per position, 4
+  // positions per warp pass and two passes unrolled, so 8 independent row
+  // loads are in flight per warp; the 4 position groups are summed at the end
+  const int vd = lane & 7, vp = lane >> 3;
+  float a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) a[i] = 0.f;
+  auto vacc = [&](int p) {
     const float w = sc[p];
-    const float2 v = __bfloat1622float2(
-        reinterpret_cast<const __nv_bfloat162*>(kv_at(p, sl[p]) + d)[lane]);
-    a0 = fmaf(w, v.x, a0);
-    a1 = fmaf(w, v.y, a1);
+    const uint4 raw = *reinterpret_cast<const uint4*>(kv_at(p, sl[p]) + d + vd * 8);
+    const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float2 f = __bfloat1622float2(b2[j]);
+      a[2 * j] = fmaf(w, f.x, a[2 * j]);
+      a[2 * j + 1] = fmaf(w, f.y, a[2 * j + 1]);
+    }
+  };
+  int p0 = 0;
+  for (; p0 + 8 <= l; p0 += 8) {
+    vacc(p0 + vp);
+    vacc(p0 + 4 + vp);
   }
-  const float inv = 1.f / sum;
-  reinterpret_cast<__nv_bfloat162*>(out + (size_t)R * d + h * kDk)[lane] =
-      __floats2bfloat162_rn(a0 * inv, a1 * inv);
+  if (p0 + vp < l) vacc(p0 + vp);
+  if (p0 + 4 + vp < l) vacc(p0 + 4 + vp);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    a[i] += __shfl_xor_sync(0xffffffffu, a[i], 8);
+    a[i] += __shfl_xor_sync(0xffffffffu, a[i], 16);
+  }
+  if (vp == 0) {
+    const float inv = 1.f / sum;
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o2[j] = __floats2bfloat162_rn(a[2 * j] * inv, a[2 * j + 1] * inv);
+    *reinterpret_cast<uint4*>(out + (size_t)R * d + h * kDk + vd * 8) = o;
+  }
 }
 
 // Source attention on the warp-level tensor path. Per (utterance, head) the
