@@ -755,9 +755,10 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   if (nchunk > 1) CK(cudaStreamWaitEvent(d->alt, d->ev0, 0));
   int launches = 0;
   if (stream_in) {
+    // copies and flags are enqueued BEFORE the kernel: under serialising
+    // tools (CUDA_LAUNCH_BLOCKING=1, profiler kernel replay) every flag is
+    // then already set when the kernel runs, instead of never arriving
     CK(cudaStreamWaitEvent(d->copy, d->ev0, 0));
-    CK(bl::launch_decode(p, st));
-    ++launches;
     unsigned* rdy = static_cast<unsigned*>(d->ready.p);
     for (size_t k = 0; k + 1 < bnd.size(); ++k) {
       const int a = bnd[k], b = bnd[k + 1];
@@ -774,6 +775,8 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
                          d->copy));
     }
     CK(cudaEventRecord(d->ev_copied, d->copy));
+    CK(bl::launch_decode(p, st));
+    ++launches;
     CK(cudaStreamWaitEvent(st, d->ev_copied, 0));
   }
   for (int k = 0; k < nchunk && !stream_in; ++k) {

@@ -45,3 +45,25 @@ def test_streamed_host_input_equals_device_input(V, T, ragged, pinned):
         for g, w in zip(got, want):
             assert g.tokens == w.tokens and g.label_times == w.label_times
             assert g.steps_taken == w.steps_taken and g.joint_logp == w.joint_logp
+
+
+def test_streamed_input_under_launch_blocking():
+    """Copies and ready flags are enqueued before the kernel, so a
+    serialising environment (CUDA_LAUNCH_BLOCKING=1, profiler replay) still
+    decodes instead of spinning until the watchdog."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_2101_05600_b200 as bl\n"
+        "r = np.random.default_rng(0)\n"
+        "g = r.standard_normal((400, 30, 9)).astype(np.float32)\n"
+        "g -= np.log(np.exp(g).sum(2, keepdims=True))\n"
+        "d = bl.Decoder(bl.UniformScorer(8), bl.DecoderConfig(beam_width=3))\n"
+        "res = d.decode([bl.Utterance(f'u{i}', bl.PosteriorGrid(g[i])) for i in range(400)])\n"
+        "assert len(res) == 400 and d.last_stats['launches'] == 1\n")
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, timeout=180,
+                       capture_output=True, text=True)
+    assert p.returncode == 0, p.stderr[-2000:]
