@@ -280,13 +280,18 @@ __device__ void child_state_lanes(const double* ph, const float* lc, const float
   const int lo = tau_p > 1 ? tau_p : 1;
   int best = lo;
   double val = kLogZero, g_prev = kLogZero;
+  // branch-free roles: both lanes load ph[i] (valid for either), each its own
+  // x column; the store walks a pointer
+  const float* xs = role == 0 ? lc : lb;
+  double* gp = gout + s;
   for (int i = 0; i < W; ++i) {
     const int t = s + i;
     const double gn_partner = __shfl_xor_sync(0xffffffffu, g_prev, 1);
-    const double b = role == 0 ? ph[i] : gn_partner;
-    const double x = role == 0 ? (double)lc[i] : (double)lb[i];
+    const double phv = ph[i];
+    const double b = role == 0 ? phv : gn_partner;
+    const double x = (double)xs[i];
     const double g = log_mul(log_add(g_prev, b, tb), x);
-    if (live) gout[t] = g;
+    if (live) gp[i] = g;
     if (t >= lo && g > val) {
       val = g;
       best = t;

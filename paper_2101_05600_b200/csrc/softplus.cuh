@@ -66,16 +66,24 @@ SP_HD long long sp_double_to_bits(double d) {
 SP_HD double sp_pow2(int k) {  // 2^k, 0 below the normal range
   return k < -1022 ? 0.0 : sp_bits_to_double((long long)(k + 1023) << 52);
 }
+// rint(x) for |x| < 2^51 and the same value as an int, by the 1.5*2^52
+// shifter (x + 1.5*2^52 rounds to an integer, round-half-even like rint; its
+// low word is the integer): two DADDs instead of FRND + F2I conversions.
+SP_HD double sp_rint_int(double x, int* ni) {
+  const double t = x + 6755399441055744.0;
+  *ni = (int)(unsigned)(sp_double_to_bits(t) & 0xffffffffLL);
+  return t - 6755399441055744.0;
+}
 
 // log1p(exp(d)) for d <= 0 (any d; very negative d returns ~exp(d) or 0).
 // Polynomials are evaluated in Estrin form to shorten the dependent chain.
 SP_HD double softplus_neg(double d, const SpTables& tb) {
   // exp(d) = 2^k * 2^(j/64) * exp(r)
-  const double dd = d < -800.0 ? -800.0 : d;
-  const double n = rint(dd * SPK(k64ln2, SP_64_OVER_LN2));
+  const double dd = fmax(d, -800.0);
+  int ni;
+  const double n = sp_rint_int(dd * SPK(k64ln2, SP_64_OVER_LN2), &ni);
   double r = fma(-n, SPK(ln2_64_hi, SP_LN2_64_HI), dd);
   r = fma(-n, SPK(ln2_64_lo, SP_LN2_64_LO), r);
-  const int ni = (int)n;
   const int j = ni & 63;
   const int k = ni >> 6;  // floor division (arithmetic shift)
   const double th = tb.thi[j];
@@ -110,7 +118,7 @@ SP_HD double softplus_neg(double d, const SpTables& tb) {
   const double c1 = fma(s2, SPK(m10, -1.0 / 10.0), b3);
   const double c2 = fma(s4, fma(s2, c1, b2), c0);       // b0 + s2 b1 + s4 (b2 + s2 b3 + s4 (-1/10))
   const double pl = fma(s2, c2, rr);                    // log1p(rr)
-  const double Ed = (double)E;
+  const double Ed = E ? 1.0 : 0.0;  // E is 0 or 1 here
   const double corr = c * iv * (E ? 0.5 : 1.0);  // c / u
   const double hi = fma(Ed, SPK(ln2_hi, SP_LN2_HI), lh);
   const double lo = fma(Ed, SPK(ln2_lo, SP_LN2_LO), ll) + pl + corr;
@@ -119,11 +127,11 @@ SP_HD double softplus_neg(double d, const SpTables& tb) {
 
 // exp(d) for d <= 0 (the first half of softplus_neg; 0 below ~-745).
 SP_HD double exp_neg(double d, const SpTables& tb) {
-  const double dd = d < -800.0 ? -800.0 : d;
-  const double n = rint(dd * SPK(k64ln2, SP_64_OVER_LN2));
+  const double dd = fmax(d, -800.0);
+  int ni;
+  const double n = sp_rint_int(dd * SPK(k64ln2, SP_64_OVER_LN2), &ni);
   double r = fma(-n, SPK(ln2_64_hi, SP_LN2_64_HI), dd);
   r = fma(-n, SPK(ln2_64_lo, SP_LN2_64_LO), r);
-  const int ni = (int)n;
   const double th = tb.thi[ni & 63];
   const double tl = tb.tlo[ni & 63];
   const double r2 = r * r;
@@ -179,11 +187,12 @@ SP_HD void log_add2(double a1, double b1, double a2, double b2, const SpTables& 
   const double mx1 = a1 < b1 ? b1 : a1, mn1 = a1 < b1 ? a1 : b1;
   const double mx2 = a2 < b2 ? b2 : a2, mn2 = a2 < b2 ? a2 : b2;
   const double dd1 = fmax(mn1 - mx1, -800.0), dd2 = fmax(mn2 - mx2, -800.0);
-  const double n1 = rint(dd1 * SPK(k64ln2, SP_64_OVER_LN2)), n2 = rint(dd2 * SPK(k64ln2, SP_64_OVER_LN2));
+  int ni1, ni2;
+  const double n1 = sp_rint_int(dd1 * SPK(k64ln2, SP_64_OVER_LN2), &ni1);
+  const double n2 = sp_rint_int(dd2 * SPK(k64ln2, SP_64_OVER_LN2), &ni2);
   double r1 = fma(-n1, SPK(ln2_64_hi, SP_LN2_64_HI), dd1), r2 = fma(-n2, SPK(ln2_64_hi, SP_LN2_64_HI), dd2);
   r1 = fma(-n1, SPK(ln2_64_lo, SP_LN2_64_LO), r1);
   r2 = fma(-n2, SPK(ln2_64_lo, SP_LN2_64_LO), r2);
-  const int ni1 = (int)n1, ni2 = (int)n2;
   const double th1 = tb.thi[ni1 & 63], th2 = tb.thi[ni2 & 63];
   const double tl1 = tb.tlo[ni1 & 63], tl2 = tb.tlo[ni2 & 63];
   const double p1 = sp_pow2(ni1 >> 6), p2 = sp_pow2(ni2 >> 6);
@@ -217,9 +226,10 @@ SP_HD void log_add2(double a1, double b1, double a2, double b2, const SpTables& 
   const double d21 = fma(s41, fma(s21, c11, b21), c01), d22 = fma(s42, fma(s22, c12, b22), c02);
   const double pl1 = fma(s21, d21, rr1), pl2 = fma(s22, d22, rr2);
   const double cr1 = c1 * iv1 * (E1 ? 0.5 : 1.0), cr2 = c2 * iv2 * (E2 ? 0.5 : 1.0);
-  const double h1 = fma((double)E1, SPK(ln2_hi, SP_LN2_HI), lh1), h2 = fma((double)E2, SPK(ln2_hi, SP_LN2_HI), lh2);
-  const double l1 = fma((double)E1, SPK(ln2_lo, SP_LN2_LO), ll1) + pl1 + cr1;
-  const double l2 = fma((double)E2, SPK(ln2_lo, SP_LN2_LO), ll2) + pl2 + cr2;
+  const double Ed1 = E1 ? 1.0 : 0.0, Ed2 = E2 ? 1.0 : 0.0;  // 0 or 1
+  const double h1 = fma(Ed1, SPK(ln2_hi, SP_LN2_HI), lh1), h2 = fma(Ed2, SPK(ln2_hi, SP_LN2_HI), lh2);
+  const double l1 = fma(Ed1, SPK(ln2_lo, SP_LN2_LO), ll1) + pl1 + cr1;
+  const double l2 = fma(Ed2, SPK(ln2_lo, SP_LN2_LO), ll2) + pl2 + cr2;
   const double s1 = mx1 + (h1 + l1), s2 = mx2 + (h2 + l2);
   const double z1 = mn1 <= -1e29 ? mx1 : s1, z2 = mn2 <= -1e29 ? mx2 : s2;
   *o1 = mx1 <= -1e29 ? -1e30 : z1;
