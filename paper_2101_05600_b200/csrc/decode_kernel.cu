@@ -941,8 +941,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // list; the exact theta (B-th largest lower bound) is ranked inside it
       // and the contenders are the list entries that reach max(theta, theta0).
       const float theta0 = sh.theta;
-      auto list_key = [&](int kidx, float ku) {
-        const int q = kidx / C, c = kidx - q * C;
+      auto list_key_qc = [&](int kidx, int q, int c, float ku) {
         if (c != sh.b_last[cur][q]) {
           const int idx = atomicAdd(&sh.n_list, 1);
           if (idx < kListCap) {
@@ -954,8 +953,24 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           }
         }
       };
+      auto list_key = [&](int kidx, float ku) {
+        const int q = kidx / C;
+        list_key_qc(kidx, q, kidx - q * C, ku);
+      };
       const int nkeys = nb * C;
-      if (P.kub_smem) {
+      if (P.kub_smem && C >= kNT) {
+        // (q, c) of kidx kept incrementally (stride kNT <= C: at most one wrap)
+        int q = 0, c = tid;
+        for (int kidx = tid; kidx < nkeys; kidx += kNT) {
+          const float ku = kub[kidx];
+          if (ku >= theta0) list_key_qc(kidx, q, c, ku);
+          c += kNT;
+          if (c >= C) {
+            c -= C;
+            ++q;
+          }
+        }
+      } else if (P.kub_smem) {
         for (int kidx = tid; kidx < nkeys; kidx += kNT) {
           const float ku = kub[kidx];
           if (ku >= theta0) list_key(kidx, ku);
