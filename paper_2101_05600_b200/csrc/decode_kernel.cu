@@ -667,7 +667,6 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       const float hw = (float)(lam * (P.dpsi0 + W * P.dpsi1)) + 1e-4f;
       const float gf = P.guard_f;
       const int row_same = sh.row_same;
-      const bool vec2 = (V & 1) == 0;  // float2 loads need 8-byte aligned rows
       // m starts at the log-zero guard (not -inf): a log-zero grid entry then
       // never triggers a rescale and contributes exp(-1e30 - m) = 0, so the
       // per-element guard test disappears (an all-zero column keeps m == gf).
@@ -845,15 +844,18 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
         const float r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
         const float r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
         const float* col = grid + (size_t)(s - 1) * V + c0;
-        const int c1off = two ? 1 : 0;
+        // columns c0 and c0+1 are both inside the row (c0 + 1 <= C = V-1,
+        // the blank), so the pair is always loaded (the odd column of an odd
+        // C is simply not emitted): one float2 load when rows are 8-byte
+        // aligned (V even), else two scalar loads; no per-thread condition.
         auto ld = [&](const float* pp, float& a, float& b) {
-          if (vec2 && two) {
+          if ((V & 1) == 0) {
             const float2 v = __ldg(reinterpret_cast<const float2*>(pp));
             a = v.x;
             b = v.y;
           } else {
             a = __ldg(pp);
-            b = __ldg(pp + c1off);
+            b = __ldg(pp + 1);
           }
         };
         float xa[kCh], xb[kCh];
