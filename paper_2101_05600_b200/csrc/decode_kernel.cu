@@ -676,7 +676,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // (terms below 2^-126 of the column max flush to zero: at most
       // W * 2^-126 absolute, covered by the W * 1e-6 key half-width).
       constexpr int kP = BMAX / 2;
-      auto acc = [&](float2(&Sx)[kP], float& m, float x, const float* ph) {
+      // lazy rescale: the shift m only moves when a value exceeds it by more
+      // than 8 nats, so every accumulated term is <= e^8
+      auto rescale = [&](float2(&Sx)[kP], float& m, float x) {
         if (x > m + 8.f) {
           const float r = __expf(m - x);
           const float2 r2 = make_float2(r, r);
@@ -684,6 +686,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           for (int q = 0; q < kP; ++q) Sx[q] = __fmul2_rn(Sx[q], r2);
           m = x;
         }
+      };
+      auto acc_term = [&](float2(&Sx)[kP], float m, float x, const float* ph) {
         const float pe = ex2_ftz((x - m) * 1.44269504088896341f);
         const float2 p2 = make_float2(pe, pe);
         if constexpr (BMAX % 4 == 0) {  // 16-byte factor rows
@@ -698,6 +702,10 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           for (int q = 0; q < kP; ++q)
             Sx[q] = __ffma2_rn(reinterpret_cast<const float2*>(ph)[q], p2, Sx[q]);
         }
+      };
+      auto acc = [&](float2(&Sx)[kP], float& m, float x, const float* ph) {
+        rescale(Sx, m, x);
+        acc_term(Sx, m, x, ph);
       };
       long long tq_frames = 0, tq_keys = 0;
       constexpr int kCh = 2;  // frames per prefetch chunk (register budget)
@@ -811,10 +819,18 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
 #pragma unroll
                 for (int k2 = 0; k2 < kRu; ++k2)
                   v[k2] = *reinterpret_cast<const float2*>(sb + (i0 + k2) * kTmaBoxCols);
+                float xma = v[0].x, xmb = v[0].y;
+#pragma unroll
+                for (int k2 = 1; k2 < kRu; ++k2) {
+                  xma = fmaxf(xma, v[k2].x);
+                  xmb = fmaxf(xmb, v[k2].y);
+                }
+                rescale(S0, m0, xma);  // one test per column per group
+                rescale(S1, m1, xmb);
 #pragma unroll
                 for (int k2 = 0; k2 < kRu; ++k2) {
-                  acc(S0, m0, v[k2].x, phr + (f0 + i0 + k2) * phs);
-                  acc(S1, m1, v[k2].y, phr + (f0 + i0 + k2) * phs);
+                  acc_term(S0, m0, v[k2].x, phr + (f0 + i0 + k2) * phs);
+                  acc_term(S1, m1, v[k2].y, phr + (f0 + i0 + k2) * phs);
                 }
               }
             } else {
@@ -876,10 +892,19 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
 #pragma unroll
             for (int k = 0; k < kCh; ++k) ld(pp + (size_t)k * V, xa[k], xb[k]);
           }
+          // one rescale test per column per chunk, against the chunk max
+          float xma = ya[0], xmb = yb[0];
+#pragma unroll
+          for (int k = 1; k < kCh; ++k) {
+            xma = fmaxf(xma, ya[k]);
+            xmb = fmaxf(xmb, yb[k]);
+          }
+          rescale(S0, m0, xma);
+          rescale(S1, m1, xmb);
 #pragma unroll
           for (int k = 0; k < kCh; ++k) {
-            acc(S0, m0, ya[k], phr + (i0 + k) * phs);
-            acc(S1, m1, yb[k], phr + (i0 + k) * phs);
+            acc_term(S0, m0, ya[k], phr + (i0 + k) * phs);
+            acc_term(S1, m1, yb[k], phr + (i0 + k) * phs);
           }
         }
         for (int i = W4; i < W; ++i) {  // remainder frames
