@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
             const float* sb = stages + (size_t)st * (kTmaStageBytes / 4) + colb;
             const int nrow = min(kTmaRows, W - k * kTmaRows);
             const int f0 = k * kTmaRows;
-            constexpr int kRu = 4;  // rows per unrolled group
+            constexpr int kRu = 8;  // rows per unrolled group
             if (nrow == kTmaRows) {  // full chunk: rows unrolled so their loads and exps overlap
 #pragma unroll
               for (int i0 = 0; i0 < kTmaRows; i0 += kRu) {
