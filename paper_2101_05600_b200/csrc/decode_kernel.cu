@@ -714,7 +714,13 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // so each parent's constants are read once for both columns
       const float* phr = PhiF;
       constexpr int phs = BMAX;  // floats per PhiF row
-      const bool lam_pos = lam > 0.0;
+      // per-step key constants held in registers across the key loop (opaque
+      // to the compiler, which otherwise re-derives them from the kernel
+      // parameters for every key: LDC + DSETP + F2F per key)
+      float klamf = lamf, kgf = gf;
+      int klam_pos = lam > 0.0 ? 1 : 0;
+      asm volatile("" : "+f"(klamf), "+f"(kgf), "+r"(klam_pos));
+      const bool lam_pos = klam_pos != 0;
       auto emit_keys = [&](int c0, bool two, const float2(&S0)[kP], const float2(&S1)[kP],
                            float m0, float m1, float r0s, float r1s) {
 #pragma unroll
@@ -740,12 +746,12 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
                 // with log(Sq) <= log(2^-99) is kept
                 under = lam_pos && !(Sq >= 7.888609052210118e-31f);  // 2^-100
                 const float lg = under ? -68.62157f : lg2_ftz(Sq) * 0.693147180559945309f;
-                const float key = lam_pos ? kbq + lamf * (m + lg) + r : kbq + r;
+                const float key = lam_pos ? kbq + klamf * (m + lg) + r : kbq + r;
                 const float h = hw + fabsf(key) * 2.4e-7f;
                 klo = under ? -INFINITY : key - h;
                 kub_v = key + h;
                 // joint exactly kLogZero: att log-zero, or psi log-zero
-                const bool zero = r == -INFINITY || (lam_pos && (mz || m == gf));
+                const bool zero = r == -INFINITY || (lam_pos && (mz || m == kgf));
                 if (zero) {
                   klo = kub_v = kZeroKey;
                   under = false;
@@ -1408,7 +1414,13 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       sh.b_taut[nxt][tid] = it.taut;
       hist_u[(size_t)l * B + tid].tau = it.tau;
     }
-    if (gw0 > 0) __syncthreads();
+    // the patch is warp 0's (nchild <= BMAX <= 32) and only warp 0 reads
+    // tau before the next block barrier (P1), so a warp barrier suffices
+    // unless the state is saved now (step mode) or the search ends
+    if (gw0 > 0) {
+      if (stepm || sh.done) __syncthreads();
+      else __syncwarp();
+    }
     PROF_MARK(10);
     if (sh.done) break;
     if (stepm) {
