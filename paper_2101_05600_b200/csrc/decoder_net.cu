@@ -455,6 +455,271 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// Self-attention over the union of the beam's ancestor entries, on the
+// warp-level tensor path (B <= 16, S <= 4096). The hypotheses of one
+// utterance share most of their prefix (the union of their KV entries is
+// ~12% of nb*l on the bench model), so per (utterance, head) the CTA lists
+// the distinct (position, slot) entries once, each tagged with the mask of
+// hypotheses whose ancestry holds it, stages their K/V in shared memory and
+// scores all B queries against every entry with mma.sync; entries outside a
+// hypothesis' ancestry are masked to -inf before the online softmax. Each
+// entry is read from HBM once per (utterance, head) instead of once per
+// hypothesis, and the per-dim unpack + FMA moves onto the tensor pipe.
+// Entry word: position (bits 0-11) | slot (12-15) | hypothesis mask (16-31).
+// The step's own K/V (position l-1) are read from the QKV rows and written
+// to the cache for the later steps. Grid (U, heads), kSuW warps; stages of
+// kSuW * kSuKeys entries, each warp one chunk per stage.
+// Launch shape from scripts/sweep_self_attn.sh (2880 segments, 747 launches):
+// (keys, warps, min CTAs) 32,4,1: 231 ms; 16,4,6: 164; 16,2,12: 147;
+// 16,2,11: 143; 16,1,16: 169 — the kernel is latency-bound on the staged
+// HBM reads, so small CTAs at high residency win.
+#ifndef BL_SU_KEYS
+#define BL_SU_KEYS 16
+#endif
+#ifndef BL_SU_WARPS
+#define BL_SU_WARPS 2
+#endif
+#ifndef BL_SU_MINB
+#define BL_SU_MINB 11
+#endif
+constexpr int kSuKeys = BL_SU_KEYS;  // entries per warp chunk
+constexpr int kSuW = BL_SU_WARPS;    // warps per CTA
+__global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
+    dec_self_attn_union_kernel(int l, const __nv_bfloat16* __restrict__ qkv, int d, int B,
+                               const int* __restrict__ anc, int S, const int* __restrict__ nb_in,
+                               __nv_bfloat16* __restrict__ cache,
+                               __nv_bfloat16* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char su_sm[];
+  constexpr int kSt = kSuW * kSuKeys;  // entries per stage
+  const int u = blockIdx.x, h = blockIdx.y;
+  const int nb = l == 1 ? 1 : nb_in[u];
+  if (nb <= 0) return;  // finished utterance
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(su_sm);
+  __nv_bfloat16* Vs = Ks + (size_t)kSt * kXKPitch;
+  float* mrg = reinterpret_cast<float*>(su_sm);  // [warps][16*64 + 32] after the last stage
+  uint32_t* ent = reinterpret_cast<uint32_t*>(Vs + (size_t)kSt * kXKPitch);  // [B*S]
+  __shared__ int wsum[kSuW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t d2 = 2 * (size_t)d, d3 = 3 * (size_t)d;
+  const __nv_bfloat16* rows = qkv + (size_t)u * B * d3;
+  // this step's K and V into the cache (position l-1, own slot)
+  for (int i = tid; i < nb * 32; i += blockDim.x) {
+    const int k = i >> 5, w = i & 31;
+    const __nv_bfloat16* r = rows + k * d3 + h * kDk;
+    __nv_bfloat16* dst = cache + (((size_t)u * S + l - 1) * B + k) * d2 + h * kDk;
+    reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(r + d)[w];
+    reinterpret_cast<uint32_t*>(dst + d)[w] = reinterpret_cast<const uint32_t*>(r + 2 * d)[w];
+  }
+  // union of the live hypotheses' entries, positions in contiguous runs per
+  // thread so the block scan keeps position order (deterministic sums)
+  const int per = (l + kSuW * 32 - 1) / (kSuW * 32);
+  const int pb = min(l, tid * per), pe = min(l, pb + per);
+  auto slots_at = [&](int p, int(&sk)[16]) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      sk[k] = k < nb ? (p == l - 1 ? k : anc[((size_t)u * B + k) * S + p]) : -1;
+  };
+  int cnt = 0;
+  for (int p = pb; p < pe; ++p) {
+    int sk[16];
+    slots_at(p, sk);
+    unsigned msk = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) msk |= sk[k] >= 0 ? 1u << sk[k] : 0u;
+    cnt += __popc(msk);
+  }
+  int inc = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) wsum[warp] = inc;
+  __syncthreads();
+  int off = inc - cnt, n = 0;
+#pragma unroll
+  for (int w = 0; w < kSuW; ++w) {
+    off += w < warp ? wsum[w] : 0;
+    n += wsum[w];
+  }
+  for (int p = pb; p < pe; ++p) {
+    int sk[16];
+    slots_at(p, sk);
+    unsigned msk = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) msk |= sk[k] >= 0 ? 1u << sk[k] : 0u;
+    while (msk) {
+      const int s = __ffs(msk) - 1;
+      msk &= msk - 1;
+      unsigned hm = 0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) hm |= (sk[k] == s ? 1u : 0u) << k;
+      ent[off++] = (uint32_t)p | ((uint32_t)s << 12) | (hm << 16);
+    }
+  }
+  // query fragments: rows lane/4 (+8), dims kc*16 + 2*(lane%4) (+8)
+  uint32_t qa[4][4];
+  const int r0 = lane >> 2, r1 = r0 + 8;
+  {
+    const int c = 2 * (lane & 3);
+    const __nv_bfloat16* p0 = rows + r0 * d3 + h * kDk + c;
+    const __nv_bfloat16* p1 = rows + r1 * d3 + h * kDk + c;
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      qa[kc][0] = r0 < nb ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16) : 0u;
+      qa[kc][1] = r1 < nb ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16) : 0u;
+      qa[kc][2] = r0 < nb ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16 + 8) : 0u;
+      qa[kc][3] = r1 < nb ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16 + 8) : 0u;
+    }
+  }
+  const float sc = 1.4426950408889634f * rsqrtf((float)kDk);  // log2(e) / sqrt(dk)
+  float o[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const uint32_t ks_base = (uint32_t)__cvta_generic_to_shared(Ks);
+  const uint32_t vs_base = (uint32_t)__cvta_generic_to_shared(Vs);
+  const int lr = lane & 7, lm = (lane >> 3) & 1;
+  for (int e0 = 0; e0 < n; e0 += kSt) {
+    __syncthreads();  // entry list written / previous stage consumed
+    for (int i = tid; i < kSt * 8; i += blockDim.x) {  // 8 x 16 B per row
+      const int t = i >> 3, c = i & 7, e = e0 + t;
+      const __nv_bfloat16* src = rows + h * kDk;  // any valid address for the zero fill
+      unsigned nbytes = 0;
+      if (e < n) {
+        const uint32_t w = ent[e];
+        const int p = (int)(w & 0xfffu), s = (int)((w >> 12) & 0xfu);
+        src = p == l - 1 ? rows + s * d3 + d + h * kDk
+                         : cache + (((size_t)u * S + p) * B + s) * d2 + h * kDk;
+        nbytes = 16;
+      }
+      cp_async16(Ks + (size_t)t * kXKPitch + c * 8, src + c * 8, nbytes);
+      cp_async16(Vs + (size_t)t * kXKPitch + c * 8, src + d + c * 8, nbytes);
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    const int key0 = warp * kSuKeys;
+    if (e0 + key0 >= n) continue;
+    float s[kSuKeys / 8][4];
+#pragma unroll
+    for (int nt = 0; nt < kSuKeys / 8; ++nt) {
+      s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) {
+        uint32_t b0, b1;
+        ldsm_x2(ks_base + (uint32_t)(((key0 + nt * 8 + lr) * kXKPitch + kc * 16 + lm * 8) * 2),
+                b0, b1);
+        mma16816(s[nt], qa[kc], b0, b1);
+      }
+    }
+    float c0 = -INFINITY, c1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < kSuKeys / 8; ++nt) {
+      const int e = e0 + key0 + nt * 8 + 2 * (lane & 3);
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const unsigned hm = e + j < n ? ent[e + j] >> 16 : 0u;
+        s[nt][j] = (hm >> r0) & 1u ? s[nt][j] * sc : -INFINITY;
+        s[nt][2 + j] = (hm >> r1) & 1u ? s[nt][2 + j] * sc : -INFINITY;
+        c0 = fmaxf(c0, s[nt][j]);
+        c1 = fmaxf(c1, s[nt][2 + j]);
+      }
+    }
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 1));
+    c0 = fmaxf(c0, __shfl_xor_sync(0xffffffffu, c0, 2));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 1));
+    c1 = fmaxf(c1, __shfl_xor_sync(0xffffffffu, c1, 2));
+    const float n0 = fmaxf(m0, c0), n1 = fmaxf(m1, c1);
+    // a row with no entry so far keeps m = -inf: exponents against 0 give 0
+    const float z0 = n0 == -INFINITY ? 0.f : n0, z1 = n1 == -INFINITY ? 0.f : n1;
+    const float a0 = exp2f(m0 - z0), a1 = exp2f(m1 - z1);
+    m0 = n0;
+    m1 = n1;
+    l0 *= a0;
+    l1 *= a1;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i][0] *= a0; o[i][1] *= a0; o[i][2] *= a1; o[i][3] *= a1;
+    }
+    uint32_t pa[kSuKeys / 16][4];
+#pragma unroll
+    for (int nt = 0; nt < kSuKeys / 8; ++nt) {
+      const float p0 = exp2f(s[nt][0] - z0), p1 = exp2f(s[nt][1] - z0);
+      const float p2 = exp2f(s[nt][2] - z1), p3 = exp2f(s[nt][3] - z1);
+      l0 += p0 + p1;
+      l1 += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2] = pk_bf16(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pk_bf16(p2, p3);
+    }
+#pragma unroll
+    for (int kk = 0; kk < kSuKeys / 16; ++kk) {
+#pragma unroll
+      for (int dt = 0; dt < 8; ++dt) {
+        uint32_t b0, b1;
+        ldsm_x2_t(vs_base + (uint32_t)(((key0 + kk * 16 + lm * 8 + lr) * kXKPitch + dt * 8) * 2),
+                  b0, b1);
+        mma16816(o[dt], pa[kk], b0, b1);
+      }
+    }
+  }
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  __syncthreads();  // every warp is done with Ks/Vs
+  float* mw = mrg + warp * (16 * 64 + 32);
+  {
+    const int c = 2 * (lane & 3);
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+      mw[r0 * 64 + dt * 8 + c] = o[dt][0];
+      mw[r0 * 64 + dt * 8 + c + 1] = o[dt][1];
+      mw[r1 * 64 + dt * 8 + c] = o[dt][2];
+      mw[r1 * 64 + dt * 8 + c + 1] = o[dt][3];
+    }
+    if ((lane & 3) == 0) {
+      mw[1024 + r0] = m0;
+      mw[1024 + r1] = m1;
+      mw[1040 + r0] = l0;
+      mw[1040 + r1] = l1;
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < 16 * 32; i += blockDim.x) {  // (row, dim pair)
+    const int r = i >> 5, c = (i & 31) * 2;
+    if (r >= nb) continue;
+    float M = -INFINITY;
+    for (int w = 0; w < kSuW; ++w) M = fmaxf(M, mrg[w * (16 * 64 + 32) + 1024 + r]);
+    float L = 0.f, x0 = 0.f, x1 = 0.f;
+    for (int w = 0; w < kSuW; ++w) {
+      const float* pw = mrg + w * (16 * 64 + 32);
+      const float mwv = pw[1024 + r];
+      if (mwv == -INFINITY) continue;  // warp saw none of this row's entries
+      const float f = exp2f(mwv - M);
+      L += pw[1040 + r] * f;
+      x0 += pw[r * 64 + c] * f;
+      x1 += pw[r * 64 + c + 1] * f;
+    }
+    reinterpret_cast<__nv_bfloat162*>(out + ((size_t)u * B + r) * d + h * kDk)[c / 2] =
+        __floats2bfloat162_rn(x0 / L, x1 / L);
+  }
+}
+
+size_t su_smem(int B, int S) {
+  return std::max(2 * (size_t)kSuW * kSuKeys * kXKPitch * 2, (size_t)kSuW * (16 * 64 + 32) * 4) +
+         (size_t)B * S * 4;
+}
+
+// the union kernel unless BL_SELF_ATTN=warp (A/B runs) or the beam / step
+// count exceed its entry encoding or shared memory
+bool use_union_self_attn(int B, int S) {
+  static const bool warp = [] {
+    const char* v = std::getenv("BL_SELF_ATTN");
+    return v && std::strcmp(v, "warp") == 0;
+  }();
+  return !warp && B <= 16 && S <= 4096 && su_smem(B, S) <= 227 * 1024;
+}
+
 size_t xm_smem(int T) {
   const size_t Tp = (size_t)((T + 63) & ~63);
   return std::max(2 * Tp * kXKPitch * 2, (size_t)kXW * (16 * 64 + 32) * 4);
@@ -682,11 +947,19 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
                      n->kv2 + (size_t)l * U * T2 * 2 * d, 2 * s.d, st)) != cudaSuccess)
       return e;
   }
-  const size_t sa = (size_t)B * S * 8;
-  if (sa > 227 * 1024) return cudaErrorInvalidValue;
-  if ((e = cudaFuncSetAttribute(dec_self_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sa)) != cudaSuccess)
-    return e;
+  if (use_union_self_attn(B, S)) {
+    if ((e = cudaFuncSetAttribute(dec_self_attn_union_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)su_smem(B, S))) != cudaSuccess)
+      return e;
+  } else {
+    const size_t sa = (size_t)B * S * 8;
+    if (sa > 227 * 1024) return cudaErrorInvalidValue;
+    if ((e = cudaFuncSetAttribute(dec_self_attn_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sa)) !=
+        cudaSuccess)
+      return e;
+  }
   const size_t xm = xm_smem(T2);
   if (xm > 227 * 1024) return cudaErrorInvalidValue;
   return cudaFuncSetAttribute(dec_cross_attn_mma_kernel,
@@ -716,8 +989,12 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
     if ((e = n->gemm(M, 3 * d, d, n->Y, y.wqkv, kPlain, y.bqkv, nullptr, n->QKV, 3 * d, st)) !=
         cudaSuccess)
       return e;
-    dec_self_attn_kernel<<<dim3(U, s.heads), 32 * B, sa, st>>>(
-        l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, n->AO);
+    if (use_union_self_attn(B, S))
+      dec_self_attn_union_kernel<<<dim3(U, s.heads), kSuW * 32, su_smem(B, S), st>>>(
+          l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, n->AO);
+    else
+      dec_self_attn_kernel<<<dim3(U, s.heads), 32 * B, sa, st>>>(
+          l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, n->AO);
     if ((e = n->gemm(M, d, d, n->AO, y.wo, kResidual, y.bo, n->X, nullptr, d, st)) != cudaSuccess)
       return e;
     layer_norm_bf16(d, n->X, M, y.ln2g, y.ln2b, n->Y, st);
