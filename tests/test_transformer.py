@@ -76,8 +76,10 @@ def _decode(grid, mem, scorer, cfg, record=True, nbest=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("beam", [1, 4])
+@pytest.mark.parametrize("beam", [1, 4, 10, 16, 20])
 def test_transformer_rows_vs_torch(beam):
+    """beam <= 16: union-of-ancestors self-attention (mma.sync); beam 20:
+    the per-hypothesis warp kernel (csrc/decoder_net.cu use_union_self_attn)."""
     from torch_decoder import decoder_scores
     grid, mem, w = _setup(TINY_ENC, TINY_DEC, 3, 200, seed=5)
     sc = tr.TransformerScorer(TINY_DEC, w)
