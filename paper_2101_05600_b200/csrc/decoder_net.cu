@@ -469,6 +469,10 @@ __global__ void __launch_bounds__(256)
 // The step's own K/V (position l-1) are read from the QKV rows and written
 // to the cache for the later steps. Grid (U, heads), kSuW warps; stages of
 // kSuW * kSuKeys entries, each warp one chunk per stage.
+// kCross = true runs the same pipeline as source attention: the entries are
+// the utterance's T memory rows (every query row sees all of them), grid
+// (U, heads, ceil(B/16)); staging 32 rows at a time keeps 11 CTAs per SM
+// where dec_cross_attn_mma_kernel stages the whole memory (3 CTAs per SM).
 // Launch shape from scripts/sweep_self_attn.sh (2880 segments, 747 launches):
 // (keys, warps, min CTAs) 32,4,1: 231 ms; 16,4,6: 164; 16,2,12: 147;
 // 16,2,11: 143; 16,1,16: 169 — the kernel is latency-bound on the staged
@@ -484,29 +488,34 @@ __global__ void __launch_bounds__(256)
 #endif
 constexpr int kSuKeys = BL_SU_KEYS;  // entries per warp chunk
 constexpr int kSuW = BL_SU_WARPS;    // warps per CTA
+template <bool kCross>
 __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
-    dec_self_attn_union_kernel(int l, const __nv_bfloat16* __restrict__ qkv, int d, int B,
-                               const int* __restrict__ anc, int S, const int* __restrict__ nb_in,
-                               __nv_bfloat16* __restrict__ cache,
-                               __nv_bfloat16* __restrict__ out) {
+    dec_attn_staged_kernel(int l, const __nv_bfloat16* __restrict__ qsrc, int d, int B,
+                           const int* __restrict__ anc, int S, const int* __restrict__ nb_in,
+                           __nv_bfloat16* __restrict__ kv, int T,
+                           __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char su_sm[];
   constexpr int kSt = kSuW * kSuKeys;  // entries per stage
   const int u = blockIdx.x, h = blockIdx.y;
+  const int q0 = kCross ? (int)blockIdx.z * 16 : 0;
   const int nb = l == 1 ? 1 : nb_in[u];
-  if (nb <= 0) return;  // finished utterance
+  if (kCross ? (l > 1 && nb <= q0) : nb <= 0) return;  // finished utterance
+  const int nrow = kCross ? min(16, B - q0) : nb;        // query rows of this CTA
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(su_sm);
   __nv_bfloat16* Vs = Ks + (size_t)kSt * kXKPitch;
   float* mrg = reinterpret_cast<float*>(su_sm);  // [warps][16*64 + 32] after the last stage
   uint32_t* ent = reinterpret_cast<uint32_t*>(Vs + (size_t)kSt * kXKPitch);  // [B*S]
   __shared__ int wsum[kSuW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const size_t d2 = 2 * (size_t)d, d3 = 3 * (size_t)d;
-  const __nv_bfloat16* rows = qkv + (size_t)u * B * d3;
+  const size_t d2 = 2 * (size_t)d, d3 = 3 * (size_t)d, qs = kCross ? d : d3;
+  const __nv_bfloat16* rows = qsrc + ((size_t)u * B + q0) * qs;
+  int n = T;  // entries: the memory rows (cross), else the union below
+  if constexpr (!kCross) {
   // this step's K and V into the cache (position l-1, own slot)
   for (int i = tid; i < nb * 32; i += blockDim.x) {
     const int k = i >> 5, w = i & 31;
     const __nv_bfloat16* r = rows + k * d3 + h * kDk;
-    __nv_bfloat16* dst = cache + (((size_t)u * S + l - 1) * B + k) * d2 + h * kDk;
+    __nv_bfloat16* dst = kv + (((size_t)u * S + l - 1) * B + k) * d2 + h * kDk;
     reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(r + d)[w];
     reinterpret_cast<uint32_t*>(dst + d)[w] = reinterpret_cast<const uint32_t*>(r + 2 * d)[w];
   }
@@ -536,7 +545,8 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   }
   if (lane == 31) wsum[warp] = inc;
   __syncthreads();
-  int off = inc - cnt, n = 0;
+  int off = inc - cnt;
+  n = 0;
 #pragma unroll
   for (int w = 0; w < kSuW; ++w) {
     off += w < warp ? wsum[w] : 0;
@@ -557,19 +567,20 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
       ent[off++] = (uint32_t)p | ((uint32_t)s << 12) | (hm << 16);
     }
   }
+  }
   // query fragments: rows lane/4 (+8), dims kc*16 + 2*(lane%4) (+8)
   uint32_t qa[4][4];
   const int r0 = lane >> 2, r1 = r0 + 8;
   {
     const int c = 2 * (lane & 3);
-    const __nv_bfloat16* p0 = rows + r0 * d3 + h * kDk + c;
-    const __nv_bfloat16* p1 = rows + r1 * d3 + h * kDk + c;
+    const __nv_bfloat16* p0 = rows + r0 * qs + h * kDk + c;
+    const __nv_bfloat16* p1 = rows + r1 * qs + h * kDk + c;
 #pragma unroll
     for (int kc = 0; kc < 4; ++kc) {
-      qa[kc][0] = r0 < nb ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16) : 0u;
-      qa[kc][1] = r1 < nb ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16) : 0u;
-      qa[kc][2] = r0 < nb ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16 + 8) : 0u;
-      qa[kc][3] = r1 < nb ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16 + 8) : 0u;
+      qa[kc][0] = r0 < nrow ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16) : 0u;
+      qa[kc][1] = r1 < nrow ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16) : 0u;
+      qa[kc][2] = r0 < nrow ? *reinterpret_cast<const uint32_t*>(p0 + kc * 16 + 8) : 0u;
+      qa[kc][3] = r1 < nrow ? *reinterpret_cast<const uint32_t*>(p1 + kc * 16 + 8) : 0u;
     }
   }
   const float sc = 1.4426950408889634f * rsqrtf((float)kDk);  // log2(e) / sqrt(dk)
@@ -586,11 +597,14 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
       const int t = i >> 3, c = i & 7, e = e0 + t;
       const __nv_bfloat16* src = rows + h * kDk;  // any valid address for the zero fill
       unsigned nbytes = 0;
-      if (e < n) {
+      if (kCross && e < n) {
+        src = kv + ((size_t)u * T + e) * d2 + h * kDk;
+        nbytes = 16;
+      } else if (e < n) {
         const uint32_t w = ent[e];
         const int p = (int)(w & 0xfffu), s = (int)((w >> 12) & 0xfu);
         src = p == l - 1 ? rows + s * d3 + d + h * kDk
-                         : cache + (((size_t)u * S + p) * B + s) * d2 + h * kDk;
+                         : kv + (((size_t)u * S + p) * B + s) * d2 + h * kDk;
         nbytes = 16;
       }
       cp_async16(Ks + (size_t)t * kXKPitch + c * 8, src + c * 8, nbytes);
@@ -618,7 +632,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
       const int e = e0 + key0 + nt * 8 + 2 * (lane & 3);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
-        const unsigned hm = e + j < n ? ent[e + j] >> 16 : 0u;
+        const unsigned hm = e + j < n ? (kCross ? 0xffffu : ent[e + j] >> 16) : 0u;
         s[nt][j] = (hm >> r0) & 1u ? s[nt][j] * sc : -INFINITY;
         s[nt][2 + j] = (hm >> r1) & 1u ? s[nt][2 + j] * sc : -INFINITY;
         c0 = fmaxf(c0, s[nt][j]);
@@ -687,7 +701,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   __syncthreads();
   for (int i = tid; i < 16 * 32; i += blockDim.x) {  // (row, dim pair)
     const int r = i >> 5, c = (i & 31) * 2;
-    if (r >= nb) continue;
+    if (r >= nrow) continue;
     float M = -INFINITY;
     for (int w = 0; w < kSuW; ++w) M = fmaxf(M, mrg[w * (16 * 64 + 32) + 1024 + r]);
     float L = 0.f, x0 = 0.f, x1 = 0.f;
@@ -700,14 +714,23 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
       x0 += pw[r * 64 + c] * f;
       x1 += pw[r * 64 + c + 1] * f;
     }
-    reinterpret_cast<__nv_bfloat162*>(out + ((size_t)u * B + r) * d + h * kDk)[c / 2] =
+    reinterpret_cast<__nv_bfloat162*>(out + ((size_t)u * B + q0 + r) * d + h * kDk)[c / 2] =
         __floats2bfloat162_rn(x0 / L, x1 / L);
   }
 }
 
-size_t su_smem(int B, int S) {
-  return std::max(2 * (size_t)kSuW * kSuKeys * kXKPitch * 2, (size_t)kSuW * (16 * 64 + 32) * 4) +
-         (size_t)B * S * 4;
+size_t xs_smem() {
+  return std::max(2 * (size_t)kSuW * kSuKeys * kXKPitch * 2, (size_t)kSuW * (16 * 64 + 32) * 4);
+}
+size_t su_smem(int B, int S) { return xs_smem() + (size_t)B * S * 4; }
+
+// staged source attention unless BL_CROSS_ATTN=whole (A/B runs)
+bool use_staged_cross_attn() {
+  static const bool whole = [] {
+    const char* v = std::getenv("BL_CROSS_ATTN");
+    return v && std::strcmp(v, "whole") == 0;
+  }();
+  return !whole;
 }
 
 // the union kernel unless BL_SELF_ATTN=warp (A/B runs) or the beam / step
@@ -948,7 +971,7 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
       return e;
   }
   if (use_union_self_attn(B, S)) {
-    if ((e = cudaFuncSetAttribute(dec_self_attn_union_kernel,
+    if ((e = cudaFuncSetAttribute(dec_attn_staged_kernel<false>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)su_smem(B, S))) != cudaSuccess)
       return e;
@@ -960,6 +983,9 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
         cudaSuccess)
       return e;
   }
+  if (use_staged_cross_attn())
+    return cudaFuncSetAttribute(dec_attn_staged_kernel<true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_smem());
   const size_t xm = xm_smem(T2);
   if (xm > 227 * 1024) return cudaErrorInvalidValue;
   return cudaFuncSetAttribute(dec_cross_attn_mma_kernel,
@@ -990,8 +1016,8 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
         cudaSuccess)
       return e;
     if (use_union_self_attn(B, S))
-      dec_self_attn_union_kernel<<<dim3(U, s.heads), kSuW * 32, su_smem(B, S), st>>>(
-          l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, n->AO);
+      dec_attn_staged_kernel<false><<<dim3(U, s.heads), kSuW * 32, su_smem(B, S), st>>>(
+          l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, 0, n->AO);
     else
       dec_self_attn_kernel<<<dim3(U, s.heads), 32 * B, sa, st>>>(
           l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, n->AO);
@@ -1000,8 +1026,12 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
     layer_norm_bf16(d, n->X, M, y.ln2g, y.ln2b, n->Y, st);
     if ((e = n->gemm(M, d, d, n->Y, y.wq2, kPlain, y.bq2, nullptr, n->QKV, d, st)) != cudaSuccess)
       return e;
-    dec_cross_attn_mma_kernel<<<dim3(U, s.heads, (B + 15) / 16), kXW * 32, xm, st>>>(
-        l, nb_live, n->QKV, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, d, B, n->AO);
+    if (use_staged_cross_attn())
+      dec_attn_staged_kernel<true><<<dim3(U, s.heads, (B + 15) / 16), kSuW * 32, xs_smem(), st>>>(
+          l, n->QKV, d, B, nullptr, 0, nb_live, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, n->AO);
+    else
+      dec_cross_attn_mma_kernel<<<dim3(U, s.heads, (B + 15) / 16), kXW * 32, xm, st>>>(
+          l, nb_live, n->QKV, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, d, B, n->AO);
     if ((e = n->gemm(M, d, d, n->AO, y.wo2, kResidual, y.bo2, n->X, nullptr, d, st)) !=
         cudaSuccess)
       return e;
