@@ -476,7 +476,11 @@ __global__ void __launch_bounds__(256)
 // Launch shape from scripts/sweep_self_attn.sh (2880 segments, 747 launches):
 // (keys, warps, min CTAs) 32,4,1: 231 ms; 16,4,6: 164; 16,2,12: 147;
 // 16,2,11: 143; 16,1,16: 169 — the kernel is latency-bound on the staged
-// HBM reads, so small CTAs at high residency win.
+// HBM reads, so small CTAs at high residency win. With source attention on
+// the same kernel (self + cross, 1494 launches): 16,2,11 single-buffered
+// 253 ms; double-buffered (BL_SU_STAGES=2) 16,2,8 264, 16,2,10 262,
+// 16,4,6 309, 32,2,8 327 — the second buffer costs more residency than
+// the overlap it buys.
 #ifndef BL_SU_KEYS
 #define BL_SU_KEYS 16
 #endif
@@ -487,7 +491,11 @@ __global__ void __launch_bounds__(256)
 #define BL_SU_MINB 11
 #endif
 constexpr int kSuKeys = BL_SU_KEYS;  // entries per warp chunk
+#ifndef BL_SU_STAGES
+#define BL_SU_STAGES 1
+#endif
 constexpr int kSuW = BL_SU_WARPS;    // warps per CTA
+constexpr int kSuStages = BL_SU_STAGES;  // staging buffers (2: next stage in flight)
 template <bool kCross>
 __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
     dec_attn_staged_kernel(int l, const __nv_bfloat16* __restrict__ qsrc, int d, int B,
@@ -502,9 +510,9 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   if (kCross ? (l > 1 && nb <= q0) : nb <= 0) return;  // finished utterance
   const int nrow = kCross ? min(16, B - q0) : nb;        // query rows of this CTA
   __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(su_sm);
-  __nv_bfloat16* Vs = Ks + (size_t)kSt * kXKPitch;
+  __nv_bfloat16* Vs = Ks + (size_t)kSuStages * kSt * kXKPitch;
   float* mrg = reinterpret_cast<float*>(su_sm);  // [warps][16*64 + 32] after the last stage
-  uint32_t* ent = reinterpret_cast<uint32_t*>(Vs + (size_t)kSt * kXKPitch);  // [B*S]
+  uint32_t* ent = reinterpret_cast<uint32_t*>(Vs + (size_t)kSuStages * kSt * kXKPitch);  // [B*S]
   __shared__ int wsum[kSuW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t d2 = 2 * (size_t)d, d3 = 3 * (size_t)d, qs = kCross ? d : d3;
@@ -591,8 +599,9 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   const uint32_t ks_base = (uint32_t)__cvta_generic_to_shared(Ks);
   const uint32_t vs_base = (uint32_t)__cvta_generic_to_shared(Vs);
   const int lr = lane & 7, lm = (lane >> 3) & 1;
-  for (int e0 = 0; e0 < n; e0 += kSt) {
-    __syncthreads();  // entry list written / previous stage consumed
+  auto issue = [&](int e0, int buf) {
+    __nv_bfloat16* Kb = Ks + (size_t)buf * kSt * kXKPitch;
+    __nv_bfloat16* Vb = Vs + (size_t)buf * kSt * kXKPitch;
     for (int i = tid; i < kSt * 8; i += blockDim.x) {  // 8 x 16 B per row
       const int t = i >> 3, c = i & 7, e = e0 + t;
       const __nv_bfloat16* src = rows + h * kDk;  // any valid address for the zero fill
@@ -607,13 +616,28 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
                          : kv + (((size_t)u * S + p) * B + s) * d2 + h * kDk;
         nbytes = 16;
       }
-      cp_async16(Ks + (size_t)t * kXKPitch + c * 8, src + c * 8, nbytes);
-      cp_async16(Vs + (size_t)t * kXKPitch + c * 8, src + d + c * 8, nbytes);
+      cp_async16(Kb + (size_t)t * kXKPitch + c * 8, src + c * 8, nbytes);
+      cp_async16(Vb + (size_t)t * kXKPitch + c * 8, src + d + c * 8, nbytes);
     }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  __syncthreads();  // entry list written
+  if (kSuStages == 2 && n > 0) issue(0, 0);
+  int stg = 0;
+  for (int e0 = 0; e0 < n; e0 += kSt, ++stg) {
+    const int buf = kSuStages == 2 ? (stg & 1) : 0;
+    if (kSuStages == 2 && e0 + kSt < n) {
+      issue(e0 + kSt, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      if (kSuStages == 1) issue(e0, 0);
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();  // stage visible to every warp
     const int key0 = warp * kSuKeys;
-    if (e0 + key0 >= n) continue;
+    const uint32_t kb = ks_base + (uint32_t)(buf * kSt * kXKPitch * 2);
+    const uint32_t vb = vs_base + (uint32_t)(buf * kSt * kXKPitch * 2);
+    if (e0 + key0 < n) {
     float s[kSuKeys / 8][4];
 #pragma unroll
     for (int nt = 0; nt < kSuKeys / 8; ++nt) {
@@ -621,7 +645,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
         uint32_t b0, b1;
-        ldsm_x2(ks_base + (uint32_t)(((key0 + nt * 8 + lr) * kXKPitch + kc * 16 + lm * 8) * 2),
+        ldsm_x2(kb + (uint32_t)(((key0 + nt * 8 + lr) * kXKPitch + kc * 16 + lm * 8) * 2),
                 b0, b1);
         mma16816(s[nt], qa[kc], b0, b1);
       }
@@ -670,11 +694,13 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
 #pragma unroll
       for (int dt = 0; dt < 8; ++dt) {
         uint32_t b0, b1;
-        ldsm_x2_t(vs_base + (uint32_t)(((key0 + kk * 16 + lm * 8 + lr) * kXKPitch + dt * 8) * 2),
+        ldsm_x2_t(vb + (uint32_t)(((key0 + kk * 16 + lm * 8 + lr) * kXKPitch + dt * 8) * 2),
                   b0, b1);
         mma16816(o[dt], pa[kk], b0, b1);
       }
     }
+    }
+    __syncthreads();  // stage consumed before its buffer is refilled
   }
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
@@ -720,7 +746,8 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
 }
 
 size_t xs_smem() {
-  return std::max(2 * (size_t)kSuW * kSuKeys * kXKPitch * 2, (size_t)kSuW * (16 * 64 + 32) * 4);
+  return std::max(2 * (size_t)kSuStages * kSuW * kSuKeys * kXKPitch * 2,
+                  (size_t)kSuW * (16 * 64 + 32) * 4);
 }
 size_t su_smem(int B, int S) { return xs_smem() + (size_t)B * S * 4; }
 
