@@ -496,14 +496,14 @@ constexpr int kSuKeys = BL_SU_KEYS;  // entries per warp chunk
 #endif
 constexpr int kSuW = BL_SU_WARPS;    // warps per CTA
 constexpr int kSuStages = BL_SU_STAGES;  // staging buffers (2: next stage in flight)
-template <bool kCross>
-__global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
+template <bool kCross, int kKeys, int kW, int kMinB>
+__global__ void __launch_bounds__(kW * 32, kMinB)
     dec_attn_staged_kernel(int l, const __nv_bfloat16* __restrict__ qsrc, int d, int B,
                            const int* __restrict__ anc, int S, const int* __restrict__ nb_in,
                            __nv_bfloat16* __restrict__ kv, int T,
                            __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char su_sm[];
-  constexpr int kSt = kSuW * kSuKeys;  // entries per stage
+  constexpr int kSt = kW * kKeys;  // entries per stage
   const int u = blockIdx.x, h = blockIdx.y;
   const int q0 = kCross ? (int)blockIdx.z * 16 : 0;
   const int nb = l == 1 ? 1 : nb_in[u];
@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   __nv_bfloat16* Vs = Ks + (size_t)kSuStages * kSt * kXKPitch;
   float* mrg = reinterpret_cast<float*>(su_sm);  // [warps][16*64 + 32] after the last stage
   uint32_t* ent = reinterpret_cast<uint32_t*>(Vs + (size_t)kSuStages * kSt * kXKPitch);  // [B*S]
-  __shared__ int wsum[kSuW];
+  __shared__ int wsum[kW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const size_t d2 = 2 * (size_t)d, d3 = 3 * (size_t)d, qs = kCross ? d : d3;
   const __nv_bfloat16* rows = qsrc + ((size_t)u * B + q0) * qs;
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   }
   // union of the live hypotheses' entries, positions in contiguous runs per
   // thread so the block scan keeps position order (deterministic sums)
-  const int per = (l + kSuW * 32 - 1) / (kSuW * 32);
+  const int per = (l + kW * 32 - 1) / (kW * 32);
   const int pb = min(l, tid * per), pe = min(l, pb + per);
   auto slots_at = [&](int p, int(&sk)[16]) {
 #pragma unroll
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   int off = inc - cnt;
   n = 0;
 #pragma unroll
-  for (int w = 0; w < kSuW; ++w) {
+  for (int w = 0; w < kW; ++w) {
     off += w < warp ? wsum[w] : 0;
     n += wsum[w];
   }
@@ -634,13 +634,13 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();  // stage visible to every warp
-    const int key0 = warp * kSuKeys;
+    const int key0 = warp * kKeys;
     const uint32_t kb = ks_base + (uint32_t)(buf * kSt * kXKPitch * 2);
     const uint32_t vb = vs_base + (uint32_t)(buf * kSt * kXKPitch * 2);
     if (e0 + key0 < n) {
-    float s[kSuKeys / 8][4];
+    float s[kKeys / 8][4];
 #pragma unroll
-    for (int nt = 0; nt < kSuKeys / 8; ++nt) {
+    for (int nt = 0; nt < kKeys / 8; ++nt) {
       s[nt][0] = s[nt][1] = s[nt][2] = s[nt][3] = 0.f;
 #pragma unroll
       for (int kc = 0; kc < 4; ++kc) {
@@ -652,7 +652,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
     }
     float c0 = -INFINITY, c1 = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < kSuKeys / 8; ++nt) {
+    for (int nt = 0; nt < kKeys / 8; ++nt) {
       const int e = e0 + key0 + nt * 8 + 2 * (lane & 3);
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -679,9 +679,9 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
     for (int i = 0; i < 8; ++i) {
       o[i][0] *= a0; o[i][1] *= a0; o[i][2] *= a1; o[i][3] *= a1;
     }
-    uint32_t pa[kSuKeys / 16][4];
+    uint32_t pa[kKeys / 16][4];
 #pragma unroll
-    for (int nt = 0; nt < kSuKeys / 8; ++nt) {
+    for (int nt = 0; nt < kKeys / 8; ++nt) {
       const float p0 = exp2f(s[nt][0] - z0), p1 = exp2f(s[nt][1] - z0);
       const float p2 = exp2f(s[nt][2] - z1), p3 = exp2f(s[nt][3] - z1);
       l0 += p0 + p1;
@@ -690,7 +690,7 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
       pa[nt >> 1][(nt & 1) * 2 + 1] = pk_bf16(p2, p3);
     }
 #pragma unroll
-    for (int kk = 0; kk < kSuKeys / 16; ++kk) {
+    for (int kk = 0; kk < kKeys / 16; ++kk) {
 #pragma unroll
       for (int dt = 0; dt < 8; ++dt) {
         uint32_t b0, b1;
@@ -729,9 +729,9 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
     const int r = i >> 5, c = (i & 31) * 2;
     if (r >= nrow) continue;
     float M = -INFINITY;
-    for (int w = 0; w < kSuW; ++w) M = fmaxf(M, mrg[w * (16 * 64 + 32) + 1024 + r]);
+    for (int w = 0; w < kW; ++w) M = fmaxf(M, mrg[w * (16 * 64 + 32) + 1024 + r]);
     float L = 0.f, x0 = 0.f, x1 = 0.f;
-    for (int w = 0; w < kSuW; ++w) {
+    for (int w = 0; w < kW; ++w) {
       const float* pw = mrg + w * (16 * 64 + 32);
       const float mwv = pw[1024 + r];
       if (mwv == -INFINITY) continue;  // warp saw none of this row's entries
@@ -745,11 +745,27 @@ __global__ void __launch_bounds__(kSuW * 32, BL_SU_MINB)
   }
 }
 
-size_t xs_smem() {
-  return std::max(2 * (size_t)kSuStages * kSuW * kSuKeys * kXKPitch * 2,
-                  (size_t)kSuW * (16 * 64 + 32) * 4);
+// source attention's own launch shape (scripts/sweep_src_attn.sh, staged
+// self + source totals over 1494 launches; (keys, warps, min CTAs)):
+// 16,2,11 253 ms; 32,2,8 247; 32,1,16 247; 32,1,20 244; 64,2,6 244;
+// 32,4,4 264; 64,4,3 280
+#ifndef BL_XS_KEYS
+#define BL_XS_KEYS 64
+#endif
+#ifndef BL_XS_WARPS
+#define BL_XS_WARPS 2
+#endif
+#ifndef BL_XS_MINB
+#define BL_XS_MINB 6
+#endif
+#define SELF_ATTN dec_attn_staged_kernel<false, kSuKeys, kSuW, BL_SU_MINB>
+#define SRC_ATTN dec_attn_staged_kernel<true, BL_XS_KEYS, BL_XS_WARPS, BL_XS_MINB>
+size_t stage_smem(int keys, int warps) {
+  return std::max(2 * (size_t)kSuStages * warps * keys * kXKPitch * 2,
+                  (size_t)warps * (16 * 64 + 32) * 4);
 }
-size_t su_smem(int B, int S) { return xs_smem() + (size_t)B * S * 4; }
+size_t xs_smem() { return stage_smem(BL_XS_KEYS, BL_XS_WARPS); }
+size_t su_smem(int B, int S) { return stage_smem(kSuKeys, kSuW) + (size_t)B * S * 4; }
 
 // staged source attention unless BL_CROSS_ATTN=whole (A/B runs)
 bool use_staged_cross_attn() {
@@ -998,7 +1014,7 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
       return e;
   }
   if (use_union_self_attn(B, S)) {
-    if ((e = cudaFuncSetAttribute(dec_attn_staged_kernel<false>,
+    if ((e = cudaFuncSetAttribute(SELF_ATTN,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)su_smem(B, S))) != cudaSuccess)
       return e;
@@ -1011,7 +1027,7 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
       return e;
   }
   if (use_staged_cross_attn())
-    return cudaFuncSetAttribute(dec_attn_staged_kernel<true>,
+    return cudaFuncSetAttribute(SRC_ATTN,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs_smem());
   const size_t xm = xm_smem(T2);
   if (xm > 227 * 1024) return cudaErrorInvalidValue;
@@ -1043,7 +1059,7 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
         cudaSuccess)
       return e;
     if (use_union_self_attn(B, S))
-      dec_attn_staged_kernel<false><<<dim3(U, s.heads), kSuW * 32, su_smem(B, S), st>>>(
+      SELF_ATTN<<<dim3(U, s.heads), kSuW * 32, su_smem(B, S), st>>>(
           l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, 0, n->AO);
     else
       dec_self_attn_kernel<<<dim3(U, s.heads), 32 * B, sa, st>>>(
@@ -1054,7 +1070,7 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
     if ((e = n->gemm(M, d, d, n->Y, y.wq2, kPlain, y.bq2, nullptr, n->QKV, d, st)) != cudaSuccess)
       return e;
     if (use_staged_cross_attn())
-      dec_attn_staged_kernel<true><<<dim3(U, s.heads, (B + 15) / 16), kSuW * 32, xs_smem(), st>>>(
+      SRC_ATTN<<<dim3(U, s.heads, (B + 15) / 16), BL_XS_WARPS * 32, xs_smem(), st>>>(
           l, n->QKV, d, B, nullptr, 0, nb_live, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, n->AO);
     else
       dec_cross_attn_mma_kernel<<<dim3(U, s.heads, (B + 15) / 16), kXW * 32, xm, st>>>(
