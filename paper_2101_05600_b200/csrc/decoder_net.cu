@@ -765,6 +765,44 @@ size_t stage_smem(int keys, int warps) {
                   (size_t)warps * (16 * 64 + 32) * 4);
 }
 size_t xs_smem() { return stage_smem(BL_XS_KEYS, BL_XS_WARPS); }
+// The same rows one warp per row (8 rows per CTA, shuffle reductions only,
+// no block barriers); the row is re-read from L1 for each pass.
+__global__ void __launch_bounds__(256)
+    dec_log_softmax64_warp_kernel(const float* __restrict__ logits, int V, int M, double lam,
+                                  double* __restrict__ att, float* __restrict__ attf) {
+  const int lane = threadIdx.x & 31;
+  const int R = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (R >= M) return;
+  const float* x = logits + (size_t)R * V;
+  float mf = -INFINITY;
+  for (int i = lane; i < V; i += 32) mf = fmaxf(mf, x[i]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) mf = fmaxf(mf, __shfl_xor_sync(0xffffffffu, mf, o));
+  const double m = mf;
+  double sum = 0.0;
+  for (int i = lane; i < V; i += 32) sum += exp((double)x[i] - m);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  const double lse = m + log(sum);
+  double* a = att + (size_t)R * V;
+  float* af = attf + (size_t)R * V;
+  const double w1 = lam <= 0.0 ? 1.0 : 1.0 - lam;
+  for (int i = lane; i < V; i += 32) {
+    const double v = (double)x[i] - lse;
+    a[i] = v;
+    af[i] = lam >= 1.0 ? 0.f : (float)(w1 * v);
+  }
+}
+
+// the warp-per-row normaliser unless BL_LOG_SOFTMAX=block (A/B runs)
+bool use_warp_log_softmax() {
+  static const bool block = [] {
+    const char* v = std::getenv("BL_LOG_SOFTMAX");
+    return v && std::strcmp(v, "block") == 0;
+  }();
+  return !block;
+}
+
 size_t su_smem(int B, int S) { return stage_smem(kSuKeys, kSuW) + (size_t)B * S * 4; }
 
 // staged source attention unless BL_CROSS_ATTN=whole (A/B runs)
@@ -1090,7 +1128,11 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
   if ((e = n->gemm(M, s.vocab, d, n->Y, n->wout, kPlain, n->bout, n->logits, nullptr, s.vocab,
                    st)) != cudaSuccess)
     return e;
-  dec_log_softmax64_kernel<<<M, 256, 0, st>>>(n->logits, s.vocab, lambda, n->att, n->attf);
+  if (use_warp_log_softmax())
+    dec_log_softmax64_warp_kernel<<<(M + 7) / 8, 256, 0, st>>>(n->logits, s.vocab, M, lambda,
+                                                               n->att, n->attf);
+  else
+    dec_log_softmax64_kernel<<<M, 256, 0, st>>>(n->logits, s.vocab, lambda, n->att, n->attf);
   return cudaGetLastError();
 }
 
