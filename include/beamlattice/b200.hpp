@@ -443,27 +443,234 @@ inline uint32_t get_u32(std::istream& is) {
   return static_cast<uint32_t>(b[0]) | (static_cast<uint32_t>(b[1]) << 8) |
          (static_cast<uint32_t>(b[2]) << 16) | (static_cast<uint32_t>(b[3]) << 24);
 }
-// shortest round-trip double, JSON style (integral values keep ".0")
-inline std::string json_double(double v) {
-  char buf[64];
-  const auto r = std::to_chars(buf, buf + sizeof(buf), v);
-  std::string s(buf, r.ptr);
-  if (s.find_first_of(".eEn") == std::string::npos) s += ".0";
-  return s;
+// nlohmann::json's number format (the reference writer, io.cpp:81-92).
+// Digits by Grisu2 (Loitsch 2010, "Printing Floating-Point Numbers Quickly and
+// Accurately with Integers") with the boundary, cached-power and rounding
+// choices nlohmann 3.11 makes, so the digits match its output byte for byte
+// (tests/test_json_format.py checks against the compiled reference); then
+// fixed notation while the decimal point falls in (-4, 15], else d.ddde+XX
+// with at least two exponent digits. Non-finite values dump as null.
+namespace grisu {
+struct Fp {
+  uint64_t f;
+  int e;
+};
+inline Fp mul(Fp x, Fp y) {
+  const uint64_t ul = x.f & 0xFFFFFFFFu, uh = x.f >> 32, vl = y.f & 0xFFFFFFFFu, vh = y.f >> 32;
+  const uint64_t p0 = ul * vl, p1 = ul * vh, p2 = uh * vl, p3 = uh * vh;
+  uint64_t q = (p0 >> 32) + (p1 & 0xFFFFFFFFu) + (p2 & 0xFFFFFFFFu) + (uint64_t{1} << 31);
+  return {p3 + (p2 >> 32) + (p1 >> 32) + (q >> 32), x.e + y.e + 64};
 }
+inline Fp normalize(Fp x) {
+  while ((x.f >> 63) == 0) {
+    x.f <<= 1;
+    --x.e;
+  }
+  return x;
+}
+struct Cached {
+  uint64_t f;
+  int e, k;
+};
+// 10^k, k = -300, -292, ..., 324, as round-to-nearest 64-bit significands
+inline const Cached& cached_power(int idx) {
+  static const Cached t[79] = {
+      {0xAB70FE17C79AC6CAULL, -1060, -300},
+      {0xFF77B1FCBEBCDC4FULL, -1034, -292},
+      {0xBE5691EF416BD60CULL, -1007, -284},
+      {0x8DD01FAD907FFC3CULL, -980, -276},
+      {0xD3515C2831559A83ULL, -954, -268},
+      {0x9D71AC8FADA6C9B5ULL, -927, -260},
+      {0xEA9C227723EE8BCBULL, -901, -252},
+      {0xAECC49914078536DULL, -874, -244},
+      {0x823C12795DB6CE57ULL, -847, -236},
+      {0xC21094364DFB5637ULL, -821, -228},
+      {0x9096EA6F3848984FULL, -794, -220},
+      {0xD77485CB25823AC7ULL, -768, -212},
+      {0xA086CFCD97BF97F4ULL, -741, -204},
+      {0xEF340A98172AACE5ULL, -715, -196},
+      {0xB23867FB2A35B28EULL, -688, -188},
+      {0x84C8D4DFD2C63F3BULL, -661, -180},
+      {0xC5DD44271AD3CDBAULL, -635, -172},
+      {0x936B9FCEBB25C996ULL, -608, -164},
+      {0xDBAC6C247D62A584ULL, -582, -156},
+      {0xA3AB66580D5FDAF6ULL, -555, -148},
+      {0xF3E2F893DEC3F126ULL, -529, -140},
+      {0xB5B5ADA8AAFF80B8ULL, -502, -132},
+      {0x87625F056C7C4A8BULL, -475, -124},
+      {0xC9BCFF6034C13053ULL, -449, -116},
+      {0x964E858C91BA2655ULL, -422, -108},
+      {0xDFF9772470297EBDULL, -396, -100},
+      {0xA6DFBD9FB8E5B88FULL, -369, -92},
+      {0xF8A95FCF88747D94ULL, -343, -84},
+      {0xB94470938FA89BCFULL, -316, -76},
+      {0x8A08F0F8BF0F156BULL, -289, -68},
+      {0xCDB02555653131B6ULL, -263, -60},
+      {0x993FE2C6D07B7FACULL, -236, -52},
+      {0xE45C10C42A2B3B06ULL, -210, -44},
+      {0xAA242499697392D3ULL, -183, -36},
+      {0xFD87B5F28300CA0EULL, -157, -28},
+      {0xBCE5086492111AEBULL, -130, -20},
+      {0x8CBCCC096F5088CCULL, -103, -12},
+      {0xD1B71758E219652CULL, -77, -4},
+      {0x9C40000000000000ULL, -50, 4},
+      {0xE8D4A51000000000ULL, -24, 12},
+      {0xAD78EBC5AC620000ULL, 3, 20},
+      {0x813F3978F8940984ULL, 30, 28},
+      {0xC097CE7BC90715B3ULL, 56, 36},
+      {0x8F7E32CE7BEA5C70ULL, 83, 44},
+      {0xD5D238A4ABE98068ULL, 109, 52},
+      {0x9F4F2726179A2245ULL, 136, 60},
+      {0xED63A231D4C4FB27ULL, 162, 68},
+      {0xB0DE65388CC8ADA8ULL, 189, 76},
+      {0x83C7088E1AAB65DBULL, 216, 84},
+      {0xC45D1DF942711D9AULL, 242, 92},
+      {0x924D692CA61BE758ULL, 269, 100},
+      {0xDA01EE641A708DEAULL, 295, 108},
+      {0xA26DA3999AEF774AULL, 322, 116},
+      {0xF209787BB47D6B85ULL, 348, 124},
+      {0xB454E4A179DD1877ULL, 375, 132},
+      {0x865B86925B9BC5C2ULL, 402, 140},
+      {0xC83553C5C8965D3DULL, 428, 148},
+      {0x952AB45CFA97A0B3ULL, 455, 156},
+      {0xDE469FBD99A05FE3ULL, 481, 164},
+      {0xA59BC234DB398C25ULL, 508, 172},
+      {0xF6C69A72A3989F5CULL, 534, 180},
+      {0xB7DCBF5354E9BECEULL, 561, 188},
+      {0x88FCF317F22241E2ULL, 588, 196},
+      {0xCC20CE9BD35C78A5ULL, 614, 204},
+      {0x98165AF37B2153DFULL, 641, 212},
+      {0xE2A0B5DC971F303AULL, 667, 220},
+      {0xA8D9D1535CE3B396ULL, 694, 228},
+      {0xFB9B7CD9A4A7443CULL, 720, 236},
+      {0xBB764C4CA7A44410ULL, 747, 244},
+      {0x8BAB8EEFB6409C1AULL, 774, 252},
+      {0xD01FEF10A657842CULL, 800, 260},
+      {0x9B10A4E5E9913129ULL, 827, 268},
+      {0xE7109BFBA19C0C9DULL, 853, 276},
+      {0xAC2820D9623BF429ULL, 880, 284},
+      {0x80444B5E7AA7CF85ULL, 907, 292},
+      {0xBF21E44003ACDD2DULL, 933, 300},
+      {0x8E679C2F5E44FF8FULL, 960, 308},
+      {0xD433179D9C8CB841ULL, 986, 316},
+      {0x9E19DB92B4E31BA9ULL, 1013, 324}};
+  return t[idx];
+}
+inline void round_last(char* buf, int len, uint64_t dist, uint64_t delta, uint64_t rest,
+                       uint64_t ten) {
+  while (rest < dist && delta - rest >= ten &&
+         (rest + ten < dist || dist - rest > rest + ten - dist)) {
+    buf[len - 1]--;
+    rest += ten;
+  }
+}
+// digits of v > 0 into buf; value = digits * 10^dec
+inline int digits(double v, char* buf, int* dec) {
+  uint64_t bits;
+  std::memcpy(&bits, &v, 8);
+  const uint64_t E = (bits >> 52) & 0x7FF, F = bits & ((uint64_t{1} << 52) - 1);
+  const Fp w0 = E == 0 ? Fp{F, 1 - 1075} : Fp{F + (uint64_t{1} << 52), static_cast<int>(E) - 1075};
+  const bool closer = F == 0 && E > 1;
+  const Fp mp{2 * w0.f + 1, w0.e - 1};
+  const Fp mm = closer ? Fp{4 * w0.f - 1, w0.e - 2} : Fp{2 * w0.f - 1, w0.e - 1};
+  const Fp wp = normalize(mp);
+  const Fp wm{mm.f << (mm.e - wp.e), wp.e};
+  const Fp w = normalize(w0);
+  const int f = -60 - wp.e - 1;
+  const int k = (f * 78913) / (1 << 18) + (f > 0 ? 1 : 0);
+  const Cached& c = cached_power((300 + k + 7) / 8);
+  const Fp cw = mul(w, {c.f, c.e}), cm = mul(wm, {c.f, c.e}), cp = mul(wp, {c.f, c.e});
+  const Fp Mm{cm.f + 1, cm.e}, Mp{cp.f - 1, cp.e};
+  *dec = -c.k;
+  uint64_t delta = Mp.f - Mm.f, dist = Mp.f - cw.f;
+  const int sh = -Mp.e;
+  const uint64_t one = uint64_t{1} << sh;
+  uint32_t p1 = static_cast<uint32_t>(Mp.f >> sh);
+  uint64_t p2 = Mp.f & (one - 1);
+  uint32_t pow10 = 1;
+  int n = 1;
+  for (uint32_t p = 1000000000u, d = 10; d > 1; p /= 10, --d)
+    if (p1 >= p) {
+      pow10 = p;
+      n = static_cast<int>(d);
+      break;
+    }
+  int len = 0;
+  while (n > 0) {
+    buf[len++] = static_cast<char>('0' + p1 / pow10);
+    p1 %= pow10;
+    --n;
+    const uint64_t rest = (uint64_t{p1} << sh) + p2;
+    if (rest <= delta) {
+      *dec += n;
+      round_last(buf, len, dist, delta, rest, uint64_t{pow10} << sh);
+      return len;
+    }
+    pow10 /= 10;
+  }
+  int m = 0;
+  for (;;) {
+    p2 *= 10;
+    buf[len++] = static_cast<char>('0' + (p2 >> sh));
+    p2 &= one - 1;
+    ++m;
+    delta *= 10;
+    dist *= 10;
+    if (p2 <= delta) break;
+  }
+  *dec -= m;
+  round_last(buf, len, dist, delta, p2, one);
+  return len;
+}
+}  // namespace grisu
+inline std::string json_double(double v) {
+  if (!std::isfinite(v)) return "null";
+  if (v == 0.0) return std::signbit(v) ? "-0.0" : "0.0";
+  char buf[32];
+  int dec = 0;
+  const int k = grisu::digits(std::fabs(v), buf, &dec);
+  const std::string digits(buf, static_cast<size_t>(k));
+  const int n = k + dec;  // decimal point position
+  std::string o;
+  if (k <= n && n <= 15) {
+    o = digits + std::string(static_cast<size_t>(n - k), '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    o = digits.substr(0, static_cast<size_t>(n)) + "." + digits.substr(static_cast<size_t>(n));
+  } else if (-4 < n && n <= 0) {
+    o = "0." + std::string(static_cast<size_t>(-n), '0') + digits;
+  } else {
+    o = digits.substr(0, 1);
+    if (k > 1) o += "." + digits.substr(1);
+    int ex = n - 1;
+    o += ex < 0 ? "e-" : "e+";
+    ex = ex < 0 ? -ex : ex;
+    if (ex < 10) o += '0';
+    o += std::to_string(ex);
+  }
+  return v < 0 ? "-" + o : o;
+}
+// nlohmann's string escapes: quote, backslash, the short control escapes,
+// other control characters as \u00XX; UTF-8 bytes pass through
 inline std::string json_string(const std::string& v) {
   std::string o = "\"";
   for (const char ch : v) {
     const unsigned char c = static_cast<unsigned char>(ch);
-    if (c == '"' || c == '\\') {
-      o += '\\';
-      o += ch;
-    } else if (c < 0x20) {
-      char e[8];
-      std::snprintf(e, sizeof(e), "\\u%04x", c);
-      o += e;
-    } else {
-      o += ch;
+    switch (c) {
+      case '"': o += "\\\""; break;
+      case '\\': o += "\\\\"; break;
+      case '\b': o += "\\b"; break;
+      case '\f': o += "\\f"; break;
+      case '\n': o += "\\n"; break;
+      case '\r': o += "\\r"; break;
+      case '\t': o += "\\t"; break;
+      default:
+        if (c < 0x20) {
+          char e[8];
+          std::snprintf(e, sizeof(e), "\\u%04x", c);
+          o += e;
+        } else {
+          o += ch;
+        }
     }
   }
   return o + "\"";

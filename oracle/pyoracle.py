@@ -266,6 +266,20 @@ class Ref:
                                        C.c_int]
         L.ref_replay_misses.restype = C.c_longlong
         L.ref_replay_misses.argtypes = [C.c_int]
+        L.ref_result_json.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_int, C.c_double,
+                                      C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int,
+                                      C.c_char_p, C.c_int]
+
+    def result_json(self, id, tokens, joint, label_times, steps, trigger) -> str:
+        """One line of the reference's write_results (io.cpp:81-92), no newline."""
+        tok = (C.c_int * max(1, len(tokens)))(*tokens)
+        lt = (C.c_int * max(1, len(label_times)))(*label_times)
+        buf = C.create_string_buffer(1 << 16)
+        n = self.lib.ref_result_json(id.encode(), tok, len(tokens), joint, lt,
+                                     len(label_times), steps, TRIGGERS.index(trigger), buf,
+                                     len(buf))
+        assert n >= 0
+        return buf.raw[:n].decode().rstrip("\n")
 
     def _corpus(self, h):
         out = []

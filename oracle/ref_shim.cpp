@@ -12,6 +12,7 @@
 #include <exception>
 #include <memory>
 #include <random>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -26,6 +27,7 @@
 #include "beamlattice/segmentation.hpp"
 #include "beamlattice/synth.hpp"
 #include "beamlattice/verify.hpp"
+#include "beamlattice/io.hpp"
 #include "oracle.h"
 
 using namespace beamlattice;
@@ -330,6 +332,33 @@ int ref_num_threads(void) {
 #else
   return 1;
 #endif
+}
+
+// One result line through the reference's own writer (io.cpp:81-92):
+// golden bytes for the drop-in JSONL writers. Returns the length, or -1.
+int ref_result_json(const char* id, const int* tokens, int n_tokens, double joint,
+                    const int* label_times, int n_lt, int steps, int trigger, char* out,
+                    int cap) {
+  try {
+    DecodeResult r;
+    r.id = id;
+    r.tokens.assign(tokens, tokens + n_tokens);
+    r.joint_logp = joint;
+    r.label_times.assign(label_times, label_times + n_lt);
+    r.steps_taken = steps;
+    r.eos_trigger = trigger == 0 ? EosTrigger::kBaseline
+                    : trigger == 1 ? EosTrigger::kCtc
+                                   : EosTrigger::kMaxLen;
+    std::ostringstream os;
+    write_results(os, {r});
+    const std::string s = os.str();
+    if ((int)s.size() >= cap) return -1;
+    std::memcpy(out, s.data(), s.size());
+    out[s.size()] = 0;
+    return (int)s.size();
+  } catch (...) {
+    return -1;
+  }
 }
 
 }  // extern "C"

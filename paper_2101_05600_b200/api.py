@@ -563,9 +563,12 @@ class Decoder:
         (required by the Transformer scorer)."""
         n = len(descs)
         ids = [d[0] for d in descs]
-        key = (id(descs), n, frame_shift_ms)
+        # the packed records are reused only when the descriptors are equal in
+        # content (ids, frames, vocab, pointers), not merely the same list
+        snap = tuple(tuple(d) for d in descs)
+        key = (n, frame_shift_ms)
         cached = self._desc_cache
-        if cached is not None and cached[0] == key and cached[1] is descs:
+        if cached is not None and cached[0] == key and cached[1] == snap:
             arr = cached[2]
         else:
             blob = b"".join(i.encode() + b"\0" for i in ids)
@@ -582,7 +585,7 @@ class Decoder:
                 rec["frame_shift_ms"][:n] = frame_shift_ms
                 rec["logp"][:n] = [d[3] for d in descs]
             arr = (rec, buf)
-            self._desc_cache = (key, descs, arr)
+            self._desc_cache = (key, snap, arr)
         rec = arr[0]
         h = C.c_void_p()
         if self.nbest == 1 and n > 0:
@@ -739,14 +742,138 @@ def read_grid(path: str) -> PosteriorGrid:
     return PosteriorGrid(np.frombuffer(data, "<f4").reshape(T, V).copy(), fs)
 
 
+def _grisu_cached_powers():
+    """10^k, k = -300, -292, ..., 324: round-to-nearest 64-bit significands
+    (the cached-power table of Grisu2 as nlohmann::json uses it)."""
+    from fractions import Fraction
+    out = []
+    for k in range(-300, 325, 8):
+        x = Fraction(10) ** k
+        e = x.numerator.bit_length() - x.denominator.bit_length() - 64
+        while x / Fraction(2) ** e >= 2 ** 64:
+            e += 1
+        while x / Fraction(2) ** e < 2 ** 63:
+            e -= 1
+        q = x / Fraction(2) ** e
+        f = int(q) + (1 if q - int(q) >= Fraction(1, 2) else 0)
+        out.append((f, e, k))
+    return out
+
+
+_GRISU_POW = None
+_M64 = (1 << 64) - 1
+
+
+def _grisu_mul(xf, xe, yf, ye):
+    ul, uh, vl, vh = xf & 0xFFFFFFFF, xf >> 32, yf & 0xFFFFFFFF, yf >> 32
+    p0, p1, p2, p3 = ul * vl, ul * vh, uh * vl, uh * vh
+    q = (p0 >> 32) + (p1 & 0xFFFFFFFF) + (p2 & 0xFFFFFFFF) + (1 << 31)
+    return (p3 + (p2 >> 32) + (p1 >> 32) + (q >> 32)) & _M64, xe + ye + 64
+
+
+def _grisu_digits(v: float):
+    """Grisu2 digits of v > 0 (Loitsch 2010) with nlohmann::json's boundary,
+    cached-power and rounding choices: v = int(digits) * 10**dec. Mirrors
+    include/beamlattice/b200.hpp grisu::digits."""
+    global _GRISU_POW
+    if _GRISU_POW is None:
+        _GRISU_POW = _grisu_cached_powers()
+    bits = struct.unpack("<Q", struct.pack("<d", v))[0]
+    E, F = bits >> 52 & 0x7FF, bits & ((1 << 52) - 1)
+    vf, ve = (F, 1 - 1075) if E == 0 else (F + (1 << 52), E - 1075)
+    mpf, mpe = 2 * vf + 1, ve - 1
+    mmf, mme = (4 * vf - 1, ve - 2) if (F == 0 and E > 1) else (2 * vf - 1, ve - 1)
+    sh = 64 - mpf.bit_length()
+    wpf, wpe = mpf << sh, mpe - sh
+    wmf, wme = mmf << (mme - wpe), wpe
+    sh = 64 - vf.bit_length()
+    wf, we = vf << sh, ve - sh
+    f = -60 - wpe - 1
+    k = abs(f * 78913) >> 18
+    k = (-k if f < 0 else k) + (1 if f > 0 else 0)
+    cf, ce, ck = _GRISU_POW[(300 + k + 7) // 8]
+    w = _grisu_mul(wf, we, cf, ce)
+    mm = _grisu_mul(wmf, wme, cf, ce)
+    mp = _grisu_mul(wpf, wpe, cf, ce)
+    mmf_, mpf_, sh = mm[0] + 1, mp[0] - 1, -mp[1]
+    dec = -ck
+    delta, dist = (mpf_ - mmf_) & _M64, (mpf_ - w[0]) & _M64
+    one = 1 << sh
+    p1, p2 = mpf_ >> sh, mpf_ & (one - 1)
+    n = max(1, len(str(p1)))
+    pow10 = 10 ** (n - 1)
+    buf = []
+
+    def rnd(dist, delta, rest, ten):
+        while rest < dist and delta - rest >= ten and \
+                (rest + ten < dist or dist - rest > rest + ten - dist):
+            buf[-1] -= 1
+            rest += ten
+
+    while n > 0:
+        d, p1 = divmod(p1, pow10)
+        buf.append(d)
+        n -= 1
+        rest = (p1 << sh) + p2
+        if rest <= delta:
+            rnd(dist, delta, rest, pow10 << sh)
+            return "".join(map(str, buf)), dec + n
+        pow10 //= 10
+    m = 0
+    while True:
+        p2 = (p2 * 10) & _M64
+        buf.append(p2 >> sh)
+        p2 &= one - 1
+        m += 1
+        delta, dist = (delta * 10) & _M64, (dist * 10) & _M64
+        if p2 <= delta:
+            break
+    rnd(dist, delta, p2, one)
+    return "".join(map(str, buf)), dec - m
+
+
+def json_double(v: float) -> str:
+    """nlohmann::json's number format (the reference writer, io.cpp:81-92):
+    Grisu2 digits, fixed notation while the decimal point falls in (-4, 15],
+    else d.ddde+XX with at least two exponent digits; non-finite -> null."""
+    v = float(v)
+    if not math.isfinite(v):
+        return "null"
+    if v == 0.0:
+        return "-0.0" if math.copysign(1.0, v) < 0 else "0.0"
+    digits, dec = _grisu_digits(abs(v))
+    k = len(digits)
+    n = k + dec
+    if k <= n <= 15:
+        o = digits + "0" * (n - k) + ".0"
+    elif 0 < n <= 15:
+        o = digits[:n] + "." + digits[n:]
+    elif -4 < n <= 0:
+        o = "0." + "0" * (-n) + digits
+    else:
+        e = n - 1
+        o = digits[0] + ("." + digits[1:] if k > 1 else "") + ("e-" if e < 0 else "e+") \
+            + "%02d" % abs(e)
+    return ("-" if v < 0 else "") + o
+
+
+def _json_ints(v) -> str:
+    return "[" + ",".join(str(int(x)) for x in v) + "]"
+
+
 def result_json(r: DecodeResult) -> str:
-    """io.cpp:81-92 line; keys sorted as nlohmann::json emits them."""
-    d = {"eos_trigger": r.eos_trigger, "id": r.id, "joint_logp": r.joint_logp,
-         "label_times": r.label_times, "steps": r.steps_taken, "tokens": r.tokens}
+    """io.cpp:81-92 line as nlohmann::json dumps it: keys sorted, raw UTF-8
+    strings, nlohmann's number format (json_double)."""
+    parts = ['"eos_trigger":' + json.dumps(r.eos_trigger, ensure_ascii=False),
+             '"id":' + json.dumps(r.id, ensure_ascii=False),
+             '"joint_logp":' + json_double(r.joint_logp),
+             '"label_times":' + _json_ints(r.label_times)]
     if r.nbest and len(r.nbest) > 1:
-        d["nbest"] = [{"joint_logp": j, "label_times": lt, "tokens": t}
-                      for t, j, lt in r.nbest]
-    return json.dumps(d, separators=(",", ":"), sort_keys=True)
+        parts.append('"nbest":[' + ",".join(
+            '{"joint_logp":%s,"label_times":%s,"tokens":%s}'
+            % (json_double(j), _json_ints(lt), _json_ints(t)) for t, j, lt in r.nbest) + "]")
+    parts += ['"steps":%d' % int(r.steps_taken), '"tokens":' + _json_ints(r.tokens)]
+    return "{" + ",".join(parts) + "}"
 
 
 def write_results(fp, results: Iterable[DecodeResult]) -> None:

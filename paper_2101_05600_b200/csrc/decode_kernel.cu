@@ -437,6 +437,10 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
         }
         __nanosleep(1000);
       }
+      // the K1 slab of the TMA variant is read by the async proxy
+      // (cp.async.bulk.tensor, issued by this thread): order those reads
+      // after the generic-proxy acquire of the ready flag
+      asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
   }

@@ -20,11 +20,15 @@ def _grids(n, T, V, ragged, seed):
     return flat.astype(np.float32), lens
 
 
-@pytest.mark.parametrize("V,T,ragged,pinned", [(500, 40, False, True), (7, 33, True, True),
-                                               (7, 33, True, False), (64, 25, True, True)])
-def test_streamed_host_input_equals_device_input(V, T, ragged, pinned):
+@pytest.mark.parametrize("V,T,ragged,pinned,n", [(500, 40, False, True, 900),
+                                                 (7, 33, True, True, 900),
+                                                 (7, 33, True, False, 900),
+                                                 (64, 25, True, True, 900),
+                                                 # vocab 5000: the TMA slab variant reads
+                                                 # the streamed grids by the async proxy
+                                                 (5000, 30, True, True, 320)])
+def test_streamed_host_input_equals_device_input(V, T, ragged, pinned, n):
     torch = pytest.importorskip("torch")
-    n = 900
     flat, lens = _grids(n, T, V, ragged, seed=V + T)
     offs = np.concatenate([[0], np.cumsum(lens)[:-1]])
     dev = torch.from_numpy(flat).cuda()
