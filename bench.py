@@ -2,24 +2,37 @@
 """Benchmark: offline batched joint CTC/attention beam search (BASELINE.json
 metric: audio-seconds decoded per wall-second, i.e. inverse RTF).
 
-Workload (configs[1], "C2"): an 8 h synthetic recording (2,880,000 fbank
-frames at 10 ms) hard-segmented into 2880 x 10 s segments
-(hard_segments(T, 1000, 1000)), each a CTC posterior grid of T_enc = 249
-frames x vocab 500 (|C| = 499, blank = eos = 499) of flat random posteriors
-(the random-init proxy), decoded with batch 64, beam 10, lambda 0.3, M1 = 5,
-M2 = 20, CTC end detection on ("both"). One step decodes all 2880 segments
-per GPU (batches in flight concurrently); under torchrun every
-rank decodes its own 8 h recording (weak scaling) and the n-best records are
-gathered to rank 0 with one NCCL all_gather.
+Headline workload (BASELINE configs[3] "C4" at N=1, i.e. the largest
+single-GPU configuration's decode shape, configs[2] "C3"): ONE 8 h synthetic
+recording (2,880,000 fbank frames at 10 ms) hard-segmented into 2880 x 10 s
+segments (hard_segments(T, 1000, 1000), segmentation.cpp:121-133), each a CTC
+posterior grid of T_enc = 249 frames x vocab 5000 (4999 tokens + blank) of
+flat random posteriors (the random-init proxy), decoded with beam 10 and the
+reference's DecoderConfig defaults (lambda 0.3, M1 5, M2 unbounded, eos
+both; beam_search.hpp:21-33) and the uniform attention scorer, 5-best kept.
+Every segment of the call is in flight at once (one persistent launch).
+
+Multi-GPU (torchrun, N > 1): strong scaling by default -- the SAME recording
+is sharded contiguously over the ranks (dist.shard), each rank decodes its
+block with no per-step collective, and the n-best records are gathered to
+rank 0 by one NCCL collective inside the timed step. --weak gives every rank
+its own 8 h recording instead.
 
   value  : grids resident in HBM, device-timed (CUDA events, max over ranks)
-  e2e    : same call with pinned HOST grids through the C ABI, H2D + D2H inside
-  --impl reference : the compiled reference CPU decoder on a bounded sample
+  e2e    : the same call with pinned HOST grids through the C ABI (H2D
+           streamed into the running kernel, results D2H), device-timed
+  parity : decoded results checked against the compiled reference
+           (oracle/_ref) outside the timed region: the committed C3 golden
+           segments plus the CPU-baseline sample of this run; any mismatch
+           fails the run
+  --impl reference : the compiled reference CPU decoder (oracle/_ref) on a
+           bounded sample of the same workload, all host threads
 """
 from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -31,25 +44,33 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "audio-sec decoded per wall-sec (inverse RTF) at 1/2/4/8 B200; prefix-score GB/s"
-T_ENC, VOCAB, BEAM, M1, M2, LAMBDA = 249, 500, 10, 5, 20, 0.3
-FRAME_SHIFT_MS = 40  # encoder frames (10 ms fbank, 4x subsampling)
+T_ENC, VOCAB, BEAM, LAMBDA, M1 = 249, 5000, 10, 0.3, 5
+NO_MARGIN = 1 << 29
+NBEST = 5
+REC_FRAMES = 2_880_000  # 8 h of 10 ms fbank frames
+FRAME_SHIFT_MS = 40     # encoder frames (10 ms fbank, 4x subsampling)
+SEG_AUDIO_S = T_ENC * FRAME_SHIFT_MS / 1000.0
 
 
 def enc_frames(fbank):  # Conv2dSubsampling (3x3/2 twice), SURVEY §8 vocab note
     return ((fbank - 3) // 2 + 1 - 3) // 2 + 1
 
 
-def workload_config(n_seg):
-    return {"workload": "C2: 8 h synthetic recording -> hard_segments(2880000, 1000, 1000) "
-                        "-> 2880 x 10 s segments per GPU; CTC grids T_enc=249 x vocab 500 "
-                        "flat random posteriors (random-init proxy); batch 64, beam 10, "
-                        "lambda 0.3, M1=5, M2=20, eos both; uniform attention scorer "
-                        "(the Transformer decoder scorer is timed in pipeline_attn)",
-            "segments_per_gpu": n_seg, "T_enc": T_ENC, "vocab": VOCAB, "batch": 64,
-            "beam": BEAM, "margin_m1": M1, "margin_m2": M2, "ctc_weight": LAMBDA,
-            "eos_mode": "both", "scorer": "uniform",
+def workload_config(n_total, n_rank, world, weak):
+    return {"workload": "C4 at N=1 (C3 decode shape): one 8 h synthetic recording -> "
+                        "hard_segments(2880000, 1000, 1000) -> 2880 x 10 s segments; CTC "
+                        "grids T_enc=249 x vocab 5000 flat random posteriors (random-init "
+                        "proxy); beam 10, DecoderConfig defaults (lambda 0.3, M1=5, "
+                        "M2=unbounded, eos both), uniform attention scorer, 5-best; all "
+                        "segments of the call in flight at once (the full Transformer model "
+                        "is timed in model_c3)",
+            "segments_total": n_total, "segments_per_gpu": n_rank, "T_enc": T_ENC,
+            "vocab": VOCAB, "beam": BEAM, "nbest": NBEST, "margin_m1": M1,
+            "margin_m2": "unbounded", "ctc_weight": LAMBDA, "eos_mode": "both",
+            "scorer": "uniform", "sharding": "weak (a recording per rank)" if weak else
+            "strong (one recording sharded contiguously)",
             "l2": "inputs larger than L2 (grids %.2f GB per GPU), no flush"
-                  % (n_seg * T_ENC * VOCAB * 4 / 1e9)}
+                  % (n_rank * T_ENC * VOCAB * 4 / 1e9)}
 
 
 class Clocks:
@@ -105,73 +126,111 @@ def peaks():
 
 
 def ncu_traffic():
+    """dram bytes per launch of the headline kernel from the committed
+    `ncu --set full` capture (profiles/ncu_summary.json), scaled to 2880
+    segments; None when absent."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
+        return d.get("c4_dram_bytes_per_launch")
     except Exception:
         return None
 
 
-def flat_grids(torch, n, seed, device):
-    """n x T_ENC x VOCAB float32 log-posteriors, rows ~ normalised Exp(1)
-    (random_grid, synth.cpp:56-70), generated on the device in chunks."""
+def segment_grids(torch, first, n, device, seed_base):
+    """Grids of segments [first, first + n) of the recording: T_ENC x VOCAB
+    float32 log-posteriors, rows ~ normalised Exp(1) (random_grid,
+    synth.cpp:56-70), one device generator seed per segment, so a segment's
+    grid does not depend on how the recording is sharded."""
     g = torch.empty((n, T_ENC, VOCAB), dtype=torch.float32, device=device)
     gen = torch.Generator(device=device)
-    gen.manual_seed(seed)
-    for s in range(0, n, 256):
-        e = min(n, s + 256)
-        x = torch.empty((e - s, T_ENC, VOCAB), dtype=torch.float64, device=device)
+    x = torch.empty((T_ENC, VOCAB), dtype=torch.float64, device=device)
+    for i in range(n):
+        gen.manual_seed(seed_base + first + i)
         x.exponential_(generator=gen)
-        x = torch.log(x / x.sum(-1, keepdim=True))
-        g[s:e] = x.float()
+        g[i] = torch.log(x / x.sum(-1, keepdim=True)).float()
     return g
 
 
-def cpu_reference_sample(grids_np, threads):
-    """The compiled reference decoder (oracle/_ref) on host cores; falls back
-    to the plain-C port when the reference could not be built."""
+def ref_decode(grids_np, ids, threads):
+    """The compiled reference decoder (oracle/_ref, batched_beam_search) on
+    host cores; the plain-C port when the reference could not be built."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     spec = po.ScorerSpec("uniform", VOCAB - 1)
-    cfg = po.config(beam_width=BEAM, ctc_weight=LAMBDA, margin_m1=M1, margin_m2=M2)
-    ids = [f"s{i}" for i in range(len(grids_np))]
+    cfg = po.config(beam_width=BEAM, ctc_weight=LAMBDA, margin_m1=M1, margin_m2=NO_MARGIN)
     t0 = time.perf_counter()
     if po.Ref.available():
-        po.Ref().decode(list(grids_np), spec, cfg, batch_size=64, ids=ids, threads=threads)
+        res, _ = po.Ref().decode(list(grids_np), spec, cfg, batch_size=128, ids=ids,
+                                 threads=threads)
         kind, cores = "reference", threads
     else:
-        po.Oracle().decode(list(grids_np), spec, cfg, ids=ids)
+        res, _ = po.Oracle().decode(list(grids_np), spec, cfg, ids=ids)
         kind, cores = "port", 1
-    wall = time.perf_counter() - t0
-    audio = len(grids_np) * T_ENC * FRAME_SHIFT_MS / 1000.0
-    return audio / wall, kind, cores, wall
+    return res, kind, cores, time.perf_counter() - t0
+
+
+def same(g, w):
+    return (g.tokens == w.tokens and g.label_times == w.label_times and g.steps_taken == w.steps
+            and g.eos_trigger == w.eos_trigger and abs(g.joint_logp - w.joint_logp) <= 1e-9)
+
+
+def golden_parity(bl, dev):
+    """The committed C3 golden segments (tests/golden, results of the
+    unmodified reference) decoded by this build on this GPU."""
+    sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+    from c3_grids import c3_grids, digest
+    with open(os.path.join(ROOT, "tests", "golden", "c3_expected.json")) as f:
+        exp = json.load(f)
+    items = c3_grids()
+    if digest(items) != exp["sha256"]:
+        return 0, len(items), ["golden grids drifted"]
+    dec = bl.Decoder(bl.UniformScorer(VOCAB - 1), bl.DecoderConfig(beam_width=BEAM),
+                     device=dev.index)
+    got = dec.decode([bl.Utterance(u, bl.PosteriorGrid(g)) for u, g in items])
+    bad = [w["id"] for g, w in zip(got, exp["results"])
+           if not (g.tokens == w["tokens"] and g.label_times == w["label_times"]
+                   and g.steps_taken == w["steps"] and g.eos_trigger == w["eos_trigger"]
+                   and abs(g.joint_logp - w["joint_logp"]) <= 1e-9)]
+    return len(items), len(bad), bad
 
 
 def run_reference(args, rank, world):
+    """The reference arm: oracle/_ref (the unmodified reference compiled here)
+    decoding 10 s vocab-5000 segments of the same workload, one segment per
+    step (about half a minute of all-core CPU work each), so the timed
+    region is capped (--ref-budget seconds) and the steps actually run are
+    reported."""
     if rank != 0:
         return
     import numpy as np
-    rng = np.random.default_rng(7)
-    grids = []
-    for _ in range(args.sample):
-        p = rng.exponential(size=(T_ENC, VOCAB))
-        grids.append(np.log(p / p.sum(1, keepdims=True)).astype(np.float32))
     threads = os.cpu_count() or 1
-    for _ in range(args.warmup):
-        cpu_reference_sample(grids[:2], threads)
+
+    def grid(seed, T):
+        p = np.random.default_rng(seed).exponential(size=(T, VOCAB))
+        return np.log(p / p.sum(1, keepdims=True)).astype(np.float32)
+
+    for w in range(args.warmup):  # warm-up on short segments (code paths, OpenMP pool)
+        ref_decode([grid(900 + w, 20)], ["warm"], threads)
     vals, walls = [], []
-    for _ in range(args.steps):
-        v, kind, cores, wall = cpu_reference_sample(grids, threads)
-        vals.append(v)
+    t_start = time.perf_counter()
+    kind = cores = None
+    for k in range(args.steps):
+        if k > 0 and time.perf_counter() - t_start > args.ref_budget:
+            break
+        _, kind, cores, wall = ref_decode([grid(100000 + k, T_ENC)], [f"seg{k}"], threads)
+        vals.append(SEG_AUDIO_S / wall)
         walls.append(wall)
-    value = statistics.mean(vals)
-    sample = (f"{args.sample} x 10 s segments (T_enc 249, vocab 500, beam 10, M2=20) per step, "
-              f"same workload as the B200 arm")
+    value = len(walls) * SEG_AUDIO_S / sum(walls)
+    sample = (f"1 x 10 s segment per step (T_enc 249, vocab 5000, beam 10, M2 unbounded, "
+              f"flat posteriors), {len(walls)} steps run of {args.steps} requested "
+              f"(timed region capped at {args.ref_budget:.0f} s), {threads} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "audio-s/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000 * statistics.mean(walls), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args.sample),
+            "n_gpus": world, "steps": len(walls), "steps_requested": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(walls),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": workload_config(len(walls), len(walls), 1, False),
             "cpu_baseline": {"value": value, "unit": "audio-s/s", "cores": cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": "audio-s/s", "h2d_bytes_per_step": 0,
@@ -179,158 +238,111 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def run_pipeline(args, torch, dist, bl, dec, ids, n, world, dev, local):
-    """End to end through the public APIs: pinned host fbank (10 s, 80-dim,
-    synthetic) -> device encoder (SMALL: 6 layers, d=256, 4 heads, ff 2048,
-    vocab 500, random-init) -> grids in HBM -> device decode -> results on
-    the host. Same segments, decoder and config as the headline."""
-    from paper_2101_05600_b200 import encoder as benc
-    spec = benc.SMALL
-    enc = benc.Encoder(spec, benc.random_weights(spec, seed=0), device=local, chunk=148)
-    fb = torch.from_numpy(benc.synthetic_fbank(n, 1000, spec.idim, seed=17 + local))
-    fb = fb.pin_memory()
-    grid = torch.empty((n, T_ENC, VOCAB), dtype=torch.float32, device=dev)
-    st = torch.cuda.Stream(device=dev)
-    enc.set_stream(st.cuda_stream)
-    dec.set_stream(st.cuda_stream)
-    stride = T_ENC * VOCAB * 4
-    descs = [(ids[i], T_ENC, VOCAB, grid.data_ptr() + i * stride) for i in range(n)]
-    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-
-    def pstep():
-        e0.record(st)
-        enc.forward_raw(n, 1000, fb.data_ptr(), False, grid.data_ptr(), sync=False)
-        e1.record(st)
-        res = dec.decode_raw(descs, on_device=True)   # returns with results on the host
-        e2.record(st)
-        return res
-
-    for _ in range(max(1, args.warmup - 1)):
-        pstep()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t_enc, t_all = [], []
-    for _ in range(args.steps):
-        pstep()
-        st.synchronize()
-        t_enc.append(e0.elapsed_time(e1))
-        t_all.append(e0.elapsed_time(e2))
-    ms = torch.tensor([statistics.mean(t_all)], device=dev)
-    if world > 1:
-        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = float(ms.item())
-    dec.set_stream(0)
-    enc_ms = statistics.mean(t_enc)
-    d, ff, L, V, F2 = spec.d_model, spec.d_ff, spec.layers, spec.vocab, spec.f2
-    flops_seg = 2.0 * (T_ENC * F2 * d * 9 * d + T_ENC * d * F2 * d
-                       + L * T_ENC * (3 * d * d + d * d + 2 * d * ff) + T_ENC * V * d)
-    audio = world * n * T_ENC * FRAME_SHIFT_MS / 1000.0
-    return {"value": audio / (ms / 1000.0), "unit": "audio-s/s", "ms_per_step": ms,
-            "encoder_ms": enc_ms, "decode_ms": ms - enc_ms,
-            "encoder_tflops": n * flops_seg / (enc_ms / 1000.0) / 1e12,
-            "encoder_flops_per_segment": flops_seg,
-            "h2d_bytes_per_step": n * 1000 * spec.idim * 4,
-            "d2h_bytes_per_step": dec.last_stats.get("d2h_bytes", 0),
-            "model": "encoder 6 layers d=256 4 heads ff=2048 vocab 500 (random-init), "
-                     "synthetic 80-dim fbank, 1000 frames per segment; decode as headline",
-            "launches_per_step": enc.launches + dec.last_stats["launches"]}
-
-
-def run_prefix_c3(torch, bl, dev, peak, n=592):
-    """BASELINE's second metric ("prefix-score GB/s") where the prefix score
-    dominates: the config-3 shape (vocab 5000, beam 10, M1 5, M2 unbounded,
-    T_enc 249, flat posteriors) on 592 segments (4 per SM), K1 algorithmic
-    bytes / kernel time against the measured HBM peak."""
-    V = 5000
+def run_c2(torch, bl, dev, n=2880):
+    """BASELINE config 2's knobs (vocab 500, M2 = 20) on 2880 segments:
+    kernel time of one call (continuity with round 1's headline)."""
+    g = torch.empty((n, T_ENC, 500), dtype=torch.float32, device=dev)
     gen = torch.Generator(device=dev)
-    gen.manual_seed(3)
-    g = torch.empty((n, T_ENC, V), dtype=torch.float32, device=dev)
-    for s0 in range(0, n, 64):
-        x = torch.empty((min(n, s0 + 64) - s0, T_ENC, V), dtype=torch.float64, device=dev)
+    gen.manual_seed(1000)
+    for s0 in range(0, n, 256):
+        x = torch.empty((min(n, s0 + 256) - s0, T_ENC, 500), dtype=torch.float64, device=dev)
         x.exponential_(generator=gen)
         g[s0:s0 + x.shape[0]] = torch.log(x / x.sum(-1, keepdim=True)).float()
         del x
-    dec = bl.Decoder(bl.UniformScorer(V - 1), bl.DecoderConfig(beam_width=BEAM), device=dev.index)
-    descs = [(f"c3_{i}", T_ENC, V, g[i].data_ptr()) for i in range(n)]
+    dec = bl.Decoder(bl.UniformScorer(499),
+                     bl.DecoderConfig(beam_width=BEAM, margin_m2=20), device=dev.index)
+    descs = [(f"c2_{i}", T_ENC, 500, g.data_ptr() + i * T_ENC * 500 * 4) for i in range(n)]
     torch.cuda.synchronize()
-    dec.decode_raw(descs, on_device=True)
-    dec.decode_raw(descs, on_device=True)
+    kms = []
+    for k in range(4):
+        dec.decode_raw(descs, on_device=True)
+        if k:
+            kms.append(dec.last_stats["kernel_ms"])
     st = dec.last_stats
-    gbs = st["k1_bytes"] / (st["kernel_ms"] / 1000.0) / 1e9
-    out = {"segments": n, "vocab": V, "kernel_ms": st["kernel_ms"], "k1_bytes": st["k1_bytes"],
-           "k1_gbs": gbs, "peak_gbs": peak[0], "frac": gbs / peak[0],
-           "audio_s_per_s": n * T_ENC * FRAME_SHIFT_MS / 1000.0 / (st["kernel_ms"] / 1000.0),
-           "kernel": "decode_kernel<10, TMA> (K1 slab streamed by cp.async.bulk.tensor)"}
+    ms = statistics.mean(kms)
+    out = {"segments": n, "vocab": 500, "margin_m2": 20, "kernel_ms": ms,
+           "audio_s_per_s": n * SEG_AUDIO_S / (ms / 1000.0),
+           "k1_gbs": st["k1_bytes"] / (ms / 1000.0) / 1e9,
+           "kernel": "decode_kernel<10, 0> (__ldg slab, keys in shared memory)"}
     del g, dec
     torch.cuda.empty_cache()
     return out
 
 
-def run_pipeline_attn(args, torch, dist, bl, ids, n, world, dev, local):
-    """The full model end to end: pinned host fbank -> device encoder (grid +
-    memory) -> joint CTC/attention decode with the device Transformer decoder
-    scorer (3 layers, d=256, 4 heads, ff 2048, vocab 500; BASELINE cfg 2's
-    '6 enc/3 dec' model, random-init) -> results on the host."""
+def run_model_c3(args, torch, dist, bl, n, world, dev, local, chunk=720):
+    """The full Librispeech-size model (BASELINE config 3: encoder 12 x d512,
+    Transformer decoder scorer 6 x d512, 8 heads, ff 2048, vocab 5000;
+    random-init) end to end: pinned host fbank -> device encoder (grid +
+    memory) -> joint CTC/attention decode with the device decoder scorer ->
+    results on the host, `chunk` segments in flight per call."""
     from paper_2101_05600_b200 import encoder as benc
     from paper_2101_05600_b200 import transformer as btr
     from paper_2101_05600_b200.api import _check, lib
     import ctypes as C
-    espec, dspec = benc.SMALL, btr.SMALL
+    espec, dspec = benc.LARGE, btr.LARGE
     enc = benc.Encoder(espec, benc.random_weights(espec, seed=0), device=local, chunk=148)
     sc = btr.TransformerScorer(dspec, btr.random_weights(dspec, seed=1), device=local)
-    cfg = bl.DecoderConfig(beam_width=BEAM, ctc_weight=LAMBDA, margin_m1=M1, margin_m2=M2,
-                           eos_mode="both")
-    dec = bl.Decoder(sc, cfg, device=local)
+    dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=BEAM), device=local)
     fb = torch.from_numpy(benc.synthetic_fbank(n, 1000, espec.idim, seed=17 + local))
     fb = fb.pin_memory()
-    grid = torch.empty((n, T_ENC, VOCAB), dtype=torch.float32, device=dev)
-    mem = torch.empty((n, T_ENC, espec.d_model), dtype=torch.bfloat16, device=dev)
+    m = min(chunk, n)
+    grid = torch.empty((m, T_ENC, VOCAB), dtype=torch.float32, device=dev)
+    mem = torch.empty((m, T_ENC, espec.d_model), dtype=torch.bfloat16, device=dev)
     st = torch.cuda.Stream(device=dev)
     enc.set_stream(st.cuda_stream)
     dec.set_stream(st.cuda_stream)
     stride = T_ENC * VOCAB * 4
-    descs = [(ids[i], T_ENC, VOCAB, grid.data_ptr() + i * stride) for i in range(n)]
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    t_enc = []
 
     def pstep():
-        e0.record(st)
-        _check(lib().bl_encoder_forward_mem(enc._h, n, 1000, C.c_void_p(fb.data_ptr()), 0,
-                                            C.c_void_p(grid.data_ptr()),
-                                            C.c_void_p(mem.data_ptr()), 0))
-        e1.record(st)
-        res = dec.decode_raw(descs, on_device=True, memory=mem.data_ptr(), mem_frames=T_ENC)
-        e2.record(st)
-        return res
+        res_all, enc_ms = [], 0.0
+        for c0 in range(0, n, m):
+            k = min(m, n - c0)
+            descs = [(f"m{c0 + i}", T_ENC, VOCAB, grid.data_ptr() + i * stride) for i in range(k)]
+            e0.record(st)
+            _check(lib().bl_encoder_forward_mem(
+                enc._h, k, 1000, C.c_void_p(fb.data_ptr() + c0 * 1000 * espec.idim * 4), 0,
+                C.c_void_p(grid.data_ptr()), C.c_void_p(mem.data_ptr()), 0))
+            e1.record(st)
+            res_all += list(dec.decode_raw(descs, on_device=True, memory=mem.data_ptr(),
+                                           mem_frames=T_ENC))
+            st.synchronize()
+            enc_ms += e0.elapsed_time(e1)
+        t_enc.append(enc_ms)
+        return res_all
 
     res = pstep()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    t_enc, t_all = [], []
-    for _ in range(max(1, args.attn_steps)):
+    walls = []
+    for _ in range(max(1, args.model_steps)):
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        t0.record(st)
         res = pstep()
-        st.synchronize()
-        t_enc.append(e0.elapsed_time(e1))
-        t_all.append(e0.elapsed_time(e2))
-    ms = torch.tensor([statistics.mean(t_all)], device=dev)
+        t1.record(st)
+        t1.synchronize()
+        walls.append(t0.elapsed_time(t1))
+    ms = torch.tensor([statistics.mean(walls)], device=dev)
     if world > 1:
         dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    enc_ms = statistics.mean(t_enc)
+    enc_ms = statistics.mean(t_enc[1:]) if len(t_enc) > 1 else t_enc[0]
     lens = [len(r.tokens) for r in res]
-    audio = world * n * T_ENC * FRAME_SHIFT_MS / 1000.0
-    out = {"value": audio / (ms / 1000.0), "unit": "audio-s/s", "ms_per_step": ms,
-           "steps": max(1, args.attn_steps), "encoder_ms": enc_ms, "decode_ms": ms - enc_ms,
+    out = {"value": world * n * SEG_AUDIO_S / (ms / 1000.0), "unit": "audio-s/s",
+           "ms_per_step": ms, "steps": len(walls), "segments_per_gpu": n,
+           "segments_per_call": m, "encoder_ms": enc_ms, "decode_ms": ms - enc_ms,
            "decode_steps_max": max(r.steps_taken for r in res),
            "mean_hyp_tokens": statistics.mean(lens),
            "h2d_bytes_per_step": n * 1000 * espec.idim * 4,
-           "d2h_bytes_per_step": dec.last_stats.get("d2h_bytes", 0),
-           "launches_per_step": enc.launches + dec.last_stats["launches"],
-           "model": "encoder 6 x d256 + Transformer decoder scorer 3 x d256 (4 heads, ff "
-                    "2048, vocab 500), random-init; the near-uniform random decoder keeps "
-                    "hypotheses ~T long (worst case for the per-step decoder)"}
-    del dec, sc
+           "model": "encoder 12 x d512 (8 heads, ff 2048) + Transformer decoder scorer 6 x d512 "
+                    "(8 heads, ff 2048), vocab 5000, random-init, synthetic 80-dim fbank; the "
+                    "near-uniform random decoder keeps hypotheses ~T long (worst case for the "
+                    "per-step decoder); device-timed, fbank in pinned host memory -> results "
+                    "on the host"}
+    del dec, sc, enc, grid, mem
     torch.cuda.empty_cache()
     return out
 
@@ -341,14 +353,19 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--segments", type=int, default=2880, help="segments per GPU")
-    ap.add_argument("--sample", type=int, default=24, help="CPU baseline segments")
+    ap.add_argument("--weak", action="store_true",
+                    help="every rank decodes its own 8 h recording (default: strong scaling)")
+    ap.add_argument("--segments", type=int, default=0,
+                    help="segments of the recording (default: all 2880)")
+    ap.add_argument("--sample", type=int, default=0,
+                    help="CPU-baseline segments (default: ceil(cores / 16), at most 2)")
+    ap.add_argument("--ref-budget", type=float, default=150.0,
+                    help="reference arm: cap on the timed region in seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-pipeline", action="store_true",
-                    help="skip the fbank -> encoder -> decoder legs")
-    ap.add_argument("--attn-steps", type=int, default=2,
-                    help="timed steps of the full-model (Transformer scorer) leg")
+    ap.add_argument("--no-legs", action="store_true", help="skip the C2 and full-model legs")
+    ap.add_argument("--model-steps", type=int, default=1,
+                    help="timed steps of the full-model (config 3) leg")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -358,6 +375,7 @@ def main():
         run_reference(args, rank, world)
         return
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
@@ -368,25 +386,29 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    n = args.segments
     # hard segmentation of the 8 h recording (integer-exact, host C++)
-    segs = bl.hard_segments(2_880_000 * n // 2880, 1000, 1000, f"rec{rank}")
-    assert len(segs) == n and all(enc_frames(s.end - s.start) == T_ENC for s in segs)
-    grids = flat_grids(torch, n, 1000 + rank, dev)
+    rec = REC_FRAMES if not args.segments else args.segments * 1000
+    segs = bl.hard_segments(rec, 1000, 1000, "rec")
+    assert all(enc_frames(s.end - s.start) == T_ENC for s in segs)
+    n_total = len(segs)
+    lo, hi = (0, n_total) if (args.weak or world == 1) else bdist.shard(n_total, world, rank)
+    n = hi - lo
+    seed_base = 100000 + (rank * 10_000_000 if args.weak else 0)
+    grids = segment_grids(torch, lo, n, dev, seed_base)
     torch.cuda.synchronize()
-    cfg = bl.DecoderConfig(beam_width=BEAM, ctc_weight=LAMBDA, margin_m1=M1, margin_m2=M2,
-                           eos_mode="both")
-    dec = bl.Decoder(bl.UniformScorer(VOCAB - 1), cfg, device=local)
+    cfg = bl.DecoderConfig(beam_width=BEAM)  # defaults: lambda .3, M1 5, M2 unbounded, both
+    dec = bl.Decoder(bl.UniformScorer(VOCAB - 1), cfg, device=local, nbest=NBEST)
     stride = T_ENC * VOCAB * 4
     base = grids.data_ptr()
-    ids = [f"{s.utterance_id}:{s.start}-{s.end}" for s in segs]
+    ids = [f"{s.utterance_id}:{s.start}-{s.end}" for s in segs[lo:hi]]
     descs = [(ids[i], T_ENC, VOCAB, base + i * stride) for i in range(n)]
-    audio_per_step = n * T_ENC * FRAME_SHIFT_MS / 1000.0
+    max_tok = T_ENC
 
     def step(on_device, d):
         res = dec.decode_raw(d, on_device=on_device)
-        if world > 1:
-            bdist.gather_results(res, T_ENC, n * world, device=dev)
+        if world > 1:  # one NCCL collective: the n-best records to rank 0
+            bdist.gather_results(res, max_tok, n_total if not args.weak else n * world,
+                                 device=dev, nbest=NBEST)
         return res
 
     for _ in range(args.warmup):
@@ -399,7 +421,7 @@ def main():
         torch.cuda.synchronize()
         ev0.record()
         for _ in range(args.steps):
-            step(True, descs)
+            res = step(True, descs)
             kms.append(dec.last_stats["kernel_ms"])
             k1.append(dec.last_stats["k1_bytes"])
             launches += dec.last_stats["launches"]
@@ -412,13 +434,18 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    value = world * audio_per_step / (ms / 1000.0)
+    units = (n * world) if args.weak else n_total
+    value = units * SEG_AUDIO_S / (ms / 1000.0)
+    stats = dict(dec.last_stats)
+    dev_res = list(res)
 
-    # e2e: pinned host grids through the C ABI (H2D + decode + D2H per step)
+    # e2e: pinned host grids through the C ABI (H2D streamed + decode + D2H)
     e2e = None
+    host = None
     if not args.no_e2e:
         host = grids.cpu().pin_memory()
         del grids
+        grids = None
         torch.cuda.empty_cache()
         hb = host.data_ptr()
         hdescs = [(ids[i], T_ENC, VOCAB, hb + i * stride) for i in range(n)]
@@ -428,59 +455,87 @@ def main():
         torch.cuda.synchronize()
         ev0.record()
         for _ in range(args.steps):
-            step(False, hdescs)
+            hres = step(False, hdescs)
         ev1.record()
         torch.cuda.synchronize()
         ems = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=dev)
         if world > 1:
             dist.all_reduce(ems, op=dist.ReduceOp.MAX)
         ems = float(ems.item())
-        e2e = {"value": world * audio_per_step / (ems / 1000.0), "unit": "audio-s/s",
+        e2e = {"value": units * SEG_AUDIO_S / (ems / 1000.0), "unit": "audio-s/s",
                "ms_per_step": ems, "h2d_bytes_per_step": n * stride,
-               "d2h_bytes_per_step": dec.last_stats.get("d2h_bytes", 0)}
+               "d2h_bytes_per_step": dec.last_stats.get("d2h_bytes", 0),
+               "same_results_as_device_input": all(
+                   a.tokens == b.tokens and a.joint_logp == b.joint_logp
+                   for a, b in zip(hres, dev_res))}
 
-    prefix_c3 = None
-    if not args.no_pipeline:
-        prefix_c3 = run_prefix_c3(torch, bl, dev, peaks())
-    pipeline = pipeline_attn = None
-    if not args.no_pipeline:
-        pipeline = run_pipeline(args, torch, dist, bl, dec, ids, n, world, dev, local)
-        pipeline_attn = run_pipeline_attn(args, torch, dist, bl, ids, n, world, dev, local)
+    # parity gate (outside the timed regions)
+    parity = {"checked": 0, "mismatches": 0, "vs": "oracle/_ref (unmodified reference)"}
+    cpu_line = None
+    if rank == 0:
+        gc, gb, gbad = golden_parity(bl, dev)
+        parity.update(golden_checked=gc, golden_mismatches=gb)
+        parity["checked"] += gc
+        parity["mismatches"] += gb
+        if not args.no_cpu_baseline and world == 1:
+            cores = os.cpu_count() or 1
+            k = args.sample or max(1, min(2, math.ceil(cores / 16)))
+            src = host if host is not None else grids
+            sample = [np.ascontiguousarray(src[i].cpu().numpy()) for i in range(k)]
+            want, kind, used, wall = ref_decode(sample, ids[:k], cores)
+            bad = [w.id for g, w in zip(dev_res[:k], want) if not same(g, w)]
+            parity.update(sample_checked=k, sample_mismatches=len(bad))
+            parity["checked"] += k
+            parity["mismatches"] += len(bad)
+            cpu_line = {"value": k * SEG_AUDIO_S / wall, "unit": "audio-s/s", "cores": used,
+                        "kind": kind,
+                        "sample": f"first {k} of the {n_total} segments (same grids as the "
+                                  f"timed run), {wall:.1f} s wall"}
+    del host
+    torch.cuda.empty_cache()
+
+    c2 = model = None
+    if not args.no_legs:
+        if rank == 0 and world == 1:
+            c2 = run_c2(torch, bl, dev)
+        del dec
+        torch.cuda.empty_cache()
+        model = run_model_c3(args, torch, dist, bl, n, world, dev, local)
 
     peak, peak_kind = peaks()
     kernel_ms = statistics.mean(kms)
-    achieved = statistics.mean(k1) / (kernel_ms / 1000.0) / 1e9
+    k1b = statistics.mean(k1)
+    achieved = k1b / (kernel_ms / 1000.0) / 1e9
+    traffic = ncu_traffic()
     line = {"metric": METRIC, "value": value, "unit": "audio-s/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": workload_config(n),
+            "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(n_total, n, world, args.weak),
             "e2e": e2e, "gpu_launches": launches,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak,
                          "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": ncu_traffic(),
-                         "kernel": "decode_kernel (persistent: K1 bulk + search epilogue)",
-                         "algorithmic_bytes_per_launch": statistics.mean(k1),
-                         "kernel_ms": kernel_ms},
+                         "traffic": traffic,
+                         "traffic_per_algorithmic_byte": (traffic / k1b) if traffic else None,
+                         "kernel": "decode_kernel<10, 2> (persistent: TMA K1 slab stream + "
+                                   "search epilogue, one CTA per segment)",
+                         "algorithmic_bytes_per_launch": k1b, "kernel_ms": kernel_ms},
             "clocks": clk.summary(),
-            "prefix_score_c3": prefix_c3,
-            "pipeline": pipeline,
-            "pipeline_attn": pipeline_attn,
-            "counters": {k: dec.last_stats[k] for k in
+            "parity": parity,
+            "counters": {k: stats[k] for k in
                          ("steps", "scorer_queries", "ctc_frames_evaluated", "contenders",
-                          "fallback_steps")}}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import numpy as np
-        sample = host[:args.sample].numpy() if e2e is not None else \
-            grids[:args.sample].cpu().numpy()
-        v, kind, cores, wall = cpu_reference_sample(list(np.ascontiguousarray(sample)),
-                                                    os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": v, "unit": "audio-s/s", "cores": cores, "kind": kind,
-                                "sample": f"first {args.sample} of the 2880 segments "
-                                          f"({wall:.1f} s wall)"}
+                          "fallback_steps")},
+            "c2_vocab500": c2,
+            "model_c3": model}
+    if cpu_line:
+        line["cpu_baseline"] = cpu_line
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0 and parity["mismatches"]:
+        print("PARITY FAILURE: decoded results differ from the reference", file=sys.stderr)
+        sys.exit(3)
 
 
 if __name__ == "__main__":

@@ -97,7 +97,9 @@ int bl_make_batches(int n, const uint32_t* true_frames, int batch_size,
                     int* order, int* n_batches);
 
 /* ---- scorers: the "model load" hook (make_scorer, scorer.hpp:84) --------- */
-/* spec: "uniform" | "table:PATH" | "loop:TOKEN:P" (scorer.cpp:117-135). */
+/* spec: "uniform" | "table:PATH" | "loop:TOKEN:P" (scorer.cpp:117-135), and
+ * "transformer:PATH[@DEVICE]" (a model file's decoder network, see
+ * bl_model_save). */
 int bl_scorer_create(const char* spec, int num_tokens, bl_scorer** out);
 /* In-memory TableScorer (scorer.hpp:38-55): n_entries contexts of length
  * ctx_len[k] <= order-1 packed in ctx[k*max(order-1,1) ...], each with a
@@ -160,6 +162,9 @@ int bl_results_counters(const bl_results* r, uint64_t* steps,
 int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1_bytes,
                      int* launches, uint64_t* fallback_steps,
                      uint64_t* contenders);
+/* Instrumentation: keys the on-chip filter kept during the prefix-score
+ * bulk (large vocabularies), summed over utterance-steps. */
+int bl_results_filter_keys(const bl_results* r, uint64_t* raw_keys);
 /* Bulk export (one call for all utterances): row i of tokens/label_times
  * (stride cap >= bl_results_max_tokens) holds n_tokens[i] entries. */
 int bl_results_max_tokens(const bl_results* r);
@@ -171,6 +176,26 @@ int bl_results_transfer(const bl_results* r, uint64_t* h2d, uint64_t* d2h);
  * only when the environment variable BL_PROFILE is set. */
 int bl_results_profile(const bl_results* r, double* out16);
 void bl_results_destroy(bl_results* r);
+
+/* ---- decoder group: several GPUs of one process ---------
+ * Replaces the reference's serial loop over batches with an OpenMP fan-out
+ * inside each (tools/beamlattice.cpp:128-132, batched.cpp:146): segments are
+ * sharded contiguously over the devices, each device decodes its block with
+ * no per-step exchange, and the result records (1-best + n-best) are gathered
+ * to the first device by one NCCL group (ncclSend/ncclRecv over NVLink),
+ * then copied to the host once. One communicator from ncclCommInitAll over
+ * the listed devices; NCCL is resolved at run time (libnccl.so.2). Uniform /
+ * table / loop scorers (a transformer scorer is bound to one device). */
+typedef struct bl_group bl_group;
+int bl_group_create(int n_devices, const int* devices, const bl_config* cfg,
+                    const bl_scorer* scorer, bl_group** out);
+int bl_group_size(const bl_group* g);
+/* bl_decoder_set_options on every member. */
+int bl_group_set_options(bl_group* g, int nbest, int exact, double slack);
+/* Host grids; results in input order, identical to one decoder's. Stats:
+ * kernel_ms = the slowest device's decode, counters summed. */
+int bl_group_decode(bl_group* g, int n, const bl_utt* utts, bl_results** out);
+void bl_group_destroy(bl_group* g);
 
 /* ------------------------------------------------------------------------
  * CTC encoder forward (SURVEY.md §8 a'1, the producer of the PosteriorGrid).
@@ -288,6 +313,27 @@ int bl_decoder_set_record(bl_decoder* d, int on);
 int bl_decoder_record_count(const bl_decoder* d);
 int bl_decoder_record_get(const bl_decoder* d, int i, int* utt, int* len, const int** prefix,
                           const double** row);
+
+/* ---- model files and the long-recording chain --------------------------- */
+/* Model file (new; the reference's model-load hook is make_scorer,
+ * scorer.hpp:84): "BLM1", u32 version 1, u32 sections, each {u32 kind
+ * (1 encoder, 2 decoder), u32 spec[6], u64 count, float32[count]} with the
+ * flat weight layouts of bl_encoder_create / bl_scorer_create_transformer.
+ * Either part may be NULL. bl_scorer_create("transformer:PATH[@DEVICE]", |C|)
+ * loads the decoder section (vocabulary checked like table:PATH). */
+int bl_model_save(const char* path, const bl_encoder_spec* enc, const float* enc_w,
+                  size_t n_enc, const bl_transformer_spec* dec, const float* dec_w,
+                  size_t n_dec);
+int bl_encoder_create_from_file(int device, const char* path, bl_encoder** out);
+
+/* One long recording end to end (the chain the reference CLI does by hand,
+ * tools/beamlattice.cpp:234-273 then :117-146): fbank [T][idim] float32 host
+ * -> hard_segments(T, min_len, max_len) -> per segment length one encoder
+ * call (grids and, for a transformer scorer, the memory stay in HBM) -> one
+ * decode call -> results in segment order, ids "<recording_id>:<start>-<end>"
+ * (fbank frames). Encoder and decoder on the same device. */
+int bl_recognize(bl_encoder* e, bl_decoder* d, const float* fbank, int T, int idim,
+                 const char* recording_id, int min_len, int max_len, bl_results** out);
 
 #ifdef __cplusplus
 }

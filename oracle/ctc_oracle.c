@@ -377,7 +377,28 @@ static void reduce_step(utt_search* s, int l, int V, const orc_config* cfg,
 typedef struct rset {
   int n;
   orc_result* r;
+  fin** nb;  /* per utterance: the finished set sorted (joint desc, insertion asc) */
+  int* nnb;
 } rset;
+
+/* n-best = the finished set in (joint desc, insertion asc) order: the
+ * entries finalize_result (batched.cpp:70-90) chooses from, ranked; the head
+ * is finalize's choice (first max in insertion order). Stable insertion sort. */
+static fin* sorted_finished(const utt_search* s) {
+  fin* out = (fin*)malloc(sizeof(fin) * (size_t)(s->nfin > 0 ? s->nfin : 1));
+  for (int k = 0; k < s->nfin; ++k) {
+    fin f = s->finished[k];
+    f.tokens = icopy(f.tokens, f.n, 0);
+    f.label_times = icopy(f.label_times, f.n, 0);
+    int j = k - 1;
+    while (j >= 0 && out[j].joint < f.joint) {
+      out[j + 1] = out[j];
+      --j;
+    }
+    out[j + 1] = f;
+  }
+  return out;
+}
 
 /* finalize_result (batched.cpp:70-90) */
 static void finalize(const utt_search* s, orc_result* out) {
@@ -513,9 +534,13 @@ void* orc_decode(int n, const int* frames, int V, const float* const* grids,
   rset* rs = (rset*)malloc(sizeof(rset));
   rs->n = n;
   rs->r = (orc_result*)calloc(n ? n : 1, sizeof(orc_result));
+  rs->nb = (fin**)calloc(n ? n : 1, sizeof(fin*));
+  rs->nnb = (int*)calloc(n ? n : 1, sizeof(int));
   for (int i = 0; i < n; ++i) {
     utt_search* s = &ss[i];
     finalize(s, &rs->r[i]);
+    rs->nb[i] = sorted_finished(s);
+    rs->nnb[i] = s->nfin;
     for (int j = 0; j < s->nbeam; ++j) {
       free(s->beam[j].tokens);
       free(s->beam[j].label_times);
@@ -535,12 +560,32 @@ void* orc_decode(int n, const int* frames, int V, const float* const* grids,
 
 int orc_results_count(void* h) { return ((rset*)h)->n; }
 void orc_results_get(void* h, int i, orc_result* out) { *out = ((rset*)h)->r[i]; }
+int orc_results_nbest(void* h, int i, int k, orc_result* out) {
+  const rset* rs = (const rset*)h;
+  if (k < 0 || k >= rs->nnb[i]) return rs->nnb[i];
+  const fin* f = &rs->nb[i][k];
+  out->n_tokens = f->n;
+  out->tokens = f->tokens;
+  out->label_times = f->label_times;
+  out->joint_logp = f->joint;
+  out->steps = f->length;
+  out->eos_trigger = f->tau_last;
+  return rs->nnb[i];
+}
+
 void orc_results_free(void* h) {
   rset* rs = (rset*)h;
   for (int i = 0; i < rs->n; ++i) {
     free((void*)rs->r[i].tokens);
     free((void*)rs->r[i].label_times);
+    for (int k = 0; k < rs->nnb[i]; ++k) {
+      free(rs->nb[i][k].tokens);
+      free(rs->nb[i][k].label_times);
+    }
+    free(rs->nb[i]);
   }
+  free(rs->nb);
+  free(rs->nnb);
   free(rs->r);
   free(rs);
 }

@@ -102,6 +102,10 @@ void* orc_decode(int n, const int* frames, int V, const float* const* grids,
 int orc_results_count(void* h);
 void orc_results_get(void* h, int i, orc_result* out);
 void orc_results_free(void* h);
+/* Entry k of utterance i's finished set in (joint desc, insertion asc) order
+ * (the n-best list; steps = entry length incl. eos, eos_trigger = tau_last).
+ * Returns the number of finished entries. */
+int orc_results_nbest(void* h, int i, int k, orc_result* out);
 
 /* make_batches (batched.cpp:12-30): writes the stable length-sorted order
  * into order[n] and returns the number of batches (chunks of batch_size). */

@@ -60,6 +60,7 @@ class Result:
     label_times: List[int]
     steps: int
     eos_trigger: str
+    nbest: list = field(default_factory=list)
 
 
 @dataclass
@@ -124,16 +125,25 @@ def _grid_ptrs(grids: Sequence[np.ndarray]):
     return arrs, ptrs, frames
 
 
-def _collect(lib, prefix, h, ids):
+def _collect(lib, prefix, h, ids, nbest=0):
     out = []
     n = getattr(lib, prefix + "results_count")(h)
     for i in range(n):
         r = OrcResult()
         getattr(lib, prefix + "results_get")(h, i, C.byref(r))
-        out.append(Result(ids[i], [r.tokens[k] for k in range(r.n_tokens)],
-                          r.joint_logp,
-                          [r.label_times[k] for k in range(r.n_tokens)],
-                          r.steps, TRIGGERS[r.eos_trigger]))
+        res = Result(ids[i], [r.tokens[k] for k in range(r.n_tokens)],
+                     r.joint_logp,
+                     [r.label_times[k] for k in range(r.n_tokens)],
+                     r.steps, TRIGGERS[r.eos_trigger])
+        if nbest:
+            # the finished set, (joint desc, insertion asc): [(tokens, joint, label_times)]
+            res.nbest = []
+            nf = lib.orc_results_nbest(h, i, -1, C.byref(r))
+            for k in range(min(nf, nbest)):
+                lib.orc_results_nbest(h, i, k, C.byref(r))
+                res.nbest.append(([r.tokens[q] for q in range(r.n_tokens)], r.joint_logp,
+                                  [r.label_times[q] for q in range(r.n_tokens)]))
+        out.append(res)
     getattr(lib, prefix + "results_free")(h)
     return out
 
@@ -174,9 +184,12 @@ class Oracle:
                                         C.c_int]
         L.orc_make_batches.argtypes = [C.c_int, C.POINTER(C.c_uint32), C.c_int,
                                        C.POINTER(C.c_int)]
+        L.orc_results_nbest.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(OrcResult)]
 
     def decode(self, grids, scorer: ScorerSpec, cfg: OrcConfig, batched=True,
-               ids=None):
+               ids=None, nbest=0):
+        """nbest > 0: each Result also carries the first `nbest` entries of
+        the finished set in (joint desc, insertion asc) order."""
         ids = ids or [f"u{i}" for i in range(len(grids))]
         arrs, ptrs, frames = _grid_ptrs(grids)
         V = arrs[0].shape[1]
@@ -188,7 +201,7 @@ class Oracle:
                                 C.byref(cnt), err, 512)
         if not h:
             raise ValueError(err.value.decode())
-        return _collect(self.lib, "orc_", h, ids), (cnt.steps, cnt.scorer_queries,
+        return _collect(self.lib, "orc_", h, ids, nbest), (cnt.steps, cnt.scorer_queries,
                                                      cnt.ctc_frames_evaluated)
 
     def hard_segments(self, T, min_len, max_len):

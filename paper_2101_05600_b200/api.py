@@ -105,6 +105,7 @@ def lib() -> C.CDLL:
     L.bl_results_counters.argtypes = [vp, u64p, u64p, u64p]
     L.bl_results_stats.argtypes = [vp, dp, u64p, ip, u64p, u64p]
     L.bl_results_profile.argtypes = [vp, dp]
+    L.bl_results_filter_keys.argtypes = [vp, u64p]
     L.bl_results_transfer.argtypes = [vp, u64p, u64p]
     L.bl_results_max_tokens.argtypes = [vp]
     L.bl_results_export.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -130,6 +131,16 @@ def lib() -> C.CDLL:
     L.bl_decode_into.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.c_int, vp, C.c_int, C.c_int,
                                  vp, vp, vp, vp, vp, vp, C.POINTER(vp)]
     L.bl_encoder_forward_mem.argtypes = [vp, C.c_int, C.c_int, vp, C.c_int, vp, vp, C.c_int]
+    L.bl_model_save.argtypes = [C.c_char_p, vp, vp, C.c_size_t, vp, vp, C.c_size_t]
+    L.bl_encoder_create_from_file.argtypes = [C.c_int, C.c_char_p, C.POINTER(vp)]
+    L.bl_recognize.argtypes = [vp, vp, vp, C.c_int, C.c_int, C.c_char_p, C.c_int, C.c_int,
+                               C.POINTER(vp)]
+    L.bl_group_create.argtypes = [C.c_int, ip, C.POINTER(_Config), vp, C.POINTER(vp)]
+    L.bl_group_size.argtypes = [vp]
+    L.bl_group_set_options.argtypes = [vp, C.c_int, C.c_int, C.c_double]
+    L.bl_group_decode.argtypes = [vp, C.c_int, C.POINTER(_Utt), C.POINTER(vp)]
+    L.bl_group_destroy.argtypes = [vp]
+    L.bl_group_destroy.restype = None
     L.bl_gemm_bf16.argtypes = [C.c_int, C.c_int, C.c_int, vp, C.c_int, vp, C.c_int, C.c_int,
                                vp, vp, vp, C.c_int, C.c_float, vp, C.c_int, vp]
     _lib = L
@@ -411,10 +422,15 @@ class _SpecScorer(Scorer):
         h = C.c_void_p()
         _check(lib().bl_scorer_create(spec.encode(), num_tokens, C.byref(h)))
         self._h = h
+        self.spec_string = spec
+        # a network scorer: decoding needs the encoder memory
+        self.is_network = spec.startswith("transformer:")
 
 
 def make_scorer(spec: str, num_tokens: int) -> Scorer:
-    """scorer.cpp:117-135: "uniform" | "table:PATH" | "loop:TOKEN:P"."""
+    """scorer.cpp:117-135: "uniform" | "table:PATH" | "loop:TOKEN:P", plus
+    "transformer:PATH[@DEVICE]" (the decoder network of a model file written
+    by paper_2101_05600_b200.model.save_model / bl_model_save)."""
     return _SpecScorer(spec, num_tokens)
 
 
@@ -677,10 +693,59 @@ class Decoder:
         L.bl_results_transfer(h, C.byref(h2d), C.byref(d2h))
         self.last_stats["h2d_bytes"] = h2d.value
         self.last_stats["d2h_bytes"] = d2h.value
+        rk = C.c_uint64()
+        L.bl_results_filter_keys(h, C.byref(rk))
+        self.last_stats["filter_keys"] = rk.value
         if os.environ.get("BL_PROFILE"):
             prof = (C.c_double * 16)()
             L.bl_results_profile(h, prof)
             self.last_stats["profile_cycles"] = [round(x) for x in prof]
+
+
+class Group:
+    """Several GPUs of one process (bl_group_*): segments sharded
+    contiguously over `devices`, decoded concurrently with no per-step
+    exchange, result records (1-best + n-best) gathered to the first device
+    by one NCCL group, results in input order."""
+
+    _collect = Decoder._collect
+    _stats = Decoder._stats
+
+    def __init__(self, scorer: Scorer, cfg: Optional[DecoderConfig] = None,
+                 devices: Sequence[int] = (0,), nbest: int = 1, exact: bool = False,
+                 slack: float = 1.0):
+        self.nbest = nbest
+        self.cfg = cfg or DecoderConfig()
+        self.scorer = scorer
+        self.devices = list(devices)
+        dv = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        _check(lib().bl_group_create(len(self.devices), dv, C.byref(self.cfg._c()),
+                                     scorer._h, C.byref(h)))
+        self._h = h
+        _check(lib().bl_group_set_options(h, nbest, 1 if exact else 0, slack))
+        self.last_stats: Dict[str, float] = {}
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and _lib is not None:
+            _lib.bl_group_destroy(self._h)
+            self._h = None
+
+    def decode(self, utterances: Sequence[Utterance],
+               counters: Optional[DecodeCounters] = None) -> "ResultSet":
+        keep = [u.grid.logp for u in utterances]
+        n = len(utterances)
+        ids = [u.id for u in utterances]
+        arr = (_Utt * max(n, 1))()
+        for i, (u, g) in enumerate(zip(utterances, keep)):
+            arr[i] = _Utt(ids[i].encode(), u.grid.num_frames, u.grid.vocab,
+                          u.grid.frame_shift_ms, g.ctypes.data)
+        h = C.c_void_p()
+        _check(lib().bl_group_decode(self._h, n, arr, C.byref(h)))
+        try:
+            return self._collect(h, counters, ids)
+        finally:
+            lib().bl_results_destroy(h)
 
 
 _decoders: Dict[tuple, Decoder] = {}

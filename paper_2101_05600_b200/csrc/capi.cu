@@ -3,6 +3,8 @@
 // reference semantics cited per function; all decoding runs on the GPU —
 // there is no CPU fallback.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <chrono>
@@ -16,6 +18,7 @@
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <json.hpp>
@@ -235,7 +238,7 @@ struct bl_decoder {
   int sc_order = 1, sc_nent = 0, sc_w = 1;
   DevBuf sc_ctx_len, sc_ctx, sc_row, sc_rows, sc_rowsf;
   // workspace
-  DevBuf grid, utts, gam, Ftab, Gtab, kubg, ubitsg, xs, taken, hist, fin, res, cnt, prof;
+  DevBuf grid, utts, gam, Ftab, Gtab, xs, taken, hist, fin, res, cnt, prof;
   HostBuf h_grid, h_utts, h_res, h_cnt, h_prof;
   bool profile = getenv("BL_PROFILE") != nullptr;
   // step-granular decoding (forced for tests, or required by a network scorer)
@@ -262,6 +265,11 @@ struct bl_decoder {
   unsigned epoch = 0;
   size_t ready_n = 0;
   cudaEvent_t ev_copied = nullptr;
+  // decoder group (bl_group_decode): result records keep a group-wide step
+  // capacity and stay on the device (padded to keep_rows rows) for the NCCL
+  // gather instead of being copied to the host by this decoder
+  int force_S = 0;
+  int keep_rows = 0;
 };
 
 struct bl_results {
@@ -276,6 +284,7 @@ struct bl_results {
   std::vector<One> r;
   int max_tokens = 0;
   uint64_t steps = 0, queries = 0, frames = 0, k1 = 0, fallback = 0, contenders = 0;
+  uint64_t raw_keys = 0;  // filter mode: keys that reached the running bound
   uint64_t h2d = 0, d2h = 0;
   double kernel_ms = 0.0;
   int launches = 0;
@@ -479,6 +488,8 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   }
   if (bl::bmax_for(B) == 0)
     throw std::invalid_argument("beam width > 32 is not supported by the device decoder");
+  if (V > (1 << 24))
+    throw std::invalid_argument("vocabulary > 2^24 is not supported by the device decoder");
   CK(cudaSetDevice(d->device));
 
   int Tmax = 0, S = 0;
@@ -491,6 +502,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     desc[i].T = T;
     desc[i].max_steps = static_cast<int>(std::ceil(d->cfg.max_steps_ratio * T));
     S = std::max(S, desc[i].max_steps);
+    S = std::max(S, d->force_S);
     desc[i].need_tail = d->cfg.margin_m2 < T ? 1 : 0;
     goff[i] = gtotal;  // dense packing: a contiguous host batch is one copy
     gtotal += (size_t)T * V;
@@ -539,7 +551,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   }
   // shared-memory plan: the aliased region (P3-P5 keys, P6 staging) is sized
   // so the whole plan fits 3 CTAs/SM (~71 KB) when the fixed parts allow it;
-  // the upper keys move to HBM when they do not fit.
+  // otherwise the keys are filtered on chip while P3 emits them (filter mode).
   const size_t fixed = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).total;
   const size_t budget = 66 * 1024;  // + static smem + 1 KB reserve: 3 CTAs in 228 KB
   const size_t need1 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 1).region_need;
@@ -547,15 +559,11 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   size_t region = fixed + need1 <= budget ? budget - fixed : std::max(need0, budget > fixed ? budget - fixed : 0);
   const int kub_smem = (!use_tma && need1 <= region) ? 1 : 0;
   region = (std::max(region, kub_smem ? need1 : need0) + 15) & ~(size_t)15;
-  if (!kub_smem) {
-    d->kubg.ensure(sizeof(float) * (size_t)U * B * C);
-    d->ubitsg.ensure(sizeof(unsigned) * (size_t)U * (((size_t)B * C + 31) / 32));
-  }
   d->xs.ensure(sizeof(double) * (size_t)U * B * (C + 1));
   d->taken.ensure((size_t)U * B * (C + 1));
   d->hist.ensure(sizeof(bl::HistRec) * (size_t)U * (S + 1) * B);
   d->fin.ensure(sizeof(bl::FinEntry) * (size_t)U * B * S);
-  d->res.ensure(sizeof(int) * (size_t)U * rs);
+  d->res.ensure(sizeof(int) * (size_t)std::max(U, d->keep_rows) * rs);
   d->cnt.ensure(sizeof(unsigned long long) * (size_t)U * 8);
   d->utts.ensure(sizeof(bl::UttDesc) * U);
   d->h_utts.ensure(sizeof(bl::UttDesc) * U);
@@ -627,8 +635,6 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.gam = static_cast<double*>(d->gam.p);
   p.Ftab = static_cast<double*>(d->Ftab.p);
   p.Gtab = static_cast<double*>(d->Gtab.p);
-  p.kubg = static_cast<float*>(d->kubg.p);
-  p.ubitsg = static_cast<unsigned*>(d->ubitsg.p);
   p.kub_smem = kub_smem;
   p.region_bytes = (int)region;
   p.use_tma = use_tma ? 1 : 0;
@@ -823,7 +829,9 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     cudaGetLastError();
   }
   const int* dres = static_cast<const int*>(d->res.p);
-  if (direct) {
+  if (d->keep_rows) {
+    // group decode: records stay in d->res for the NCCL gather
+  } else if (direct) {
     const size_t sp = sizeof(int) * (size_t)rs, dp = sizeof(int) * (size_t)into->cap;
     CK(cudaMemcpy2DAsync(d->h_res.p, sizeof(int) * bl::kResHdr, dres, sp,
                          sizeof(int) * bl::kResHdr, U, cudaMemcpyDeviceToHost, st));
@@ -856,9 +864,26 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   CK(cudaEventElapsedTime(&ms, d->ev0, d->ev1));
   res->kernel_ms = ms;
   res->launches = launches;
-  res->d2h = (direct ? sizeof(int) * (size_t)U * (bl::kResHdr + 2 * (size_t)S)
-                     : sizeof(int) * (size_t)U * rs) +
+  res->d2h = (d->keep_rows ? 0
+                            : direct ? sizeof(int) * (size_t)U * (bl::kResHdr + 2 * (size_t)S)
+                                     : sizeof(int) * (size_t)U * rs) +
              sizeof(unsigned long long) * (size_t)U * 8;
+  if (d->keep_rows) {  // counters and stats only; the group assembles the results
+    const unsigned long long* hc = static_cast<const unsigned long long*>(d->h_cnt.p);
+    for (int i = 0; i < n; ++i) {
+      const unsigned long long* c = hc + (size_t)i * 8;
+      res->steps += c[0];
+      res->queries += c[1];
+      res->frames += c[2];
+      res->k1 += c[3];
+      res->fallback += c[4];
+      res->contenders += c[5];
+      res->raw_keys += c[6];
+    }
+    res->max_tokens = S;
+    *out = res.release();
+    return BL_OK;
+  }
 
   const int* hr = static_cast<const int*>(d->h_res.p);
   const unsigned long long* hc = static_cast<const unsigned long long*>(d->h_cnt.p);
@@ -884,6 +909,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       res->k1 += c[3];
       res->fallback += c[4];
       res->contenders += c[5];
+      res->raw_keys += c[6];
     }
     if (host_timing) {
       auto ms = [](clk::time_point a, clk::time_point b) {
@@ -924,12 +950,69 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     res->k1 += c[3];
     res->fallback += c[4];
     res->contenders += c[5];
+    res->raw_keys += c[6];
   }
   *out = res.release();
   return BL_OK;
 }
 
 }  // namespace
+
+// ----------------------------------------------------------- model files
+// One binary file with the network weights of a model: "BLM1", u32 version
+// (1), u32 section count, then per section u32 kind (1 = encoder, 2 =
+// decoder), u32 spec[6] (encoder: idim d_model heads d_ff layers vocab;
+// decoder: d_model heads d_ff layers vocab 0), u64 count, float32[count] in
+// the flat layouts of bl_encoder_create / bl_scorer_create_transformer.
+// Little-endian. The reference's "model load" hook is make_scorer
+// (scorer.hpp:84); "transformer:PATH" loads the decoder section.
+struct ModelFile {
+  bool has_enc = false, has_dec = false;
+  bl_encoder_spec enc{};
+  bl_transformer_spec dec{};
+  std::vector<float> enc_w, dec_w;
+};
+
+ModelFile read_model(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw std::runtime_error("cannot open model file: " + path);
+  auto u32 = [&]() {
+    uint32_t v = 0;
+    is.read(reinterpret_cast<char*>(&v), 4);
+    if (!is) throw std::runtime_error("truncated model file: " + path);
+    return v;
+  };
+  char magic[4];
+  is.read(magic, 4);
+  if (!is || std::memcmp(magic, "BLM1", 4) != 0)
+    throw std::runtime_error("bad magic in model file: " + path);
+  if (u32() != 1) throw std::runtime_error("unsupported model file version in " + path);
+  const uint32_t nsec = u32();
+  ModelFile mf;
+  for (uint32_t k = 0; k < nsec; ++k) {
+    const uint32_t kind = u32();
+    uint32_t sp[6];
+    for (auto& x : sp) x = u32();
+    uint64_t count = 0;
+    is.read(reinterpret_cast<char*>(&count), 8);
+    if (!is || count > (1ull << 34)) throw std::runtime_error("bad section in " + path);
+    std::vector<float> w(count);
+    is.read(reinterpret_cast<char*>(w.data()), (std::streamsize)(count * sizeof(float)));
+    if (!is) throw std::runtime_error("truncated model file: " + path);
+    if (kind == 1) {
+      mf.has_enc = true;
+      mf.enc = {(int)sp[0], (int)sp[1], (int)sp[2], (int)sp[3], (int)sp[4], (int)sp[5]};
+      mf.enc_w = std::move(w);
+    } else if (kind == 2) {
+      mf.has_dec = true;
+      mf.dec = {(int)sp[0], (int)sp[1], (int)sp[2], (int)sp[3], (int)sp[4]};
+      mf.dec_w = std::move(w);
+    } else {
+      throw std::runtime_error("unknown section kind in " + path);
+    }
+  }
+  return mf;
+}
 
 // ====================================================================== C ABI
 extern "C" {
@@ -1105,6 +1188,25 @@ int bl_scorer_create(const char* spec_c, int num_tokens, bl_scorer** out) {
       int token = std::stoi(rest.substr(0, colon));
       double p = std::stod(rest.substr(colon + 1));
       *out = make_loop(num_tokens, token, p);
+      return BL_OK;
+    }
+    if (spec.rfind("transformer:", 0) == 0) {
+      // "transformer:PATH[@DEVICE]": the decoder section of a model file
+      // (bl_model_save), loaded onto DEVICE (default 0)
+      std::string path = spec.substr(12);
+      int device = 0;
+      const auto at = path.rfind('@');
+      if (at != std::string::npos) {
+        device = std::stoi(path.substr(at + 1));
+        path = path.substr(0, at);
+      }
+      ModelFile mf = read_model(path);
+      if (!mf.has_dec) throw std::runtime_error("model file has no decoder section: " + path);
+      if (mf.dec.vocab - 1 != num_tokens)
+        throw std::runtime_error("transformer scorer vocabulary does not match grids");
+      const int rc = bl_scorer_create_transformer(device, &mf.dec, mf.dec_w.data(),
+                                                  mf.dec_w.size(), out);
+      if (rc != BL_OK) throw BlError{rc, g_err};
       return BL_OK;
     }
     throw std::runtime_error("unknown scorer spec: " + spec);
@@ -1321,6 +1423,10 @@ int bl_decode_memory(bl_decoder* d, int n, const bl_utt* utts, int grids_on_devi
 }
 
 int bl_results_count(const bl_results* r) { return (int)r->r.size(); }
+int bl_results_filter_keys(const bl_results* r, uint64_t* raw_keys) {
+  *raw_keys = r->raw_keys;
+  return BL_OK;
+}
 int bl_results_max_tokens(const bl_results* r) { return r->max_tokens; }
 
 int bl_results_get(const bl_results* r, int i, const char** id, const int** tokens,
@@ -1405,6 +1511,7 @@ void bl_results_destroy(bl_results* r) { delete r; }
 // ------------------------------------------------------------------ encoder
 struct bl_encoder {
   int device = 0;
+  bl_encoder_spec spec{};
   bl::EncoderImpl* impl = nullptr;
   cudaStream_t own = nullptr;
   int chunk = 148;  // 148 x 249 rows = 2 waves of 128-row tiles on 148 SMs
@@ -1440,6 +1547,7 @@ int bl_encoder_create(int device, const bl_encoder_spec* spec, const float* weig
     CK(cudaSetDevice(device));
     std::unique_ptr<bl_encoder> e(new bl_encoder);
     e->device = device;
+    e->spec = *spec;
     CK(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking));
     CK(bl::enc_create(s, weights, &e->impl));
     bl::enc_set_stream(e->impl, e->own);
@@ -1504,6 +1612,131 @@ void bl_encoder_destroy(bl_encoder* e) {
   delete e;
 }
 
+int bl_model_save(const char* path, const bl_encoder_spec* enc, const float* enc_w,
+                  size_t n_enc, const bl_transformer_spec* dec, const float* dec_w,
+                  size_t n_dec) {
+  return guarded([&] {
+    if (!path) throw std::invalid_argument("null path");
+    if (enc && n_enc != bl_encoder_num_weights(enc))
+      throw std::invalid_argument("encoder weight count mismatch");
+    if (dec && n_dec != bl_transformer_num_weights(dec))
+      throw std::invalid_argument("decoder weight count mismatch");
+    std::ofstream os(path, std::ios::binary);
+    if (!os) throw std::runtime_error(std::string("cannot write model file: ") + path);
+    auto u32 = [&](uint32_t v) { os.write(reinterpret_cast<const char*>(&v), 4); };
+    os.write("BLM1", 4);
+    u32(1);
+    u32((enc ? 1 : 0) + (dec ? 1 : 0));
+    if (enc) {
+      u32(1);
+      for (int v : {enc->idim, enc->d_model, enc->heads, enc->d_ff, enc->layers, enc->vocab})
+        u32((uint32_t)v);
+      const uint64_t c = n_enc;
+      os.write(reinterpret_cast<const char*>(&c), 8);
+      os.write(reinterpret_cast<const char*>(enc_w), (std::streamsize)(n_enc * sizeof(float)));
+    }
+    if (dec) {
+      u32(2);
+      for (int v : {dec->d_model, dec->heads, dec->d_ff, dec->layers, dec->vocab, 0})
+        u32((uint32_t)v);
+      const uint64_t c = n_dec;
+      os.write(reinterpret_cast<const char*>(&c), 8);
+      os.write(reinterpret_cast<const char*>(dec_w), (std::streamsize)(n_dec * sizeof(float)));
+    }
+    if (!os) throw std::runtime_error(std::string("short write: ") + path);
+    return BL_OK;
+  });
+}
+
+int bl_encoder_create_from_file(int device, const char* path, bl_encoder** out) {
+  return guarded([&] {
+    if (!path) throw std::invalid_argument("null path");
+    ModelFile mf = read_model(path);
+    if (!mf.has_enc) throw std::runtime_error(std::string("model file has no encoder: ") + path);
+    const int rc = bl_encoder_create(device, &mf.enc, mf.enc_w.data(), mf.enc_w.size(), out);
+    if (rc != BL_OK) throw BlError{rc, g_err};
+    return BL_OK;
+  });
+}
+
+// segment -> slice -> encode -> batched decode for one long recording: the
+// chaining the reference leaves to its CLI (tools/beamlattice.cpp:234-273
+// segments, :117-146 decodes pre-cut grids). hard_segments
+// (segmentation.cpp:121-133) gives at most two segment lengths; each length
+// is one encoder call (grids, and the memory for a transformer scorer, stay
+// in HBM) and one decode call. Results in segment order, ids
+// "<rec>:<start>-<end>".
+int bl_recognize(bl_encoder* e, bl_decoder* d, const float* fbank, int T, int idim,
+                 const char* recording_id, int min_len, int max_len, bl_results** out) {
+  return guarded([&] {
+    if (!e || !d || !fbank || !out) throw std::invalid_argument("null argument");
+    if (idim != e->spec.idim) throw std::invalid_argument("fbank dimension does not match the encoder");
+    if (e->spec.vocab - 1 != d->num_tokens)
+      throw std::invalid_argument("encoder vocabulary does not match the decoder's scorer");
+    if (e->device != d->device) throw std::invalid_argument("encoder and decoder on different devices");
+    const bool attn = d->net != nullptr;
+    int nseg = 0;
+    const int cap = T / std::max(1, max_len) + 2;
+    std::vector<int> st(cap), en(cap);
+    int rc = bl_hard_segments(T, min_len, max_len, st.data(), en.data(), cap, &nseg);
+    if (rc != BL_OK) throw BlError{rc, g_err};
+    const std::string rec = recording_id ? recording_id : "rec";
+    std::map<int, std::vector<int>> groups;  // length -> segment indices
+    for (int i = 0; i < nseg; ++i) groups[en[i] - st[i]].push_back(i);
+    auto res = std::make_unique<bl_results>();
+    res->r.resize(nseg);
+    CK(cudaSetDevice(d->device));
+    for (const auto& [len, idx] : groups) {
+      const int T2 = bl::enc_frames_out(len);
+      if (T2 < 1)
+        throw std::invalid_argument("segment of " + std::to_string(len) +
+                                    " frames is too short for the encoder");
+      const int m = (int)idx.size();
+      HostBuf slab;  // the group's segments back to back, page-locked
+      slab.ensure(sizeof(float) * (size_t)m * len * idim);
+      float* hs = static_cast<float*>(slab.p);
+      for (int r = 0; r < m; ++r)
+        std::memcpy(hs + (size_t)r * len * idim, fbank + (size_t)st[idx[r]] * idim,
+                    sizeof(float) * (size_t)len * idim);
+      DevBuf grid, mem;
+      const int V = e->spec.vocab;
+      grid.ensure(sizeof(float) * (size_t)m * T2 * V);
+      if (attn) mem.ensure(2 * (size_t)m * T2 * e->spec.d_model);
+      rc = bl_encoder_forward_mem(e, m, len, hs, 0, static_cast<float*>(grid.p),
+                                  attn ? mem.p : nullptr, 1);
+      if (rc != BL_OK) throw BlError{rc, g_err};
+      std::vector<std::string> ids(m);
+      std::vector<bl_utt> utts(m);
+      for (int r = 0; r < m; ++r) {
+        const int i = idx[r];
+        ids[r] = rec + ":" + std::to_string(st[i]) + "-" + std::to_string(en[i]);
+        utts[r] = {ids[r].c_str(), (uint32_t)T2, (uint32_t)V, 40,
+                   static_cast<const float*>(grid.p) + (size_t)r * T2 * V};
+      }
+      bl_results* part = nullptr;
+      rc = attn ? bl_decode_memory(d, m, utts.data(), 1, mem.p, T2, &part)
+                : bl_decode(d, m, utts.data(), 1, &part);
+      if (rc != BL_OK) throw BlError{rc, g_err};
+      std::unique_ptr<bl_results> pp(part);
+      for (int r = 0; r < m; ++r) res->r[idx[r]] = std::move(pp->r[r]);
+      res->max_tokens = std::max(res->max_tokens, pp->max_tokens);
+      res->steps += pp->steps;
+      res->queries += pp->queries;
+      res->frames += pp->frames;
+      res->k1 += pp->k1;
+      res->fallback += pp->fallback;
+      res->contenders += pp->contenders;
+      res->raw_keys += pp->raw_keys;
+      res->kernel_ms += pp->kernel_ms;
+      res->launches += pp->launches + e->launches;
+      res->h2d += sizeof(float) * (size_t)m * len * idim;
+      res->d2h += pp->d2h;
+    }
+    *out = res.release();
+    return BL_OK;
+  });
+}
+
 int bl_gemm_bf16(int M, int N, int K, const void* A, int lda, const void* B, int ldb, int mode,
                  const float* bias, float* out_f32, void* out_bf16, int ldo, float scale,
                  const float* pe, int pe_rows, void* stream) {
@@ -1529,6 +1762,248 @@ int bl_gemm_bf16(int M, int N, int K, const void* A, int lda, const void* B, int
     CK(bl::gemm_bf16(g, static_cast<cudaStream_t>(stream)));
     return BL_OK;
   });
+}
+
+// ---------------------------------------------------------------- groups
+// One process driving several GPUs: the reference's only
+// parallelism is an OpenMP fan-out inside a serial loop over batches
+// (batched.cpp:146, tools/beamlattice.cpp:128-132). Here the segments are
+// sharded contiguously over the group's devices, every device decodes its
+// block with no per-step exchange (one host thread per device), and the
+// result records (1-best + n-best) are gathered to the first device by ONE
+// NCCL group of ncclSend/ncclRecv, then copied to the host once. NCCL is
+// resolved at run time (the copy already loaded in the process, e.g. by
+// torch, else libnccl.so.2), so the library itself has no link-time NCCL
+// dependency.
+}  // extern "C"
+
+namespace {
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*CommInitAll)(ncclComm_t*, int, const int*) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*ErrStr)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+      if (!a.h) a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (a.h) break;
+    }
+    if (a.h) {
+      a.CommInitAll = reinterpret_cast<decltype(a.CommInitAll)>(dlsym(a.h, "ncclCommInitAll"));
+      a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(a.h, "ncclCommDestroy"));
+      a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(a.h, "ncclGroupStart"));
+      a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(a.h, "ncclGroupEnd"));
+      a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(a.h, "ncclSend"));
+      a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(a.h, "ncclRecv"));
+      a.ErrStr = reinterpret_cast<decltype(a.ErrStr)>(dlsym(a.h, "ncclGetErrorString"));
+    }
+    return a;
+  }();
+  if (!api.CommInitAll || !api.CommDestroy || !api.GroupStart || !api.GroupEnd || !api.Send ||
+      !api.Recv || !api.ErrStr)
+    throw BlError{BL_CUDA_ERROR, "NCCL (libnccl.so.2) is not available"};
+  return api;
+}
+
+#define NK(call)                                                                    \
+  do {                                                                              \
+    const ncclResult_t _r = (call);                                                 \
+    if (_r != ncclSuccess)                                                          \
+      throw BlError{BL_CUDA_ERROR, std::string(#call) + ": " + nccl_api().ErrStr(_r)}; \
+  } while (0)
+
+// one result record (bl::res_stride layout, decode_kernel.cu finalize) ->
+// DecodeResult fields
+void parse_record(const int* r, int S, bl_results::One& o) {
+  const int nt = r[0];
+  o.steps = r[1];
+  o.trigger = r[2];
+  std::memcpy(&o.joint, r + 4, sizeof(double));
+  o.tokens.assign(r + bl::kResHdr, r + bl::kResHdr + nt);
+  o.label_times.assign(r + bl::kResHdr + S, r + bl::kResHdr + S + nt);
+  for (int k = 0; k < r[3]; ++k) {
+    const int* q = r + bl::kResHdr + 2 * S + k * (4 + 2 * S);
+    double jv;
+    std::memcpy(&jv, q + 2, sizeof(double));
+    o.nb_joint.push_back(jv);
+    o.nb_tokens.emplace_back(q + 4, q + 4 + q[0]);
+    o.nb_times.emplace_back(q + 4 + S, q + 4 + S + q[0]);
+  }
+}
+
+}  // namespace
+
+struct bl_group {
+  std::vector<int> dev;
+  std::vector<bl_decoder*> dec;
+  std::vector<ncclComm_t> comm;
+  DevBuf gather;  // on dev[0]: [devices][rows][record]
+  HostBuf h_gather;
+};
+
+extern "C" {
+
+int bl_group_create(int n_devices, const int* devices, const bl_config* cfg,
+                    const bl_scorer* scorer, bl_group** out) {
+  return guarded([&] {
+    if (n_devices < 1 || !devices) throw std::invalid_argument("group: no devices");
+    if (!scorer) throw std::invalid_argument("scorer is required");
+    if (scorer->kind == 3)
+      throw std::invalid_argument("group: the transformer scorer is bound to one device");
+    std::unique_ptr<bl_group> g(new bl_group);
+    g->dev.assign(devices, devices + n_devices);
+    for (int k = 0; k < n_devices; ++k) {
+      bl_decoder* d = nullptr;
+      const int rc = bl_decoder_create(devices[k], cfg, scorer, &d);
+      if (rc != BL_OK) {
+        for (auto* x : g->dec) bl_decoder_destroy(x);
+        throw BlError{rc, g_err};
+      }
+      g->dec.push_back(d);
+    }
+    const NcclApi& nc = nccl_api();
+    g->comm.resize(n_devices);
+    const ncclResult_t r = nc.CommInitAll(g->comm.data(), n_devices, devices);
+    if (r != ncclSuccess) {
+      for (auto* x : g->dec) bl_decoder_destroy(x);
+      throw BlError{BL_CUDA_ERROR, std::string("ncclCommInitAll: ") + nc.ErrStr(r)};
+    }
+    *out = g.release();
+    return BL_OK;
+  });
+}
+
+int bl_group_size(const bl_group* g) { return (int)g->dev.size(); }
+
+int bl_group_set_options(bl_group* g, int nbest, int exact, double slack) {
+  for (auto* d : g->dec) {
+    const int rc = bl_decoder_set_options(d, nbest, exact, slack);
+    if (rc != BL_OK) return rc;
+  }
+  return BL_OK;
+}
+
+int bl_group_decode(bl_group* g, int n, const bl_utt* utts, bl_results** out) {
+  return guarded([&] {
+    const int G = (int)g->dec.size();
+    auto res = std::make_unique<bl_results>();
+    if (n == 0) {
+      *out = res.release();
+      return BL_OK;
+    }
+    // one record layout for the whole group: step capacity over all segments
+    int S = 1;
+    for (int i = 0; i < n; ++i)
+      S = std::max(S, static_cast<int>(std::ceil(g->dec[0]->cfg.max_steps_ratio *
+                                                 utts[i].num_frames)));
+    const int rs = bl::res_stride(S, std::max(1, g->dec[0]->nbest));
+    std::vector<int> a(G + 1);
+    for (int r = 0; r <= G; ++r) a[r] = (int)((long long)n * r / G);  // contiguous shards
+    int rows = 1;
+    for (int r = 0; r < G; ++r) rows = std::max(rows, a[r + 1] - a[r]);
+    std::vector<bl_results*> part(G, nullptr);
+    std::vector<int> rc(G, BL_OK);
+    std::vector<std::string> msg(G);
+    std::vector<std::thread> th;
+    for (int r = 0; r < G; ++r) {
+      th.emplace_back([&, r] {
+        bl_decoder* d = g->dec[r];
+        d->force_S = S;
+        d->keep_rows = rows;
+        d->memory = nullptr;
+        rc[r] = guarded([&] {
+          CK(cudaSetDevice(d->device));
+          if (a[r + 1] == a[r]) {  // empty shard: a zeroed block keeps the gather uniform
+            d->res.ensure(sizeof(int) * (size_t)rows * rs);
+            CK(cudaMemsetAsync(d->res.p, 0, sizeof(int) * (size_t)rows * rs, d->stream));
+            CK(cudaStreamSynchronize(d->stream));
+            part[r] = new bl_results;
+            return BL_OK;
+          }
+          return decode_impl(d, a[r + 1] - a[r], utts + a[r], 0, &part[r]);
+        });
+        if (rc[r] != BL_OK) msg[r] = g_err;
+        d->force_S = 0;
+        d->keep_rows = 0;
+      });
+    }
+    for (auto& t : th) t.join();
+    for (int r = 0; r < G; ++r)
+      if (rc[r] != BL_OK) {
+        for (auto* p : part) delete p;
+        throw BlError{rc[r], msg[r]};
+      }
+    // ONE NCCL group: every device's records -> device 0
+    const NcclApi& nc = nccl_api();
+    const size_t words = (size_t)rows * rs;
+    CK(cudaSetDevice(g->dev[0]));
+    g->gather.ensure(sizeof(int) * words * G);
+    NK(nc.GroupStart());
+    for (int r = 0; r < G; ++r) {
+      NK(nc.Send(g->dec[r]->res.p, words, ncclInt32, 0, g->comm[r], g->dec[r]->stream));
+      NK(nc.Recv(static_cast<int*>(g->gather.p) + r * words, words, ncclInt32, r, g->comm[0],
+                 g->dec[0]->stream));
+    }
+    NK(nc.GroupEnd());
+    for (int r = 0; r < G; ++r) {
+      CK(cudaSetDevice(g->dev[r]));
+      CK(cudaStreamSynchronize(g->dec[r]->stream));
+    }
+    CK(cudaSetDevice(g->dev[0]));
+    g->h_gather.ensure(sizeof(int) * words * G);
+    CK(cudaMemcpyAsync(g->h_gather.p, g->gather.p, sizeof(int) * words * G,
+                       cudaMemcpyDeviceToHost, g->dec[0]->stream));
+    CK(cudaStreamSynchronize(g->dec[0]->stream));
+    const int* h = static_cast<const int*>(g->h_gather.p);
+    res->r.resize(n);
+    for (int r = 0; r < G; ++r) {
+      for (int i = a[r]; i < a[r + 1]; ++i) {
+        auto& o = res->r[i];
+        o.id = utts[i].id ? utts[i].id : "";
+        parse_record(h + (size_t)r * words + (size_t)(i - a[r]) * rs, S, o);
+        res->max_tokens = std::max(res->max_tokens, (int)o.tokens.size());
+      }
+      const bl_results* p = part[r];
+      res->steps += p->steps;
+      res->queries += p->queries;
+      res->frames += p->frames;
+      res->k1 += p->k1;
+      res->fallback += p->fallback;
+      res->contenders += p->contenders;
+      res->raw_keys += p->raw_keys;
+      res->h2d += p->h2d;
+      res->d2h += p->d2h;
+      res->launches += p->launches;
+      res->kernel_ms = std::max(res->kernel_ms, p->kernel_ms);
+      delete p;
+    }
+    res->d2h += sizeof(int) * words * G;
+    *out = res.release();
+    return BL_OK;
+  });
+}
+
+void bl_group_destroy(bl_group* g) {
+  if (!g) return;
+  for (size_t r = 0; r < g->comm.size(); ++r) {
+    if (!g->comm[r]) continue;
+    cudaSetDevice(g->dev[r]);
+    nccl_api().CommDestroy(g->comm[r]);
+  }
+  for (auto* d : g->dec) bl_decoder_destroy(d);
+  cudaSetDevice(g->dev[0]);  // the gather buffer lives on the first device
+  delete g;
 }
 
 }  // extern "C"

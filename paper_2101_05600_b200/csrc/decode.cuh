@@ -79,9 +79,9 @@ struct KParams {
   double* gam;     // [U][2][caps][2][Tp]
   double* Ftab;    // [U][Tp][C]   eos tail tables (need_tail only)
   double* Gtab;    // [U][Tp]
-  float* kubg;     // [U][B][C]    certified upper keys when they do not fit in smem
-  unsigned* ubitsg;  // [U][(B*C+31)/32] underflow-key flags (with kubg)
-  int kub_smem;    // 1: upper keys live in shared memory
+  int kub_smem;    // 1: every upper key lives in shared memory (P5 scans them);
+                   // 0: keys are filtered on chip against a running bound
+                   // while P3 emits them (raw list, kRawCap entries)
   int region_bytes;  // aliased smem region (see smem_plan)
   double* xs;      // [U][B][C+1]  exact joints (fallback path)
   unsigned char* taken;  // [U][B][C+1]
@@ -114,10 +114,11 @@ struct KParams {
 
 // Dynamic shared-memory plan (identical on host and device).
 constexpr int kListCap = 256;  // keys reaching theta0 (P5), 16 B each
+constexpr int kRawCap = 512;   // keys reaching the running bound during P3 (filter mode)
 
 struct SmemPlan {
   size_t phi, region, items, bbl, total;
-  size_t phif, kub, ubits, clist, stages, region_need;  // P3-P5 view of `region`
+  size_t phif, kub, ubits, clist, raw, stages, region_need;  // P3-P5 view of `region`
 };
 constexpr int kItemBytes = 24;  // score(double) + parent, token, tau, taut
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
@@ -134,12 +135,27 @@ __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, 
   p.kub = align16(sizeof(float) * (size_t)Tmax * bmax);
   const size_t words = ((size_t)B * C + 31) / 32;
   p.ubits = kub_smem ? align16(p.kub + sizeof(float) * (size_t)B * C) : p.kub;
-  p.clist = kub_smem ? align16(p.ubits + sizeof(unsigned) * words) : p.kub;
-  // TMA stages (kub/ubits then live in HBM): after the list, 128-byte
-  // aligned in absolute shared-memory offset (cp.async.bulk.tensor dst)
-  p.stages = ((p.region + p.clist + 16 * (size_t)kListCap + 127) & ~(size_t)127) - p.region;
-  p.region_need = tma_stages ? p.stages + (size_t)tma_stages * kTmaStageBytes
-                             : p.clist + 16 * (size_t)kListCap;
+  if (kub_smem) {  // keys mode: every key, its flag, then the theta0 list
+    p.clist = align16(p.ubits + sizeof(unsigned) * words);
+    p.raw = p.clist + 16 * (size_t)kListCap;
+    p.stages = p.raw;
+    p.region_need = p.raw;
+  } else {
+    // filter mode: the raw list (8 B per key: upper key + packed index),
+    // then the TMA stages, 128-byte aligned in absolute shared-memory offset
+    // (cp.async.bulk.tensor dst); the theta0 list is built after P3, so with
+    // TMA it takes the stage area, else it follows the raw list
+    p.raw = p.kub;
+    const size_t raw_end = p.raw + 8 * (size_t)kRawCap;
+    p.stages = ((p.region + raw_end + 127) & ~(size_t)127) - p.region;
+    if (tma_stages) {
+      p.clist = p.stages;
+      p.region_need = p.stages + (size_t)tma_stages * kTmaStageBytes;
+    } else {
+      p.clist = align16(raw_end);
+      p.region_need = p.clist + 16 * (size_t)kListCap;
+    }
+  }
   p.items = align16(p.region + region_bytes);
   p.bbl = align16(p.items + (size_t)kItemBytes * (caps + bmax));
   p.total = align16(p.bbl + sizeof(double) * (size_t)(S + 2));

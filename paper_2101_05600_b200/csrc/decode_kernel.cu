@@ -111,6 +111,29 @@ __device__ __forceinline__ float warp_max_f(float v) {
 
 constexpr float kZeroKey = -3.0e38f;  // key of a joint that is exactly kLogZero
 
+// order-preserving float <-> int map (shared-memory atomicMax on floats)
+__device__ __forceinline__ int f2ord(float f) {
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float ord2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+// k-th largest (0-based) of the 32 lanes' values: bitonic sort, descending
+// (whole warp)
+__device__ __forceinline__ float warp_kth_desc(float v, int k, int lane) {
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const float o = __shfl_xor_sync(0xffffffffu, v, stride);
+      const bool desc = (lane & size) == 0;
+      const bool lower = (lane & stride) == 0;
+      v = (lower == desc) ? fmaxf(v, o) : fminf(v, o);
+    }
+  }
+  return __shfl_sync(0xffffffffu, v, k);
+}
+
 // ------------------------------------------------------- TMA / mbarrier PTX
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -181,7 +204,8 @@ struct Shared {
   double best_all, best_fin_val, off;
   float theta, theta2;
   int n_list;
-  unsigned long long c_queries, c_frames, c_k1, c_fallback, c_cont, c_steps;
+  int th_run, n_raw;  // filter mode: running bound (f2ord) and raw-list size
+  unsigned long long c_queries, c_frames, c_k1, c_fallback, c_cont, c_steps, c_raw;
 };
 
 __device__ __forceinline__ double* gam_ptr(const KParams& P, int u, int area,
@@ -371,13 +395,18 @@ __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
     prof_t = _now;                                     \
   }
 
-template <int BMAX, bool kTma>
-__global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
+// kMode 0: K1 slab by __ldg, every upper key in shared memory (keys mode);
+// 1: __ldg, keys filtered on chip (filter mode); 2: TMA slab, filter mode
+template <int BMAX, int kMode>
+__global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
     decode_kernel(const __grid_constant__ KParams P) {
+  constexpr bool kTma = kMode == 2;
+  constexpr bool keys_mode = kMode == 0;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ Shared<BMAX> sh;
   __shared__ SpTables tb;
   __shared__ __align__(8) unsigned long long mbar[kTmaStagesMax];
+  __shared__ int cons[kTmaStagesMax];  // warps done with each TMA stage (monotonic)
 
   const int u = blockIdx.x + P.u0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -389,16 +418,19 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
   long long prof_t = clock64();
 
   // dynamic smem carve-up (smem_plan, decode.cuh)
-  const SmemPlan pl = smem_plan(P.Tmax, B, BMAX, C, P.caps, P.S, P.region_bytes, P.kub_smem);
+  const SmemPlan pl = smem_plan(P.Tmax, B, BMAX, C, P.caps, P.S, P.region_bytes, P.kub_smem,
+                                kTma ? P.tma_stages : 0);
   double* phi = reinterpret_cast<double*>(dsm + pl.phi);    // [B][Tmax]
   unsigned char* region = dsm + pl.region;                  // aliased, region_bytes
   float* PhiF = reinterpret_cast<float*>(region + pl.phif);  // [Tmax][BMAX]
-  float* kub = P.kub_smem ? reinterpret_cast<float*>(region + pl.kub)
-                          : P.kubg + (size_t)u * B * C;      // [B][C]
+  // keys mode (kub_smem): every upper key and its underflow flag in shared
+  // memory, scanned by P5; filter mode: keys reaching the running bound go
+  // to the raw list as P3 emits them
+  float* kub = reinterpret_cast<float*>(region + pl.kub);          // [B][C]
   const int ub_words = (B * C + 31) >> 5;
-  unsigned* ubits = P.kub_smem ? reinterpret_cast<unsigned*>(region + pl.ubits)
-                               : P.ubitsg + (size_t)u * ub_words;  // underflow-key flags
+  unsigned* ubits = reinterpret_cast<unsigned*>(region + pl.ubits);  // underflow-key flags
   float4* clist = reinterpret_cast<float4*>(region + pl.clist);    // [kListCap]
+  uint2* rawl = reinterpret_cast<uint2*>(region + pl.raw);         // [kRawCap] {ku, under|q|c}
   const int caps = P.caps;
   Item* items = reinterpret_cast<Item*>(dsm + pl.items);     // [caps + BMAX], eos at caps
   double* best_by_len = reinterpret_cast<double*>(dsm + pl.bbl);    // [S+2]
@@ -415,7 +447,10 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
   unsigned char* st_u = stepm ? P.state + (size_t)u * P.state_stride : nullptr;
   if (stepm && P.step_l > 1 && *reinterpret_cast<volatile int*>(st_u)) return;  // finished
   if (kTma && tid == 0) {
-    for (int k = 0; k < P.tma_stages; ++k) mbar_init(&mbar[k], 1);
+    for (int k = 0; k < P.tma_stages; ++k) {
+      mbar_init(&mbar[k], 1);
+      cons[k] = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < 320; i += kNT)
@@ -500,6 +535,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     sh.trigger = 2;
     sh.steps = 0;
     sh.c_queries = sh.c_frames = sh.c_k1 = sh.c_fallback = sh.c_cont = sh.c_steps = 0;
+    sh.c_raw = 0;
     sh.b_row[0][0] = P.net_rows ? u * B : lookup_row(P, hist_c, 0, 0, 0, 0);
   }
   __syncthreads();
@@ -573,6 +609,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
         sh.c_k1 += 4ull * V * W + 16ull * nb * (W + 1) + 4ull * nb * V;
         sh.n_cont = 0;
         sh.fallback = P.exact;
+        sh.th_run = f2ord(-INFINITY);
+        sh.n_raw = 0;
       }
     }
     __syncthreads();
@@ -653,7 +691,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           const int i = idx / pad, j = nb + (idx - i * pad);
           PhiF[(size_t)i * BMAX + j] = 0.f;
         }
-        for (int idx = tid; idx < ub_words; idx += kNT) ubits[idx] = 0u;
+        if (keys_mode)
+          for (int idx = tid; idx < ub_words; idx += kNT) ubits[idx] = 0u;
       }
     }
     __syncthreads();
@@ -668,6 +707,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       // top-2 certified lower bounds (theta0, P4), the exact theta comes from
       // the short list of keys that reach theta0 (P5).
       float l1 = -INFINITY, l2 = -INFINITY;
+      float lcol = -INFINITY;  // filter mode: best column's worst-parent lower bound
       const float hw = (float)(lam * (P.dpsi0 + W * P.dpsi1)) + 1e-4f;
       const float gf = P.guard_f;
       const int row_same = sh.row_same;
@@ -725,8 +765,19 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       int klam_pos = lam > 0.0 ? 1 : 0;
       asm volatile("" : "+f"(klamf), "+f"(kgf), "+r"(klam_pos));
       const bool lam_pos = klam_pos != 0;
+      // Keys of one column pair: certified bounds. Pass 1 keeps the thread's
+      // top-2 lower bounds (and in keys mode writes every upper key and its
+      // underflow flag to shared memory for the P5 scan). Filter mode then
+      // runs pass 2 (emit == true) after the warp's running bound is known:
+      // the same keys are recomputed (identical arithmetic) and those whose
+      // upper bound reaches the bound go to the raw list.
       auto emit_keys = [&](int c0, bool two, const float2(&S0)[kP], const float2(&S1)[kP],
-                           float m0, float m1, float r0s, float r1s) {
+                           float m0, float m1, float r0s, float r1s, bool emit, float th,
+                           float& kmax) {
+        // filter mode, pass 1: min over the parents of each column's lower
+        // bounds (with B live parents, B distinct candidates reach it), and
+        // the largest upper key (pass 2 is skipped when it misses the bound)
+        float cmin0 = INFINITY, cmin1 = INFINITY;
 #pragma unroll
         for (int q = 0; q < BMAX; ++q) {
           if (q < nb) {
@@ -760,21 +811,60 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
                   klo = kub_v = kZeroKey;
                   under = false;
                 }
-                if (klo > l2) {
-                  if (klo > l1) {
-                    l2 = l1;
-                    l1 = klo;
-                  } else {
-                    l2 = klo;
+                if (!emit) {
+                  kmax = fmaxf(kmax, kub_v);
+                  if (cc) cmin1 = fminf(cmin1, klo);
+                  else cmin0 = fminf(cmin0, klo);
+                  if (klo > l2) {
+                    if (klo > l1) {
+                      l2 = l1;
+                      l1 = klo;
+                    } else {
+                      l2 = klo;
+                    }
                   }
+                } else if (kub_v >= th) {
+                  const int idx = atomicAdd(&sh.n_raw, 1);
+                  if (idx < kRawCap)
+                    rawl[idx] = make_uint2(__float_as_uint(kub_v),
+                                           (under ? 0x80000000u : 0u) | ((unsigned)q << 24) |
+                                               (unsigned)c);
                 }
               }
-              const int kidx = q * C + c;
-              kub[kidx] = kub_v;
-              if (under) atomicOr(&ubits[kidx >> 5], 1u << (kidx & 31));
+              if (keys_mode) {
+                const int kidx = q * C + c;
+                kub[kidx] = kub_v;
+                if (under) atomicOr(&ubits[kidx >> 5], 1u << (kidx & 31));
+              }
+              if (c == last) {  // the repeat column is scored exactly: no bound from it
+                if (cc) cmin1 = -INFINITY;
+                else cmin0 = -INFINITY;
+              }
             }
           }
         }
+        if (!keys_mode && !emit && nb >= B)
+          lcol = fmaxf(lcol, fmaxf(cmin0, two ? cmin1 : -INFINITY));
+      };
+      // Filter mode (whole warp, after a column tile's pass 1): the B-th
+      // largest of the lanes' best lower bounds is a valid lower bound on
+      // theta0 (B distinct candidates reach it), so the block-wide running
+      // maximum of these bounds only rises towards theta0; a key whose upper
+      // bound is below it can never reach theta0 and is dropped.
+      // Three valid bounds, the best taken: the B-th best of the lanes' best
+      // keys (spread-out candidates), the ceil(B/2)-th best of their second
+      // best, and the best column whose B parents all reach a value
+      // (clustered candidates: near-equal parents share their best tokens).
+      // The two sorts run on the first tiles and every fourth after (`full`):
+      // the running bound is near theta0 by then and only rises.
+      auto warp_bound = [&](bool full) -> float {
+        float wb = warp_max_f(lcol);
+        if (full)
+          wb = fmaxf(wb, fmaxf(warp_kth_desc(l1, B - 1, lane),
+                               warp_kth_desc(l2, (B - 1) >> 1, lane)));
+        if (lane == 0) atomicMax(&sh.th_run, f2ord(wb));
+        __syncwarp();
+        return fmaxf(wb, ord2f(*reinterpret_cast<volatile int*>(&sh.th_run)));
       };
       if constexpr (kTma) {
         // K1 slab streamed by TMA: job j = (512-column tile, kTmaRows-row
@@ -850,25 +940,44 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
                 acc(S1, m1, v.y, phr + (f0 + i) * phs);
               }
             }
-            if (k == nch - 1) emit_keys(c0, two, S0, S1, m0, two ? m1 : gf, r0s, r1s);
           }
-          __syncthreads();  // stage consumed by every thread
-          if (tid == 0 && j + NST < J) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(j + NST, g + NST);
+          // stage release per warp: the warp that finishes it last refills
+          // it (no block barrier; the other warps stream on)
+          __syncwarp();
+          if (lane == 0) {
+            __threadfence_block();
+            const int done = atomicAdd(&cons[st], 1);
+            if (done == (int)(g / (unsigned)NST) * kNWarp + kNWarp - 1 && j + NST < J) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              issue(j + NST, g + NST);
+            }
+          }
+          if (k == nch - 1) {  // the tile's keys (whole warp: warp_bound)
+            float kmax = -INFINITY;
+            if (active)
+              emit_keys(c0, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, false, 0.f, kmax);
+            const float th = warp_bound(tile < 3 || (tile & 3) == 0);
+            if (active && kmax >= th)
+              emit_keys(c0, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, true, th, kmax);
           }
         }
         tma_jobs += J;
       } else {
-      for (int c0 = 2 * tid; c0 < C; c0 += 2 * kNT) {
-        const long long tq1 = clock64();
-        const bool two = c0 + 1 < C;
+      // warp-uniform trip count (warp_bound is a warp collective); thread
+      // tid still owns columns 2 * tid + k * 2 * kNT
+      for (int cb = 64 * warp; cb < C; cb += 2 * kNT) {
+        const int c0 = cb + 2 * lane;
+        const bool act = c0 < C;
+        float kmax = -INFINITY;
         float2 S0[kP], S1[kP];
+        float m0 = gf, m1 = gf, r0s = 0.f, r1s = 0.f;
+        const bool two = c0 + 1 < C;
 #pragma unroll
         for (int q = 0; q < kP; ++q) S0[q] = S1[q] = make_float2(0.f, 0.f);
-        float m0 = gf, m1 = gf;
-        const float r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
-        const float r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
+        if (act) {
+        const long long tq1 = clock64();
+        r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
+        r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
         const float* col = grid + (size_t)(s - 1) * V + c0;
         // columns c0 and c0+1 are both inside the row (c0 + 1 <= C = V-1,
         // the blank), so the pair is always loaded (the odd column of an odd
@@ -926,8 +1035,14 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
         if (!two) m1 = gf;
         const long long tq2 = clock64();
         tq_frames += tq2 - tq1;
-        emit_keys(c0, two, S0, S1, m0, m1, r0s, r1s);
+        emit_keys(c0, two, S0, S1, m0, m1, r0s, r1s, false, 0.f, kmax);
         tq_keys += clock64() - tq2;
+        }
+        if (!keys_mode) {
+          const int it = cb / (2 * kNT);
+          const float th = warp_bound(it < 3 || (it & 3) == 0);
+          if (act && kmax >= th) emit_keys(c0, two, S0, S1, m0, m1, r0s, r1s, true, th, kmax);
+        }
       }
       }
       if (P.prof && tid == 0) {
@@ -995,7 +1110,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
         list_key_qc(kidx, q, kidx - q * C, ku);
       };
       const int nkeys = nb * C;
-      if (P.kub_smem && C >= kNT) {
+      if (keys_mode && C >= kNT) {
         // (q, c) of kidx kept incrementally (stride kNT <= C: at most one wrap)
         int q = 0, c = tid;
         for (int kidx = tid; kidx < nkeys; kidx += kNT) {
@@ -1007,25 +1122,34 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
             ++q;
           }
         }
-      } else if (P.kub_smem) {
+      } else if (keys_mode) {
         for (int kidx = tid; kidx < nkeys; kidx += kNT) {
           const float ku = kub[kidx];
           if (ku >= theta0) list_key(kidx, ku);
         }
       } else {
-        // upper keys in HBM: kScan independent loads per thread before any
-        // test (one dependent load per key would serialise their latency)
-        constexpr int kScan = 8;
-        for (int k0 = tid; k0 < nkeys; k0 += kScan * kNT) {
-          float ku[kScan];
-#pragma unroll
-          for (int r = 0; r < kScan; ++r) {
-            const int kidx = k0 + r * kNT;
-            ku[r] = kidx < nkeys ? kub[kidx] : -INFINITY;
+        // filter mode: the raw list holds every key that reached the running
+        // bound (a superset of the keys reaching theta0); keep those that
+        // reach theta0. A raw-list overflow falls back like a list overflow.
+        const int nraw = sh.n_raw;
+        if (tid == 0) sh.c_raw += nraw;
+        if (nraw > kRawCap) {
+          if (tid == 0) sh.n_list = kListCap + 1;
+        } else {
+          for (int k = tid; k < nraw; k += kNT) {
+            const uint2 e2 = rawl[k];
+            const float ku = __uint_as_float(e2.x);
+            if (ku >= theta0) {
+              const int idx = atomicAdd(&sh.n_list, 1);
+              if (idx < kListCap) {
+                // derived lower bound: the one the keys-mode P5 scan lists
+                clist[idx] = make_float4(
+                    (e2.y >> 31) ? -INFINITY : ku - 2.000002f * (hw + (fabsf(ku) + hw) * 2.4e-7f),
+                    ku, __int_as_float((int)((e2.y >> 24) & 0x7fu)),
+                    __int_as_float((int)(e2.y & 0xffffffu)));
+              }
+            }
           }
-#pragma unroll
-          for (int r = 0; r < kScan; ++r)
-            if (ku[r] >= theta0) list_key(k0 + r * kNT, ku[r]);
         }
       }
       __syncthreads();
@@ -1089,7 +1213,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
       float* stL = reinterpret_cast<float*>(region);
       float* stB = reinterpret_cast<float*>(region + offB);
       double* stR = reinterpret_cast<double*>(region + offR);
-      if (staged) {
+      if (staged && keys_mode) {  // small windows (80-register variant)
         for (int idx = tid; idx < (nc + 1) * W; idx += kNT) {
           const int q = idx / W, i = idx - q * W;
           const int c = q < nc ? items[q].token : blank;
@@ -1102,6 +1226,50 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
           if (sh.b_last[cur][j] < 0) continue;
           const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
           stR[idx] = gread(gbp, s + i - 1, sh.b_vlo[cur][j], sh.b_cov[cur][j]);
+        }
+      } else if (staged) {
+        // kSt independent loads per thread in flight before any store (the
+        // columns are scattered rows apart in HBM: one load at a time would
+        // serialise their latency)
+        constexpr int kSt = 4;
+        const int ntot = (nc + 1) * W;
+        for (int base = tid; base < ntot; base += kSt * kNT) {
+          float v[kSt];
+#pragma unroll
+          for (int r = 0; r < kSt; ++r) {
+            const int idx = base + r * kNT;
+            if (idx < ntot) {
+              const int q = idx / W, i = idx - q * W;
+              const int c = q < nc ? items[q].token : blank;
+              v[r] = grid[(size_t)(s - 1 + i) * V + c];
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < kSt; ++r) {
+            const int idx = base + r * kNT;
+            if (idx < ntot) {
+              if (idx < nc * W) stL[idx] = v[r];
+              else stB[idx - nc * W] = v[r];
+            }
+          }
+        }
+        const int rtot = nb * W;
+        for (int base = tid; base < rtot; base += kSt * kNT) {
+          double v[kSt];
+#pragma unroll
+          for (int r = 0; r < kSt; ++r) {
+            const int idx = base + r * kNT;
+            const int j = idx / W, i = idx - j * W;
+            if (idx < rtot && sh.b_last[cur][j] >= 0) {
+              const double* gbp = gam_ptr(P, u, sh.b_area[cur][j], sh.b_slot[cur][j], 1);
+              v[r] = gread(gbp, s + i - 1, sh.b_vlo[cur][j], sh.b_cov[cur][j]);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < kSt; ++r) {
+            const int idx = base + r * kNT;
+            if (idx < rtot && sh.b_last[cur][idx / W] >= 0) stR[idx] = v[r];
+          }
         }
       }
       __syncthreads();
@@ -1420,9 +1588,11 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     }
     // the patch is warp 0's (nchild <= BMAX <= 32) and only warp 0 reads
     // tau before the next block barrier (P1), so a warp barrier suffices
-    // unless the state is saved now (step mode) or the search ends
+    // unless the state is saved now (step mode) or the search ends (end
+    // detection, or the step bound: the next iteration breaks before P1 and
+    // finalize reads the history with every warp)
     if (gw0 > 0) {
-      if (stepm || sh.done) __syncthreads();
+      if (stepm || sh.done || l >= ud.max_steps) __syncthreads();
       else __syncwarp();
     }
     PROF_MARK(10);
@@ -1509,7 +1679,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && !kTma ? 3 : 2))
     cn[3] = sh.c_k1;
     cn[4] = sh.c_fallback;
     cn[5] = sh.c_cont;
-    cn[6] = 0;
+    cn[6] = sh.c_raw;
     cn[7] = 0;
   }
   // n-best over finished entries: (joint desc, insertion asc)
@@ -1612,30 +1782,34 @@ size_t decode_smem_bytes(const KParams& p) {
                    p.tma_stages).total;
 }
 
-template <int BMAX, bool kTma>
+static int mode_of(const KParams& p) { return p.use_tma ? 2 : (p.kub_smem ? 0 : 1); }
+
+template <int BMAX, int kMode>
 static cudaError_t launch_v(const KParams& p, cudaStream_t st) {
   const size_t sm = decode_smem_bytes(p);
-  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX, kTma>,
+  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX, kMode>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)sm);
   if (err != cudaSuccess) return err;
   if (std::getenv("BL_DEBUG")) {
     int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decode_kernel<BMAX, kTma>, kNT, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decode_kernel<BMAX, kMode>, kNT, sm);
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, decode_kernel<BMAX, kTma>);
+    cudaFuncGetAttributes(&fa, decode_kernel<BMAX, kMode>);
     std::fprintf(stderr, "[bl] decode_kernel<%d,%d>: grid %d, dyn smem %zu, static %zu, regs %d, %d CTA/SM\n",
-                 BMAX, (int)kTma, p.U, sm, fa.sharedSizeBytes, fa.numRegs, nb);
+                 BMAX, kMode, p.U, sm, fa.sharedSizeBytes, fa.numRegs, nb);
   }
-  decode_kernel<BMAX, kTma><<<p.U, kNT, sm, st>>>(p);
+  decode_kernel<BMAX, kMode><<<p.U, kNT, sm, st>>>(p);
   return cudaGetLastError();
 }
 
 template <int BMAX>
 static size_t static_smem_t(const KParams& p) {
   cudaFuncAttributes fa{};
-  if (p.use_tma) cudaFuncGetAttributes(&fa, decode_kernel<BMAX, true>);
-  else cudaFuncGetAttributes(&fa, decode_kernel<BMAX, false>);
+  const int m = mode_of(p);
+  if (m == 2) cudaFuncGetAttributes(&fa, decode_kernel<BMAX, 2>);
+  else if (m == 1) cudaFuncGetAttributes(&fa, decode_kernel<BMAX, 1>);
+  else cudaFuncGetAttributes(&fa, decode_kernel<BMAX, 0>);
   return fa.sharedSizeBytes;
 }
 
@@ -1654,7 +1828,9 @@ size_t decode_static_smem(const KParams& p) {
 
 template <int BMAX>
 static cudaError_t launch_t(const KParams& p, cudaStream_t st) {
-  return p.use_tma ? launch_v<BMAX, true>(p, st) : launch_v<BMAX, false>(p, st);
+  const int m = mode_of(p);
+  return m == 2 ? launch_v<BMAX, 2>(p, st) : m == 1 ? launch_v<BMAX, 1>(p, st)
+                                               : launch_v<BMAX, 0>(p, st);
 }
 
 cudaError_t launch_decode(const KParams& p, cudaStream_t st) {

@@ -34,8 +34,7 @@ def recognize(fbank: np.ndarray, encoder: Encoder, decoder: Decoder,
     T = fb.shape[0]
     segs = list(segments) if segments is not None else \
         hard_segments(T, min_len, max_len, recording_id)
-    attn = hasattr(decoder.scorer, "spec") and decoder.scorer.__class__.__name__ == \
-        "TransformerScorer"
+    attn = getattr(decoder.scorer, "is_network", False)
     groups: dict = {}
     for i, s in enumerate(segs):
         groups.setdefault(s.end - s.start, []).append(i)

@@ -114,6 +114,7 @@ class TransformerScorer(Scorer):
         self._h = h
         self._n = spec.vocab - 1
         self.spec = spec
+        self.is_network = True
 
     def score(self, utterance_id, prefix):  # no host-side query for the network
         raise NotImplementedError("the Transformer scorer runs on device inside the decoder")

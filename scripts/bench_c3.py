@@ -19,7 +19,7 @@ descs = [(f"c{i}", 249, V, g[i].data_ptr()) for i in range(n)]
 for _ in range(2):
     dec.decode_raw(descs, on_device=True)
 st = dec.last_stats
-print({k: st[k] for k in ("kernel_ms", "k1_bytes", "fallback_steps", "contenders", "steps")})
+print({k: st[k] for k in ("kernel_ms", "k1_bytes", "fallback_steps", "contenders", "steps", "filter_keys")})
 print("K1 GB/s %.1f  audio-s/s %.0f" % (st["k1_bytes"] / st["kernel_ms"] / 1e6, n * 9.96 / (st["kernel_ms"] / 1e3)))
 if os.environ.get("BL_PROFILE"):
     names = ["init", "P1", "P2", "P3", "P4", "P5", "P6", "P7", "fb", "P8", "P9", "fin", "t0:P3fr", "t0:P3keys", "t0:P6ser", "t0:P6stg"]

@@ -1,0 +1,85 @@
+"""Parity at the exact decode shape the bench headline times (BASELINE
+config 3 / config 4 per segment): T_enc = 249, vocab 5000, beam 10,
+DecoderConfig defaults (lambda 0.3, M1 5, M2 unbounded, eos both), decoded
+by the TMA slab variant with on-chip key filtering, against results of the
+UNMODIFIED reference compiled here (tests/golden/c3_expected.json, made by
+tests/golden/make_c3_golden.py with oracle/_ref; grids regenerated from
+seeds, sha256-checked). Fast (certified fp32 bulk), exact (fp64 decisions)
+and step-granular modes; host grids and HBM-resident grids; the counters
+equal the reference's. The 'dupcols' segment (32 identical high-mass token
+columns) ties hundreds of candidates, so the contender set overflows and the
+exact fallback runs on some steps (fallback_steps > 0)."""
+import json
+import os
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2101_05600_b200 as bl
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "golden"))
+from c3_grids import V, c3_grids, digest  # noqa: E402
+
+TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def c3():
+    with open(os.path.join(HERE, "golden", "c3_expected.json")) as f:
+        exp = json.load(f)
+    items = c3_grids()
+    assert digest(items) == exp["sha256"], "seeded C3 grids drifted from the golden run"
+    return exp, items
+
+
+def test_c3_golden_is_pinned(c3):
+    """CPU: the golden file matches its grids and the reference counters
+    (ctc_frames_evaluated = sum over steps of |C| * W per hypothesis)."""
+    exp, items = c3
+    assert len(exp["results"]) == len(items) == 10
+    assert exp["counters"]["ctc_frames_evaluated"] > 0
+
+
+def _check(got, exp):
+    bad = []
+    for g, w in zip(got, exp["results"]):
+        if (g.id != w["id"] or g.tokens != w["tokens"] or g.label_times != w["label_times"]
+                or g.steps_taken != w["steps"] or g.eos_trigger != w["eos_trigger"]
+                or abs(g.joint_logp - w["joint_logp"]) > TOL):
+            bad.append((g.id, g.tokens[:5], w["tokens"][:5], g.joint_logp, w["joint_logp"]))
+    assert not bad, bad[:3]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["fast", "exact", "step"])
+def test_c3_shape_vs_reference(c3, mode):
+    exp, items = c3
+    dec = bl.Decoder(bl.UniformScorer(V - 1), bl.DecoderConfig(beam_width=10),
+                     exact=mode == "exact", step_mode=mode == "step")
+    cnt = bl.DecodeCounters()
+    got = dec.decode([bl.Utterance(u, bl.PosteriorGrid(g)) for u, g in items], cnt)
+    _check(got, exp)
+    assert (cnt.steps, cnt.scorer_queries, cnt.ctc_frames_evaluated) == \
+        (exp["counters"]["steps"], exp["counters"]["scorer_queries"],
+         exp["counters"]["ctc_frames_evaluated"])
+    if mode == "fast":
+        st = dec.last_stats
+        assert st["fallback_steps"] > 0, st  # dupcols forces the exact fallback
+        assert st["fallback_steps"] < st["steps"] // 4, st
+
+
+@pytest.mark.gpu
+def test_c3_shape_device_resident(c3):
+    """The bench's layout: every grid in one dense HBM buffer (TMA map over
+    all rows), decoded from device pointers."""
+    torch = pytest.importorskip("torch")
+    exp, items = c3
+    g = torch.from_numpy(np.stack([x for _, x in items])).cuda()
+    dec = bl.Decoder(bl.UniformScorer(V - 1), bl.DecoderConfig(beam_width=10))
+    stride = g.shape[1] * V * 4
+    torch.cuda.synchronize()
+    got = list(dec.decode_raw([(u, g.shape[1], V, g.data_ptr() + i * stride)
+                               for i, (u, _) in enumerate(items)], on_device=True))
+    _check(got, exp)

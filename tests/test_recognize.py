@@ -68,3 +68,41 @@ def test_recognize_vad_segments():
     out = recognize(_recording(T), e, dec, segments=segs)
     assert [s for s, _ in out] == segs
     assert all(r.steps_taken >= 1 for _, r in out)
+
+
+def test_model_file_and_native_chain(tmp_path):
+    """BLM1 model file (bl_model_save): the encoder loaded from it and the
+    decoder loaded through the reference's model-load hook
+    (make_scorer("transformer:PATH"), scorer.hpp:84) decode a long recording
+    through the native chain (bl_recognize) exactly like the in-memory
+    weights through the Python chain (recognize.py)."""
+    from paper_2101_05600_b200 import model as bm
+    ew, dw = enc.random_weights(ESPEC, seed=11), tr.random_weights(DSPEC, seed=12)
+    path = str(tmp_path / "m.blm")
+    bm.save_model(path, ESPEC, ew, DSPEC, dw)
+    fb = _recording(3100, seed=13)
+    kw = dict(beam_width=4, margin_m2=15)
+    want = recognize(fb, enc.Encoder(ESPEC, ew),
+                     bl.Decoder(tr.TransformerScorer(DSPEC, dw), bl.DecoderConfig(**kw)),
+                     "m", 600, 800)
+    e2 = bm.load_encoder(path)
+    sc2 = bl.make_scorer("transformer:" + path, DSPEC.vocab - 1)
+    got = bm.recognize_native(fb, e2, bl.Decoder(sc2, bl.DecoderConfig(**kw)), "m", 600, 800)
+    assert [r.id for r in got] == [r.id for _, r in want]
+    for g, (_, w) in zip(got, want):
+        assert g.tokens == w.tokens and g.label_times == w.label_times
+        assert g.steps_taken == w.steps_taken and abs(g.joint_logp - w.joint_logp) <= 1e-9
+    with pytest.raises(RuntimeError, match="vocabulary"):
+        bl.make_scorer("transformer:" + path, 99)
+
+
+def test_native_chain_uniform_equals_python_chain():
+    fb = _recording(5200, seed=14)
+    e = enc.Encoder(ESPEC, enc.random_weights(ESPEC, seed=15))
+    kw = dict(beam_width=5, margin_m2=15)
+    from paper_2101_05600_b200 import model as bm
+    want = recognize(fb, e, bl.Decoder(bl.UniformScorer(63), bl.DecoderConfig(**kw)), "t")
+    got = bm.recognize_native(fb, e, bl.Decoder(bl.UniformScorer(63), bl.DecoderConfig(**kw)),
+                              "t")
+    assert [(r.id, r.tokens, r.joint_logp) for r in got] == \
+        [(r.id, r.tokens, r.joint_logp) for _, r in want]

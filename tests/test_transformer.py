@@ -76,12 +76,16 @@ def _decode(grid, mem, scorer, cfg, record=True, nbest=1):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("beam", [1, 4, 10, 16, 20])
-def test_transformer_rows_vs_torch(beam):
+@pytest.mark.parametrize("beam,frames", [(1, 200), (4, 200), (10, 200), (16, 200), (20, 200),
+                                         (10, 1000), (20, 1000)])
+def test_transformer_rows_vs_torch(beam, frames):
     """beam <= 16: union-of-ancestors self-attention (mma.sync); beam 20:
-    the per-hypothesis warp kernel (csrc/decoder_net.cu use_union_self_attn)."""
+    the per-hypothesis warp kernel (csrc/decoder_net.cu use_union_self_attn).
+    1000 frames (T2 = 249 memory rows, 128 per stage): the staged source
+    attention runs several stages per warp with the cross-warp merge, and the
+    self-attention union list spans several stages late in the decode."""
     from torch_decoder import decoder_scores
-    grid, mem, w = _setup(TINY_ENC, TINY_DEC, 3, 200, seed=5)
+    grid, mem, w = _setup(TINY_ENC, TINY_DEC, 3, frames, seed=5)
     sc = tr.TransformerScorer(TINY_DEC, w)
     dec, res, ids = _decode(grid, mem, sc, bl.DecoderConfig(beam_width=beam))
     recs = dec.records()
