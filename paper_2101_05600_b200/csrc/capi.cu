@@ -238,7 +238,7 @@ struct bl_decoder {
   int sc_order = 1, sc_nent = 0, sc_w = 1;
   DevBuf sc_ctx_len, sc_ctx, sc_row, sc_rows, sc_rowsf;
   // workspace
-  DevBuf grid, utts, gam, Ftab, Gtab, xs, taken, hist, fin, res, cnt, prof;
+  DevBuf grid, utts, gam, Ftab, Gtab, mshift, xs, taken, hist, fin, res, cnt, prof;
   HostBuf h_grid, h_utts, h_res, h_cnt, h_prof;
   bool profile = getenv("BL_PROFILE") != nullptr;
   // step-granular decoding (forced for tests, or required by a network scorer)
@@ -526,9 +526,12 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   // device pointers) with 16-byte rows.
   const float* gbase = nullptr;
   bool use_tma = V >= 1024 && V % 4 == 0 && std::getenv("BL_NO_TMA") == nullptr;
+  // the 3D tensor map of the tensor-core variant reads whole 32-column
+  // blocks: up to 31 floats past the last row (a pad for our own buffer)
+  const size_t gpad = 128;
   if (use_tma) {
     if (!on_device) {
-      d->grid.ensure(sizeof(float) * gtotal);
+      d->grid.ensure(sizeof(float) * gtotal + gpad);
       gbase = static_cast<const float*>(d->grid.p);
     } else {
       gbase = utts[0].logp;
@@ -536,18 +539,52 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     }
     use_tma = use_tma && (reinterpret_cast<uintptr_t>(gbase) & 15) == 0;
   }
-  int tma_stages = use_tma ? (U <= 148 ? bl::kTmaStagesMax : 4) : 0;
+  // Tensor-core K1 bulk (decode_kernel.cu, kMode 3): TMA slab, at most 16
+  // parents (N = 16), and unbounded right margin (every window ends at T, so
+  // a column's max over the rows the next window can reach bounds it).
+  // Opt-in (BL_TC=1): measured slower than the CUDA-core bulk at the C3 shape
+  // because the runtime runs tcgen05 kernels one CTA per SM, which leaves the
+  // serial search phases without a second CTA to overlap.
+  bool use_tc = use_tma && B <= 16 && std::getenv("BL_TC") != nullptr;
+  for (int i = 0; i < n && use_tc; ++i) use_tc = desc[i].need_tail == 0;
+  if (use_tc && on_device) {
+    // the grid allocation must cover the last block's overhang
+    using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static RangeFn range = nullptr;
+    if (!range) {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) ==
+              cudaSuccess &&
+          q == cudaDriverEntryPointSuccess)
+        range = reinterpret_cast<RangeFn>(fn);
+    }
+    CUdeviceptr b0 = 0;
+    size_t sz = 0;
+    use_tc = range && range(&b0, &sz, reinterpret_cast<CUdeviceptr>(gbase)) == CUDA_SUCCESS &&
+             reinterpret_cast<CUdeviceptr>(gbase) + sizeof(float) * gtotal + gpad <= b0 + sz;
+    cudaGetLastError();
+  }
+  // tcgen05 kernels run one CTA per SM (the runtime's occupancy for any
+  // kernel using tcgen05.alloc): the tensor-core variant takes the deepest ring
+  int tma_stages = use_tma ? (use_tc ? bl::kTmaStagesMax : U <= 148 ? 6 : 4) : 0;
   {
     // long utterances: fewer TMA stages (down to 2), then the non-TMA path,
-    // before the plan is rejected (12 KB left for static shared memory)
+    // before the plan is rejected (12 KB left for static shared memory);
+    // large calls (two CTAs per SM wanted): fewer stages until two fit
     const size_t lim = (227 - 12) * 1024;
     const size_t fixed0 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).total;
-    auto need = [&](int st) { return fixed0 + bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0, st).region_need; };
+    auto need = [&](int st) {
+      return fixed0 + bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0, st, use_tc).region_need;
+    };
     while (use_tma && tma_stages > 2 && need(tma_stages) > lim) --tma_stages;
     if (use_tma && need(tma_stages) > lim) {
-      use_tma = false;
+      use_tma = use_tc = false;
       tma_stages = 0;
     }
+    while (use_tma && !use_tc && U > 148 && tma_stages > 3 &&
+           need(tma_stages) + 6 * 1024 > 113 * 1024)
+      --tma_stages;
   }
   // shared-memory plan: the aliased region (P3-P5 keys, P6 staging) is sized
   // so the whole plan fits 3 CTAs/SM (~71 KB) when the fixed parts allow it;
@@ -555,7 +592,8 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   const size_t fixed = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).total;
   const size_t budget = 66 * 1024;  // + static smem + 1 KB reserve: 3 CTAs in 228 KB
   const size_t need1 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 1).region_need;
-  const size_t need0 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0, tma_stages).region_need;
+  const size_t need0 =
+      bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0, tma_stages, use_tc).region_need;
   size_t region = fixed + need1 <= budget ? budget - fixed : std::max(need0, budget > fixed ? budget - fixed : 0);
   const int kub_smem = (!use_tma && need1 <= region) ? 1 : 0;
   region = (std::max(region, kub_smem ? need1 : need0) + 15) & ~(size_t)15;
@@ -581,7 +619,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   };
   std::vector<Run> runs;
   if (!on_device) {
-    d->grid.ensure(sizeof(float) * gtotal);
+    d->grid.ensure(sizeof(float) * gtotal + gpad);
     for (int i = 0; i < n; ++i) {
       if (!runs.empty() && runs.back().i1 == i &&
           utts[i].logp == utts[i - 1].logp + (size_t)desc[i - 1].T * V)
@@ -623,7 +661,10 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.guard_f = guard_float();
   p.exact = d->exact;
   p.nbest = nbest;
-  p.dpsi0 = 5e-4 * d->slack;
+  // certified psi half-width: the tensor-core bulk rounds the factors and
+  // truncates the exponentials to tf32 (relative error <= 2^-11 + 2^-10 per
+  // product, so <= 1.5e-3 on each sum): 2.5e-3 more
+  p.dpsi0 = (use_tc ? 3e-3 : 5e-4) * d->slack;
   p.dpsi1 = 1e-6 * d->slack;
   p.sc_order = d->sc_order;
   p.sc_nent = d->sc_nent;
@@ -638,6 +679,12 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.kub_smem = kub_smem;
   p.region_bytes = (int)region;
   p.use_tma = use_tma ? 1 : 0;
+  p.use_tc = use_tc ? 1 : 0;
+  if (use_tc) {
+    p.mshift_stride = ((C + 511) / 512) * 512;
+    d->mshift.ensure(sizeof(float) * 2 * (size_t)U * p.mshift_stride);
+    p.mshift = static_cast<float*>(d->mshift.p);
+  }
   p.tma_stages = tma_stages;
   if (use_tma) {
     using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
@@ -653,15 +700,28 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
         throw BlError{BL_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable"};
       encode = reinterpret_cast<EncodeFn>(fn);
     }
-    const cuuint64_t dims[2] = {(cuuint64_t)V, (cuuint64_t)(gtotal / V)};
-    const cuuint64_t strides[1] = {(cuuint64_t)V * sizeof(float)};
-    const cuuint32_t box[2] = {(cuuint32_t)bl::kTmaBoxCols, (cuuint32_t)bl::kTmaRows};
-    const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                              const_cast<float*>(gbase), dims, strides, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (use_tc) {
+      // {32 columns, rows, 32-column blocks}: a box of 16 blocks x 8 rows
+      // lands as 16 MN-major swizzle atoms of 8 rows x 128 B (32-byte-atom
+      // 128-byte swizzle), the tf32 A operand layout of tcgen05.mma
+      const cuuint64_t dims[3] = {32, (cuuint64_t)(gtotal / V), (cuuint64_t)((V + 31) / 32)};
+      const cuuint64_t strides[2] = {(cuuint64_t)V * sizeof(float), 128};
+      const cuuint32_t box[3] = {32, 8, 16};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(gbase), dims,
+                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+      const cuuint64_t dims[2] = {(cuuint64_t)V, (cuuint64_t)(gtotal / V)};
+      const cuuint64_t strides[1] = {(cuuint64_t)V * sizeof(float)};
+      const cuuint32_t box[2] = {(cuuint32_t)bl::kTmaBoxCols, (cuuint32_t)bl::kTmaRows};
+      const cuuint32_t estr[2] = {1, 1};
+      r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(gbase), dims,
+                 strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r != CUDA_SUCCESS)
       throw BlError{BL_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r)};
   }

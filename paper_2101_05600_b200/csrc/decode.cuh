@@ -42,15 +42,23 @@ struct HistRec {
 };
 
 // TMA streaming of the CTC window slab (large vocabularies): 512-column tiles
-// (two columns per thread) x kTmaRows-row chunks, kTmaStagesMax stages.
+// (two columns per thread) x kTmaRows-row chunks, kTmaStagesMax stages. The
+// tensor-core variant uses the same 16 KB stages as 16 swizzle blocks of
+// 8 rows x 32 columns, and a factor operand of 512 B per 8-row chunk.
 constexpr int kTmaBoxCols = 256;
 constexpr int kTmaRows = 8;
-constexpr int kTmaStagesMax = 6;
+constexpr int kTmaStagesMax = 10;
 constexpr int kTmaStageBytes = 2 * kTmaRows * kTmaBoxCols * 4;
 
 struct KParams {
-  CUtensorMap tmap;  // 2D map over all utterances' grid rows [sum T][V] (fp32)
+  CUtensorMap tmap;  // TMA map over all utterances' grid rows: 2D [sum T][V] (fp32),
+                     // or with use_tc 3D {32 cols, sum T rows, V/32 column blocks}
+                     // with 32-byte-atom 128-byte swizzle (the MN-major tf32
+                     // operand layout of tcgen05.mma)
   int use_tma, tma_stages;
+  int use_tc;        // tensor-core bulk (tcgen05.mma kind::tf32), see decode_kernel.cu
+  float* mshift;     // use_tc: [2][U][mshift_stride] per-column exp shifts by step parity
+  int mshift_stride;
   const UttDesc* utts;
   int U, V, C, B;
   int u0;          // first utterance of this launch (chunked launches)
@@ -125,14 +133,18 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t
 // region_bytes: size of the aliased region (P3-P5: fp32 factors, upper keys,
 // underflow flags, theta0 list; P6: contender staging with stride W). The
 // host sizes it so the whole plan fits 3 CTAs per SM when possible.
+constexpr int kTcChunkBytes = 512;  // factor operand per 8-row chunk: 16 parents x 8 tf32
 __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, int caps,
                                               int S, size_t region_bytes, int kub_smem,
-                                              int tma_stages = 0) {
+                                              int tma_stages = 0, int tc = 0) {
   SmemPlan p;
   p.phi = 0;
   p.region = align16(p.phi + sizeof(double) * (size_t)B * Tmax);
   p.phif = 0;
-  p.kub = align16(sizeof(float) * (size_t)Tmax * bmax);
+  // P3 factors: fp32 [Tmax][bmax] rows, or (tensor cores) the K-major tf32
+  // operand, one 512 B chunk per 8 rows
+  p.kub = tc ? (size_t)kTcChunkBytes * (size_t)((Tmax + 7) / 8)
+             : align16(sizeof(float) * (size_t)Tmax * bmax);
   const size_t words = ((size_t)B * C + 31) / 32;
   p.ubits = kub_smem ? align16(p.kub + sizeof(float) * (size_t)B * C) : p.kub;
   if (kub_smem) {  // keys mode: every key, its flag, then the theta0 list
@@ -148,6 +160,7 @@ __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, 
     p.raw = p.kub;
     const size_t raw_end = p.raw + 8 * (size_t)kRawCap;
     p.stages = ((p.region + raw_end + 127) & ~(size_t)127) - p.region;
+    if (tc) p.stages += 1024;  // the kernel aligns the stage ring to 1024 B (swizzle atoms)
     if (tma_stages) {
       p.clist = p.stages;
       p.region_need = p.stages + (size_t)tma_stages * kTmaStageBytes;

@@ -35,6 +35,7 @@
 #include "softplus.cuh"
 
 namespace bl {
+namespace {  // device helpers: internal to each mode's translation unit
 
 // ---------------------------------------------------------------- logmath
 __device__ __forceinline__ bool is_zero(double x) { return x <= kLogZeroGuard; }
@@ -165,6 +166,24 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "r"(parity)
       : "memory");
 }
+// bounded wait (tensor-core variant): a barrier that never completes reports
+// where and traps instead of hanging the device
+__device__ __noinline__ void mbar_wait_dbg(unsigned long long* bar, unsigned parity, int tag,
+                                           unsigned g) {
+  const long long t0 = clock64();
+  for (;;) {
+    unsigned ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (ok) return;
+    if (clock64() - t0 > (1ll << 33)) {
+      printf("[bl] decode_kernel: barrier wait timed out: cta %d thread %d tag %d job %u parity %u\n",
+             blockIdx.x, threadIdx.x, tag, g, parity);
+      asm volatile("trap;");
+    }
+  }
+}
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
                                             unsigned long long* bar) {
   asm volatile(
@@ -173,6 +192,73 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
       : "memory");
 }
+
+// 3D box {32 columns, 8 rows, 16 column blocks} (tensor-core variant)
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y,
+                                            int z, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+// UMMA shared-memory descriptors (sm_100 layout: start>>4 @0, LBO>>4 @16,
+// SBO>>4 @32, version 1 @46, layout type @61)
+__device__ __forceinline__ unsigned long long umma_desc_mn32(const void* p) {
+  // MN-major, 128-byte swizzle with 32-byte atoms (type 1): 32 tf32 of MN per
+  // 128 B row, 4 K rows per 512 B atom; MN atoms 1024 B apart (LBO), K
+  // 4-row groups 512 B apart (SBO) -- the TMA stage as loaded
+  return (unsigned long long)((smem_u32(p) & 0x3FFFF) >> 4) | (64ull << 16) | (32ull << 32) |
+         (1ull << 46) | (1ull << 61);
+}
+__device__ __forceinline__ unsigned long long umma_desc_kint(const void* p) {
+  // K-major, no swizzle: 8-row x 16-byte core matrices, K chunks 128 B apart
+  // (LBO), 8-row N groups 256 B apart (SBO)
+  return (unsigned long long)((smem_u32(p) & 0x3FFFF) >> 4) | (8ull << 16) | (16ull << 32) |
+         (1ull << 46);
+}
+// D[128 x 16] (+)= A[128 x 8] . B[8 x 16], tf32 inputs, fp32 accumulate in TMEM;
+// idesc: F32 accumulator @4, A/B TF32 @7/@10, A MN-major @15, N/8 @17, M/16 @24
+constexpr unsigned kTcIdesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) |
+                              ((16u >> 3) << 17) | ((128u >> 4) << 24);
+__device__ __forceinline__ void umma_tf32(unsigned tmem, unsigned long long da,
+                                          unsigned long long db, unsigned acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %4, p;\n\t}\n" ::"r"(tmem),
+      "l"(da), "l"(db), "r"(acc), "r"(kTcIdesc));
+}
+__device__ __forceinline__ void umma_commit(unsigned long long* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(unsigned taddr, float (&v)[16]) {
+  unsigned r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tc_before_sync() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_after_sync() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ float tf32_rna(float x) {
+  unsigned r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+constexpr int kTcTmemCols = 128;  // two 64-column accumulator buffers (4 subtiles x 16)
 
 struct SelE {
   double score;
@@ -395,18 +481,23 @@ __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
     prof_t = _now;                                     \
   }
 
+}  // namespace
+
 // kMode 0: K1 slab by __ldg, every upper key in shared memory (keys mode);
 // 1: __ldg, keys filtered on chip (filter mode); 2: TMA slab, filter mode
 template <int BMAX, int kMode>
 __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
     decode_kernel(const __grid_constant__ KParams P) {
-  constexpr bool kTma = kMode == 2;
+  constexpr bool kTma = kMode >= 2;
+  constexpr bool kTc = kMode == 3;  // K1 bulk on tcgen05.mma (kind::tf32), accumulators in TMEM
   constexpr bool keys_mode = kMode == 0;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ Shared<BMAX> sh;
   __shared__ SpTables tb;
   __shared__ __align__(8) unsigned long long mbar[kTmaStagesMax];
   __shared__ int cons[kTmaStagesMax];  // warps done with each TMA stage (monotonic)
+  __shared__ __align__(8) unsigned long long mmad[kTmaStagesMax];  // tensor cores: stage's MMAs done
+  __shared__ unsigned tmem_base;
 
   const int u = blockIdx.x + P.u0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -419,7 +510,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
 
   // dynamic smem carve-up (smem_plan, decode.cuh)
   const SmemPlan pl = smem_plan(P.Tmax, B, BMAX, C, P.caps, P.S, P.region_bytes, P.kub_smem,
-                                kTma ? P.tma_stages : 0);
+                                kTma ? P.tma_stages : 0, kTc ? 1 : 0);
   double* phi = reinterpret_cast<double*>(dsm + pl.phi);    // [B][Tmax]
   unsigned char* region = dsm + pl.region;                  // aliased, region_bytes
   float* PhiF = reinterpret_cast<float*>(region + pl.phif);  // [Tmax][BMAX]
@@ -449,10 +540,29 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
   if (kTma && tid == 0) {
     for (int k = 0; k < P.tma_stages; ++k) {
       mbar_init(&mbar[k], 1);
+      if (kTc) mbar_init(&mmad[k], 1);
       cons[k] = 0;
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  if (kTc && warp == 0) {  // accumulators: 2 x (4 subtiles x 16 parents) fp32 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "r"(kTcTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // the tensor-core stage ring starts on a 1024-byte boundary (swizzle atoms)
+  unsigned char* tc_stg = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(region + pl.stages - 1024) + 1023) & ~(uintptr_t)1023);
+  auto tmem_free = [&]() {
+    if constexpr (kTc) {
+      tc_before_sync();
+      __syncthreads();
+      if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(kTcTmemCols));
+    }
+  };
   for (int i = tid; i < 320; i += kNT)
     reinterpret_cast<double*>(&tb)[i] = reinterpret_cast<const double*>(&c_sptab)[i];
   if (P.ready) {
@@ -559,6 +669,68 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         if (two) Ft[(size_t)k * C + c1] = f1;
       }
     }
+  }
+  if constexpr (kTc) {
+    // The step-1 exp shift of every column: its max over all T frames (the
+    // step-1 window is [1, T]); each later step takes the max over the rows
+    // the next window can still reach while it streams its own (P3).
+    const int nch = (T + 7) >> 3, ntile = (C + 511) >> 9, J = ntile * nch;
+    const int NST = P.tma_stages;
+    float* msh1 = P.mshift + ((size_t)1 * P.U + u) * P.mshift_stride;  // step 1's parity
+    auto issue0 = [&](int j, unsigned g) {
+      const int st = (int)(g % (unsigned)NST), tile = j / nch, k = j - tile * nch;
+      mbar_expect_tx(&mbar[st], kTmaStageBytes);
+      tma_load_3d(tc_stg + (size_t)st * kTmaStageBytes, &P.tmap, 0, ud.row0 + k * 8, tile * 16,
+                  &mbar[st]);
+    };
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      for (int j = 0; j < NST && j < J; ++j) issue0(j, tma_jobs + j);
+    }
+    const int tbk = tid >> 4, gq = tid & 7, rg = (tid >> 3) & 1;
+    const float gfl = P.guard_f;
+    float4 mx = make_float4(gfl, gfl, gfl, gfl);
+    for (int j = 0; j < J; ++j) {
+      const unsigned g = tma_jobs + j;
+      const int st = (int)(g % (unsigned)NST), tile = j / nch, k = j - tile * nch;
+      if (k == 0) mx = make_float4(gfl, gfl, gfl, gfl);
+      mbar_wait_dbg(&mbar[st], (g / (unsigned)NST) & 1u, 1, g);
+      const float* sb =
+          reinterpret_cast<const float*>(tc_stg + (size_t)st * kTmaStageBytes) + tbk * 256;
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int r = rg + 2 * rr;
+        if (8 * k + r < T) {
+          const float4 x = *reinterpret_cast<const float4*>(
+              sb + r * 32 + (((((gq >> 1) ^ r) & 3) << 3) | ((gq & 1) << 2)));
+          mx.x = fmaxf(mx.x, x.x);
+          mx.y = fmaxf(mx.y, x.y);
+          mx.z = fmaxf(mx.z, x.z);
+          mx.w = fmaxf(mx.w, x.w);
+        }
+      }
+      __syncthreads();  // stage consumed (one-time pass: a block barrier is fine)
+      if (tid == 0) {
+        // keep the per-stage use counts of P3 in step: the release count and
+        // the MMA-done barrier's phase (no MMA ran on this use)
+        cons[st] += kNWarp;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mmad[st]))
+                     : "memory");
+        if (j + NST < J) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue0(j + NST, g + NST);
+        }
+      }
+      if (k == nch - 1) {
+        mx.x = fmaxf(mx.x, __shfl_xor_sync(0xffffffffu, mx.x, 8));
+        mx.y = fmaxf(mx.y, __shfl_xor_sync(0xffffffffu, mx.y, 8));
+        mx.z = fmaxf(mx.z, __shfl_xor_sync(0xffffffffu, mx.z, 8));
+        mx.w = fmaxf(mx.w, __shfl_xor_sync(0xffffffffu, mx.w, 8));
+        if (rg == 0)
+          *reinterpret_cast<float4*>(msh1 + tile * 512 + tbk * 32 + gq * 4) = mx;
+      }
+    }
+    tma_jobs += J;
   }
   __syncthreads();
   }  // fresh start
@@ -679,13 +851,30 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           if (act) {
             for (int i = hl; i < W; i += 16) {  // this lane's own phi entries
               const double pv = phi[(size_t)j * P.Tmax + i];
-              PhiF[(size_t)i * BMAX + j] =
-                  (!is_zero(Mj) && !is_zero(pv)) ? __expf((float)(pv - Mj)) : 0.f;
+              const float f = (!is_zero(Mj) && !is_zero(pv)) ? __expf((float)(pv - Mj)) : 0.f;
+              if constexpr (kTc) {
+                // K-major tf32 operand: chunk i/8, 8-row N group, 16-byte K chunk
+                PhiF[(i >> 3) * 128 + (j >> 3) * 64 + ((i & 7) >> 2) * 32 + (j & 7) * 4 +
+                     (i & 3)] = tf32_rna(f);
+              } else {
+                PhiF[(size_t)i * BMAX + j] = f;
+              }
             }
           }
         }
       }
-      if (!P.exact) {
+      if (!P.exact && kTc) {
+        // zero operand entries: parents nb..15 on every row of the chunks,
+        // and rows W.. of the last chunk (their slab rows lie past the window)
+        const int rows = ((W + 7) >> 3) * 8;
+        for (int idx = tid; idx < rows * 16; idx += kNT) {
+          const int i = idx >> 4, j = idx & 15;
+          if (j >= nb || i >= W)
+            PhiF[(i >> 3) * 128 + (j >> 3) * 64 + ((i & 7) >> 2) * 32 + (j & 7) * 4 + (i & 3)] =
+                0.f;
+        }
+      }
+      if (!P.exact && !kTc) {
         const int pad = BMAX - nb;  // factor columns of absent parents are zero
         for (int idx = tid; idx < W * pad; idx += kNT) {
           const int i = idx / pad, j = nb + (idx - i * pad);
@@ -771,9 +960,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       // runs pass 2 (emit == true) after the warp's running bound is known:
       // the same keys are recomputed (identical arithmetic) and those whose
       // upper bound reaches the bound go to the raw list.
-      auto emit_keys = [&](int c0, bool two, const float2(&S0)[kP], const float2(&S1)[kP],
-                           float m0, float m1, float r0s, float r1s, bool emit, float th,
-                           float& kmax) {
+      auto emit_keys = [&](int c0, int c1, bool two, const float2(&S0)[kP],
+                           const float2(&S1)[kP], float m0, float m1, float r0s, float r1s,
+                           bool emit, float th, float& kmax) {
         // filter mode, pass 1: min over the parents of each column's lower
         // bounds (with B live parents, B distinct candidates reach it), and
         // the largest upper key (pass 2 is skipped when it misses the bound)
@@ -786,7 +975,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             const bool mz = sh.mzero[q] != 0;
 #pragma unroll
             for (int cc = 0; cc < 2; ++cc) {
-              const int c = c0 + cc;
+              const int c = cc ? c1 : c0;
               if (cc == 1 && !two) break;
               const float m = cc ? m1 : m0;
               const float2 Sp = cc ? S1[q >> 1] : S0[q >> 1];
@@ -866,7 +1055,140 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         __syncwarp();
         return fmaxf(wb, ord2f(*reinterpret_cast<volatile int*>(&sh.th_run)));
       };
-      if constexpr (kTma) {
+      if constexpr (kTc) {
+        // K1 bulk on the tensor cores. For a 512-column tile,
+        //   S[c][j] = sum_t exp(L[t,c] - m_c) * a_j[t]   (a_j = PhiF, P2)
+        // is a [512 x W] . [W x 16] product: the TMA stage (8 rows x 512
+        // columns as 16 blocks of 8 x 32, 32-byte-atom 128-byte swizzle) is
+        // exponentiated IN PLACE and then is the MN-major tf32 A operand of
+        // four tcgen05.mma (M = 128 columns, N = 16 parents, K = 8 rows),
+        // accumulating in TMEM (two 64-column buffers, alternating tiles).
+        // The shift m_c is fixed for the step: the max of column c over the
+        // rows the window can reach (so every exp is <= 1 and no rescale is
+        // needed); it was taken while the previous step streamed (or by the
+        // step-1 pass), and this step takes the next step's the same way.
+        // The warp that finishes a stage last issues its MMAs and refills
+        // the previous job's stage once that stage's MMAs are done.
+        const int nch = (W + 7) >> 3;
+        const int ntile = (C + 511) >> 9;
+        const int J = ntile * nch;
+        const int NST = P.tma_stages;
+        const int urow = ud.row0 + s - 1;
+        const unsigned tmem = tmem_base;
+        auto issue = [&](int j, unsigned g) {
+          const int st = (int)(g % (unsigned)NST), tile = j / nch, k = j - tile * nch;
+          mbar_expect_tx(&mbar[st], kTmaStageBytes);
+          tma_load_3d(tc_stg + (size_t)st * kTmaStageBytes, &P.tmap, 0, urow + k * 8, tile * 16,
+                      &mbar[st]);
+        };
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          for (int j = 0; j < NST && j < J; ++j) issue(j, tma_jobs + j);
+        }
+        // transform roles: block tbk of the stage, logical 4-column quad gq,
+        // rows rg, rg + 2, rg + 4, rg + 6 (conflict-free 16-byte accesses)
+        const int tbk = tid >> 4, gq = tid & 7, rg = (tid >> 3) & 1;
+        const float* msh = P.mshift + ((size_t)(l & 1) * P.U + u) * P.mshift_stride;
+        float* msn = P.mshift + ((size_t)((l + 1) & 1) * P.U + u) * P.mshift_stride;
+        // the frame s is in the next window only if s > l (s >= l always)
+        const int skip0 = (s == l) ? 1 : 0;
+        constexpr float kL2e = 1.44269504088896341f;
+        float4 ml2 = make_float4(0.f, 0.f, 0.f, 0.f), mx = ml2;
+        // epilogue roles: TMEM lanes 32 * (warp % 4) + lane of subtiles
+        // 2 * (warp / 4) and + 1, i.e. columns ca and ca + 128 of the tile
+        const int sub0 = 2 * (warp >> 2);
+        for (int j = 0; j < J; ++j) {
+          const unsigned g = tma_jobs + j;
+          const int st = (int)(g % (unsigned)NST);
+          const int tile = j / nch, k = j - tile * nch;
+          const int colq = tile * 512 + tbk * 32 + gq * 4;
+          if (k == 0) {
+            const float4 m4 = *reinterpret_cast<const float4*>(msh + colq);
+            ml2 = make_float4(m4.x * kL2e, m4.y * kL2e, m4.z * kL2e, m4.w * kL2e);
+            mx = make_float4(gf, gf, gf, gf);
+          }
+          mbar_wait_dbg(&mbar[st], (g / (unsigned)NST) & 1u, 2, g);
+          float* sb = reinterpret_cast<float*>(tc_stg + (size_t)st * kTmaStageBytes) + tbk * 256;
+#pragma unroll
+          for (int rr = 0; rr < 4; ++rr) {
+            const int r = rg + 2 * rr;
+            const int fr = 8 * k + r;  // frame s + fr
+            float4* px = reinterpret_cast<float4*>(
+                sb + r * 32 + (((((gq >> 1) ^ r) & 3) << 3) | ((gq & 1) << 2)));
+            const float4 x = *px;
+            float4 pv = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (fr < W) {
+              if (fr > 0 || !skip0) {
+                mx.x = fmaxf(mx.x, x.x);
+                mx.y = fmaxf(mx.y, x.y);
+                mx.z = fmaxf(mx.z, x.z);
+                mx.w = fmaxf(mx.w, x.w);
+              }
+              pv.x = ex2_ftz(fmaf(x.x, kL2e, -ml2.x));
+              pv.y = ex2_ftz(fmaf(x.y, kL2e, -ml2.y));
+              pv.z = ex2_ftz(fmaf(x.z, kL2e, -ml2.z));
+              pv.w = ex2_ftz(fmaf(x.w, kL2e, -ml2.w));
+            }
+            *px = pv;
+          }
+          // generic-proxy writes -> the MMA (async proxy); arrival
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          tc_before_sync();
+          __syncwarp();
+          if (lane == 0) {
+            const int done = atomicAdd(&cons[st], 1);
+            if (done == (int)(g / (unsigned)NST) * kNWarp + kNWarp - 1) {
+              tc_after_sync();
+              const unsigned char* a0 = tc_stg + (size_t)st * kTmaStageBytes;
+              const unsigned long long db = umma_desc_kint(reinterpret_cast<const unsigned char*>(PhiF) + k * kTcChunkBytes);
+              const unsigned dcol = tmem + (unsigned)((tile & 1) * 64);
+#pragma unroll
+              for (int sub = 0; sub < 4; ++sub)
+                umma_tf32(dcol + sub * 16, umma_desc_mn32(a0 + sub * 4096), db, k > 0 ? 1u : 0u);
+              umma_commit(&mmad[st]);
+              if (j > 0 && j - 1 + NST < J) {  // refill the previous job's stage
+                const unsigned gp = g - 1;
+                const int stp = (int)(gp % (unsigned)NST);
+                mbar_wait_dbg(&mmad[stp], (gp / (unsigned)NST) & 1u, 3, gp);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issue(j - 1 + NST, gp + NST);
+              }
+            }
+          }
+          if (k == nch - 1) {  // tile epilogue
+            mx.x = fmaxf(mx.x, __shfl_xor_sync(0xffffffffu, mx.x, 8));
+            mx.y = fmaxf(mx.y, __shfl_xor_sync(0xffffffffu, mx.y, 8));
+            mx.z = fmaxf(mx.z, __shfl_xor_sync(0xffffffffu, mx.z, 8));
+            mx.w = fmaxf(mx.w, __shfl_xor_sync(0xffffffffu, mx.w, 8));
+            if (rg == 0) *reinterpret_cast<float4*>(msn + colq) = mx;
+            mbar_wait_dbg(&mmad[st], (g / (unsigned)NST) & 1u, 4, g);  // the tile's last MMAs
+            tc_after_sync();
+            float v0[16], v1[16];
+            const unsigned trow = tmem + ((unsigned)(32 * (warp & 3)) << 16) +
+                                  (unsigned)((tile & 1) * 64);
+            tmem_ld16(trow + sub0 * 16, v0);
+            tmem_ld16(trow + (sub0 + 1) * 16, v1);
+            tc_before_sync();
+            const int ca = tile * 512 + sub0 * 128 + 32 * (warp & 3) + lane, cb = ca + 128;
+            const bool acta = ca < C, actb = cb < C;
+            float2 S0[kP], S1[kP];
+#pragma unroll
+            for (int q = 0; q < kP; ++q) {
+              S0[q] = make_float2(v0[2 * q], v0[2 * q + 1]);
+              S1[q] = make_float2(v1[2 * q], v1[2 * q + 1]);
+            }
+            const float ma = msh[ca], mb = msh[cb];
+            const float ra = (row_same >= 0 && acta) ? P.sc_rowsf[(size_t)row_same * V + ca] : 0.f;
+            const float rb = (row_same >= 0 && actb) ? P.sc_rowsf[(size_t)row_same * V + cb] : 0.f;
+            float kmax = -INFINITY;
+            if (acta) emit_keys(ca, cb, actb, S0, S1, ma, actb ? mb : gf, ra, rb, false, 0.f, kmax);
+            const float th = warp_bound(tile < 3 || (tile & 3) == 0);
+            if (acta && kmax >= th)
+              emit_keys(ca, cb, actb, S0, S1, ma, actb ? mb : gf, ra, rb, true, th, kmax);
+          }
+        }
+        tma_jobs += J;
+      } else if constexpr (kTma) {
         // K1 slab streamed by TMA: job j = (512-column tile, kTmaRows-row
         // chunk); thread 0 keeps tma_stages jobs in flight on mbarriers, all
         // threads consume each chunk from shared memory.
@@ -942,10 +1264,13 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             }
           }
           // stage release per warp: the warp that finishes it last refills
-          // it (no block barrier; the other warps stream on)
+          // it (no block barrier; the other warps stream on). Every lane's
+          // reads of the stage were consumed by its FMAs above, and a warp's
+          // shared-memory accesses (these reads, then lane 0's atomic) are
+          // performed in order, so the refill (issued after the last count)
+          // cannot overtake a read.
           __syncwarp();
           if (lane == 0) {
-            __threadfence_block();
             const int done = atomicAdd(&cons[st], 1);
             if (done == (int)(g / (unsigned)NST) * kNWarp + kNWarp - 1 && j + NST < J) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -955,10 +1280,10 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           if (k == nch - 1) {  // the tile's keys (whole warp: warp_bound)
             float kmax = -INFINITY;
             if (active)
-              emit_keys(c0, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, false, 0.f, kmax);
+              emit_keys(c0, c0 + 1, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, false, 0.f, kmax);
             const float th = warp_bound(tile < 3 || (tile & 3) == 0);
             if (active && kmax >= th)
-              emit_keys(c0, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, true, th, kmax);
+              emit_keys(c0, c0 + 1, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, true, th, kmax);
           }
         }
         tma_jobs += J;
@@ -1035,13 +1360,14 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         if (!two) m1 = gf;
         const long long tq2 = clock64();
         tq_frames += tq2 - tq1;
-        emit_keys(c0, two, S0, S1, m0, m1, r0s, r1s, false, 0.f, kmax);
+        emit_keys(c0, c0 + 1, two, S0, S1, m0, m1, r0s, r1s, false, 0.f, kmax);
         tq_keys += clock64() - tq2;
         }
         if (!keys_mode) {
           const int it = cb / (2 * kNT);
           const float th = warp_bound(it < 3 || (it & 3) == 0);
-          if (act && kmax >= th) emit_keys(c0, two, S0, S1, m0, m1, r0s, r1s, true, th, kmax);
+          if (act && kmax >= th)
+            emit_keys(c0, c0 + 1, two, S0, S1, m0, m1, r0s, r1s, true, th, kmax);
         }
       }
       }
@@ -1605,6 +1931,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       double* sb = reinterpret_cast<double*>(st_u + 16 + align16(sizeof(Shared<BMAX>)));
       for (int i = tid; i <= P.S + 1; i += kNT) sb[i] = best_by_len[i];
       if (tid == 0) *reinterpret_cast<int*>(st_u) = 0;
+      tmem_free();
       return;
     }
   }
@@ -1748,9 +2075,119 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
     *reinterpret_cast<int*>(st_u) = 1;
     atomicAdd(P.n_done, 1u);
   }
+  tmem_free();
 }
 
 // ------------------------------------------------------------ launchers
+// The four kernel modes compile as separate translation units (Makefile:
+// decode_kernel.cu with -DDK_MODE=0..3); each defines its mode's launcher
+// over the beam instantiations, and mode 0's unit also holds the dispatch.
+size_t decode_smem_bytes(const KParams& p);
+int bmax_for(int B);
+
+static int mode_of(const KParams& p) {
+  return p.use_tc ? 3 : p.use_tma ? 2 : (p.kub_smem ? 0 : 1);
+}
+
+template <int BMAX, int kMode>
+static cudaError_t launch_v(const KParams& p, cudaStream_t st) {
+  const size_t sm = decode_smem_bytes(p);
+  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX, kMode>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+  if (err != cudaSuccess) {
+    if (std::getenv("BL_DEBUG"))
+      std::fprintf(stderr, "[bl] decode_kernel<%d,%d>: set max dynamic smem %zu: %s\n", BMAX,
+                   kMode, sm, cudaGetErrorString(err));
+    return err;
+  }
+  if (std::getenv("BL_DEBUG")) {
+    int nb = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decode_kernel<BMAX, kMode>, kNT, sm);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, decode_kernel<BMAX, kMode>);
+    size_t avail2 = 0;
+    cudaOccupancyAvailableDynamicSMemPerBlock(&avail2, decode_kernel<BMAX, kMode>, 2, kNT);
+    cudaGetLastError();  // fails for tcgen05 kernels (one CTA per SM): not a launch error
+    std::fprintf(stderr, "[bl] decode_kernel<%d,%d>: grid %d, dyn smem %zu, static %zu, regs %d, "
+                 "local %zu, max threads %d, %d CTA/SM (dyn smem available at 2 CTA/SM: %zu)\n",
+                 BMAX, kMode, p.U, sm, fa.sharedSizeBytes, fa.numRegs, fa.localSizeBytes,
+                 fa.maxThreadsPerBlock, nb, avail2);
+  }
+  decode_kernel<BMAX, kMode><<<p.U, kNT, sm, st>>>(p);
+  err = cudaGetLastError();
+  if (err != cudaSuccess && std::getenv("BL_DEBUG"))
+    std::fprintf(stderr, "[bl] decode_kernel<%d,%d>: launch of %d CTAs, %zu B dynamic smem: %s\n",
+                 BMAX, kMode, p.U, sm, cudaGetErrorString(err));
+  return err;
+}
+
+template <int BMAX, int kMode>
+static size_t static_v() {
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, decode_kernel<BMAX, kMode>);
+  return fa.sharedSizeBytes;
+}
+
+// launcher / static shared memory of mode DK_MODE for beam capacity `bmax`
+#define BL_MODE_FNS(M)                                                              \
+  cudaError_t launch_mode##M(int bmax, const KParams& p, cudaStream_t st) {         \
+    switch (bmax) {                                                                 \
+      case 4: return launch_v<4, M>(p, st);                                         \
+      case 8: return launch_v<8, M>(p, st);                                         \
+      case 10: return launch_v<10, M>(p, st);                                       \
+      case 12: return launch_v<12, M>(p, st);                                       \
+      case 16: return launch_v<16, M>(p, st);                                       \
+      BL_WIDE_CASES(M)                                                              \
+    }                                                                               \
+    return cudaErrorInvalidValue;                                                   \
+  }                                                                                 \
+  size_t static_mode##M(int bmax) {                                                 \
+    switch (bmax) {                                                                 \
+      case 4: return static_v<4, M>();                                              \
+      case 8: return static_v<8, M>();                                              \
+      case 10: return static_v<10, M>();                                            \
+      case 12: return static_v<12, M>();                                            \
+      case 16: return static_v<16, M>();                                            \
+      BL_WIDE_STATIC(M)                                                             \
+    }                                                                               \
+    return 0;                                                                       \
+  }
+
+cudaError_t launch_mode0(int, const KParams&, cudaStream_t);
+cudaError_t launch_mode1(int, const KParams&, cudaStream_t);
+cudaError_t launch_mode2(int, const KParams&, cudaStream_t);
+cudaError_t launch_mode3(int, const KParams&, cudaStream_t);
+size_t static_mode0(int);
+size_t static_mode1(int);
+size_t static_mode2(int);
+size_t static_mode3(int);
+
+#if DK_MODE == 3  // the tensor-core bulk holds at most 16 parents
+#define BL_WIDE_CASES(M)
+#define BL_WIDE_STATIC(M)
+#else
+#define BL_WIDE_CASES(M)                      \
+  case 24: return launch_v<24, M>(p, st);     \
+  case 32: return launch_v<32, M>(p, st);
+#define BL_WIDE_STATIC(M)              \
+  case 24: return static_v<24, M>();   \
+  case 32: return static_v<32, M>();
+#endif
+
+#if DK_MODE == 0
+BL_MODE_FNS(0)
+#elif DK_MODE == 1
+BL_MODE_FNS(1)
+#elif DK_MODE == 2
+BL_MODE_FNS(2)
+#elif DK_MODE == 3
+BL_MODE_FNS(3)
+#else
+#error "compile decode_kernel.cu with -DDK_MODE=0..3"
+#endif
+
+#if DK_MODE == 0
 int bmax_for(int B) {
   if (B <= 4) return 4;
   if (B <= 8) return 8;
@@ -1779,71 +2216,30 @@ size_t step_state_bytes(int B, int S) {
 
 size_t decode_smem_bytes(const KParams& p) {
   return smem_plan(p.Tmax, p.B, bmax_for(p.B), p.C, p.caps, p.S, p.region_bytes, p.kub_smem,
-                   p.tma_stages).total;
-}
-
-static int mode_of(const KParams& p) { return p.use_tma ? 2 : (p.kub_smem ? 0 : 1); }
-
-template <int BMAX, int kMode>
-static cudaError_t launch_v(const KParams& p, cudaStream_t st) {
-  const size_t sm = decode_smem_bytes(p);
-  cudaError_t err = cudaFuncSetAttribute(decode_kernel<BMAX, kMode>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
-  if (err != cudaSuccess) return err;
-  if (std::getenv("BL_DEBUG")) {
-    int nb = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, decode_kernel<BMAX, kMode>, kNT, sm);
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, decode_kernel<BMAX, kMode>);
-    std::fprintf(stderr, "[bl] decode_kernel<%d,%d>: grid %d, dyn smem %zu, static %zu, regs %d, %d CTA/SM\n",
-                 BMAX, kMode, p.U, sm, fa.sharedSizeBytes, fa.numRegs, nb);
-  }
-  decode_kernel<BMAX, kMode><<<p.U, kNT, sm, st>>>(p);
-  return cudaGetLastError();
-}
-
-template <int BMAX>
-static size_t static_smem_t(const KParams& p) {
-  cudaFuncAttributes fa{};
-  const int m = mode_of(p);
-  if (m == 2) cudaFuncGetAttributes(&fa, decode_kernel<BMAX, 2>);
-  else if (m == 1) cudaFuncGetAttributes(&fa, decode_kernel<BMAX, 1>);
-  else cudaFuncGetAttributes(&fa, decode_kernel<BMAX, 0>);
-  return fa.sharedSizeBytes;
+                   p.tma_stages, p.use_tc).total;
 }
 
 // static shared memory of the kernel variant `p` selects
 size_t decode_static_smem(const KParams& p) {
-  switch (bmax_for(p.B)) {
-    case 4: return static_smem_t<4>(p);
-    case 8: return static_smem_t<8>(p);
-    case 10: return static_smem_t<10>(p);
-    case 12: return static_smem_t<12>(p);
-    case 16: return static_smem_t<16>(p);
-    case 24: return static_smem_t<24>(p);
-    default: return static_smem_t<32>(p);
+  const int b = bmax_for(p.B);
+  switch (mode_of(p)) {
+    case 3: return b <= 16 ? static_mode3(b) : 0;
+    case 2: return static_mode2(b);
+    case 1: return static_mode1(b);
+    default: return static_mode0(b);
   }
-}
-
-template <int BMAX>
-static cudaError_t launch_t(const KParams& p, cudaStream_t st) {
-  const int m = mode_of(p);
-  return m == 2 ? launch_v<BMAX, 2>(p, st) : m == 1 ? launch_v<BMAX, 1>(p, st)
-                                               : launch_v<BMAX, 0>(p, st);
 }
 
 cudaError_t launch_decode(const KParams& p, cudaStream_t st) {
-  switch (bmax_for(p.B)) {
-    case 4: return launch_t<4>(p, st);
-    case 8: return launch_t<8>(p, st);
-    case 10: return launch_t<10>(p, st);
-    case 12: return launch_t<12>(p, st);
-    case 16: return launch_t<16>(p, st);
-    case 24: return launch_t<24>(p, st);
-    case 32: return launch_t<32>(p, st);
+  const int b = bmax_for(p.B);
+  if (b == 0) return cudaErrorInvalidValue;
+  switch (mode_of(p)) {
+    case 3: return b <= 16 ? launch_mode3(b, p, st) : cudaErrorInvalidValue;
+    case 2: return launch_mode2(b, p, st);
+    case 1: return launch_mode1(b, p, st);
+    default: return launch_mode0(b, p, st);
   }
-  return cudaErrorInvalidValue;
 }
+#endif
 
 }  // namespace bl

@@ -53,18 +53,22 @@ def _check(got, exp):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("mode", ["fast", "exact", "step"])
-def test_c3_shape_vs_reference(c3, mode):
+@pytest.mark.parametrize("mode", ["fast", "exact", "step", "tc", "tc_step"])
+def test_c3_shape_vs_reference(c3, mode, monkeypatch):
+    """tc: the opt-in tensor-core bulk (BL_TC=1: tcgen05.mma kind::tf32 on
+    the in-place exponentiated TMA stage), in one launch and step-granular."""
     exp, items = c3
+    if mode.startswith("tc"):
+        monkeypatch.setenv("BL_TC", "1")
     dec = bl.Decoder(bl.UniformScorer(V - 1), bl.DecoderConfig(beam_width=10),
-                     exact=mode == "exact", step_mode=mode == "step")
+                     exact=mode == "exact", step_mode=mode in ("step", "tc_step"))
     cnt = bl.DecodeCounters()
     got = dec.decode([bl.Utterance(u, bl.PosteriorGrid(g)) for u, g in items], cnt)
     _check(got, exp)
     assert (cnt.steps, cnt.scorer_queries, cnt.ctc_frames_evaluated) == \
         (exp["counters"]["steps"], exp["counters"]["scorer_queries"],
          exp["counters"]["ctc_frames_evaluated"])
-    if mode == "fast":
+    if mode in ("fast", "tc"):
         st = dec.last_stats
         assert st["fallback_steps"] > 0, st  # dupcols forces the exact fallback
         assert st["fallback_steps"] < st["steps"] // 4, st
