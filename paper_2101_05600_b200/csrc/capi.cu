@@ -542,11 +542,17 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   // Tensor-core K1 bulk (decode_kernel.cu, kMode 3): TMA slab, at most 16
   // parents (N = 16), and unbounded right margin (every window ends at T, so
   // a column's max over the rows the next window can reach bounds it).
-  // Opt-in (BL_TC=1): measured slower than the CUDA-core bulk at the C3 shape
-  // because the runtime runs tcgen05 kernels one CTA per SM, which leaves the
-  // serial search phases without a second CTA to overlap.
-  bool use_tc = use_tma && B <= 16 && std::getenv("BL_TC") != nullptr;
-  for (int i = 0; i < n && use_tc; ++i) use_tc = desc[i].need_tail == 0;
+  // Tensor-core bulk (both opt-in, both measured slower than the CUDA-core
+  // bulk at the C3 shape): 1 = tcgen05.mma (BL_TC=1; the
+  // runtime runs tcgen05 kernels one CTA per SM, which leaves the serial
+  // search phases without a second CTA to overlap), 2 = mma.sync m16n8k8
+  // tf32 (BL_MMA=1; two CTAs per SM, register accumulators).
+  int use_tc = !use_tma || B > 16 ? 0
+               : std::getenv("BL_TC") != nullptr  ? 1
+               : std::getenv("BL_MMA") != nullptr ? 2
+                                                  : 0;
+  for (int i = 0; i < n && use_tc; ++i)
+    if (desc[i].need_tail) use_tc = 0;
   if (use_tc && on_device) {
     // the grid allocation must cover the last block's overhang
     using RangeFn = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
@@ -561,13 +567,14 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     }
     CUdeviceptr b0 = 0;
     size_t sz = 0;
-    use_tc = range && range(&b0, &sz, reinterpret_cast<CUdeviceptr>(gbase)) == CUDA_SUCCESS &&
-             reinterpret_cast<CUdeviceptr>(gbase) + sizeof(float) * gtotal + gpad <= b0 + sz;
+    if (!(range && range(&b0, &sz, reinterpret_cast<CUdeviceptr>(gbase)) == CUDA_SUCCESS &&
+          reinterpret_cast<CUdeviceptr>(gbase) + sizeof(float) * gtotal + gpad <= b0 + sz))
+      use_tc = 0;
     cudaGetLastError();
   }
   // tcgen05 kernels run one CTA per SM (the runtime's occupancy for any
   // kernel using tcgen05.alloc): the tensor-core variant takes the deepest ring
-  int tma_stages = use_tma ? (use_tc ? bl::kTmaStagesMax : U <= 148 ? 6 : 4) : 0;
+  int tma_stages = use_tma ? (use_tc == 1 ? bl::kTmaStagesMax : U <= 148 ? 6 : 4) : 0;
   {
     // long utterances: fewer TMA stages (down to 2), then the non-TMA path,
     // before the plan is rejected (12 KB left for static shared memory);
@@ -579,10 +586,11 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     };
     while (use_tma && tma_stages > 2 && need(tma_stages) > lim) --tma_stages;
     if (use_tma && need(tma_stages) > lim) {
-      use_tma = use_tc = false;
+      use_tma = false;
+      use_tc = 0;
       tma_stages = 0;
     }
-    while (use_tma && !use_tc && U > 148 && tma_stages > 3 &&
+    while (use_tma && use_tc != 1 && U > 148 && tma_stages > 3 &&
            need(tma_stages) + 6 * 1024 > 113 * 1024)
       --tma_stages;
   }
@@ -664,7 +672,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   // certified psi half-width: the tensor-core bulk rounds the factors and
   // truncates the exponentials to tf32 (relative error <= 2^-11 + 2^-10 per
   // product, so <= 1.5e-3 on each sum): 2.5e-3 more
-  p.dpsi0 = (use_tc ? 3e-3 : 5e-4) * d->slack;
+  p.dpsi0 = (use_tc ? 3e-3 : 5e-4) * d->slack;  // (both tensor-core variants use tf32)
   p.dpsi1 = 1e-6 * d->slack;
   p.sc_order = d->sc_order;
   p.sc_nent = d->sc_nent;
@@ -679,7 +687,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   p.kub_smem = kub_smem;
   p.region_bytes = (int)region;
   p.use_tma = use_tma ? 1 : 0;
-  p.use_tc = use_tc ? 1 : 0;
+  p.use_tc = use_tc;
   if (use_tc) {
     p.mshift_stride = ((C + 511) / 512) * 512;
     d->mshift.ensure(sizeof(float) * 2 * (size_t)U * p.mshift_stride);
@@ -709,10 +717,12 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       const cuuint64_t strides[2] = {(cuuint64_t)V * sizeof(float), 128};
       const cuuint32_t box[3] = {32, 8, 16};
       const cuuint32_t estr[3] = {1, 1, 1};
+      // (mma.sync: the standard 128-byte swizzle, whose 16-byte chunks make
+      // the fragment loads conflict-free)
       r = encode(&p.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(gbase), dims,
                  strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                 CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                 use_tc == 1 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
       const cuuint64_t dims[2] = {(cuuint64_t)V, (cuuint64_t)(gtotal / V)};
       const cuuint64_t strides[1] = {(cuuint64_t)V * sizeof(float)};

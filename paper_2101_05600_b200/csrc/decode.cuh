@@ -56,7 +56,8 @@ struct KParams {
                      // with 32-byte-atom 128-byte swizzle (the MN-major tf32
                      // operand layout of tcgen05.mma)
   int use_tma, tma_stages;
-  int use_tc;        // tensor-core bulk (tcgen05.mma kind::tf32), see decode_kernel.cu
+  int use_tc;        // tensor-core bulk: 1 = tcgen05.mma kind::tf32 (TMEM), 2 = mma.sync
+                     // m16n8k8 tf32 (registers), see decode_kernel.cu
   float* mshift;     // use_tc: [2][U][mshift_stride] per-column exp shifts by step parity
   int mshift_stride;
   const UttDesc* utts;
@@ -143,8 +144,9 @@ __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, 
   p.phif = 0;
   // P3 factors: fp32 [Tmax][bmax] rows, or (tensor cores) the K-major tf32
   // operand, one 512 B chunk per 8 rows
-  p.kub = tc ? (size_t)kTcChunkBytes * (size_t)((Tmax + 7) / 8)
-             : align16(sizeof(float) * (size_t)Tmax * bmax);
+  // (tc: 1 = tcgen05 operand layout, 2 = mma.sync: fp32 rows, 1024-B aligned ring)
+  p.kub = tc == 1 ? (size_t)kTcChunkBytes * (size_t)((Tmax + 7) / 8)
+                  : align16(sizeof(float) * (size_t)Tmax * bmax);
   const size_t words = ((size_t)B * C + 31) / 32;
   p.ubits = kub_smem ? align16(p.kub + sizeof(float) * (size_t)B * C) : p.kub;
   if (kub_smem) {  // keys mode: every key, its flag, then the theta0 list

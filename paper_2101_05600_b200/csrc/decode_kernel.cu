@@ -484,12 +484,15 @@ __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
 }  // namespace
 
 // kMode 0: K1 slab by __ldg, every upper key in shared memory (keys mode);
-// 1: __ldg, keys filtered on chip (filter mode); 2: TMA slab, filter mode
+// 1: __ldg, keys filtered on chip (filter mode); 2: TMA slab, filter mode;
+// 3: TMA slab + tcgen05.mma tf32 bulk; 4: TMA slab + mma.sync tf32 bulk
 template <int BMAX, int kMode>
 __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
     decode_kernel(const __grid_constant__ KParams P) {
   constexpr bool kTma = kMode >= 2;
-  constexpr bool kTc = kMode == 3;  // K1 bulk on tcgen05.mma (kind::tf32), accumulators in TMEM
+  constexpr bool kTc = kMode == 3;   // K1 bulk on tcgen05.mma (kind::tf32), accumulators in TMEM
+  constexpr bool kMma = kMode == 4;  // K1 bulk on mma.sync m16n8k8 tf32, accumulators in registers
+  constexpr bool kShift = kTc || kMma;  // fixed per-step column shifts (no lazy rescale)
   constexpr bool keys_mode = kMode == 0;
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ Shared<BMAX> sh;
@@ -510,7 +513,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
 
   // dynamic smem carve-up (smem_plan, decode.cuh)
   const SmemPlan pl = smem_plan(P.Tmax, B, BMAX, C, P.caps, P.S, P.region_bytes, P.kub_smem,
-                                kTma ? P.tma_stages : 0, kTc ? 1 : 0);
+                                kTma ? P.tma_stages : 0, kTc ? 1 : kMma ? 2 : 0);
   double* phi = reinterpret_cast<double*>(dsm + pl.phi);    // [B][Tmax]
   unsigned char* region = dsm + pl.region;                  // aliased, region_bytes
   float* PhiF = reinterpret_cast<float*>(region + pl.phif);  // [Tmax][BMAX]
@@ -670,7 +673,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       }
     }
   }
-  if constexpr (kTc) {
+  if constexpr (kShift) {
     // The step-1 exp shift of every column: its max over all T frames (the
     // step-1 window is [1, T]); each later step takes the max over the rows
     // the next window can still reach while it streams its own (P3).
@@ -701,8 +704,11 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       for (int rr = 0; rr < 4; ++rr) {
         const int r = rg + 2 * rr;
         if (8 * k + r < T) {
-          const float4 x = *reinterpret_cast<const float4*>(
-              sb + r * 32 + (((((gq >> 1) ^ r) & 3) << 3) | ((gq & 1) << 2)));
+          // 16-byte chunk gq of row r: 32-byte-atom swizzle (tcgen05) or the
+          // standard 128-byte swizzle (mma.sync)
+          const int ph = kTc ? ((((gq >> 1) ^ r) & 3) << 3) | ((gq & 1) << 2)
+                             : ((gq ^ r) & 7) << 2;
+          const float4 x = *reinterpret_cast<const float4*>(sb + r * 32 + ph);
           mx.x = fmaxf(mx.x, x.x);
           mx.y = fmaxf(mx.y, x.y);
           mx.z = fmaxf(mx.z, x.z);
@@ -714,8 +720,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         // keep the per-stage use counts of P3 in step: the release count and
         // the MMA-done barrier's phase (no MMA ran on this use)
         cons[st] += kNWarp;
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mmad[st]))
-                     : "memory");
+        if (kTc)
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mmad[st]))
+                       : "memory");
         if (j + NST < J) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           issue0(j + NST, g + NST);
@@ -856,6 +863,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
                 // K-major tf32 operand: chunk i/8, 8-row N group, 16-byte K chunk
                 PhiF[(i >> 3) * 128 + (j >> 3) * 64 + ((i & 7) >> 2) * 32 + (j & 7) * 4 +
                      (i & 3)] = tf32_rna(f);
+              } else if constexpr (kMma) {
+                PhiF[(size_t)i * BMAX + j] = tf32_rna(f);
               } else {
                 PhiF[(size_t)i * BMAX + j] = f;
               }
@@ -1185,6 +1194,187 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             const float th = warp_bound(tile < 3 || (tile & 3) == 0);
             if (acta && kmax >= th)
               emit_keys(ca, cb, actb, S0, S1, ma, actb ? mb : gf, ra, rb, true, th, kmax);
+          }
+        }
+        tma_jobs += J;
+      } else if constexpr (kMma) {
+        // K1 bulk on the warp-level tensor cores (mma.sync m16n8k8 tf32):
+        // for a 512-column tile, S[c][j] = sum_t exp(L[t,c] - m_c) a_j[t] is a
+        // [512 x W] . [W x 16] product. Warp w owns columns 64w .. 64w+63
+        // (swizzle blocks 2w, 2w+1 of the stage); lane (g, t) (g = lane/4,
+        // t = lane%4) loads, per 8-row chunk, rows t and t+4 of the 16-byte
+        // chunk chA(g) of both blocks (the standard 128-byte swizzle makes
+        // these loads conflict-free), exponentiates them against the fixed
+        // utterance's column maxima (the step-1 pass: a valid shift for every
+        // window, all of them lie inside [1, T]; no lazy rescale) and
+        // feeds them as A fragments: m-tile e has m = g <-> block 2w column e
+        // of the chunk and m = g+8 <-> block 2w+1, k = t, t+4 <-> the two rows;
+        // B fragments are the parents' factors (n = g, g+8). The accumulators
+        // stay in registers: lane (g, t) ends the tile with S for its 8
+        // columns x parents 2t, 2t+1, 8+2t, 9+2t. Stages are released per
+        // warp as in the CUDA-core variant. Two CTAs per SM as before.
+        const int nch = (W + 7) >> 3;
+        const int ntile = (C + 511) >> 9;
+        const int J = ntile * nch;
+        const int NST = P.tma_stages;
+        const int urow = ud.row0 + s - 1;
+        auto issue = [&](int j, unsigned g) {
+          const int st = (int)(g % (unsigned)NST), tile = j / nch, k = j - tile * nch;
+          mbar_expect_tx(&mbar[st], kTmaStageBytes);
+          tma_load_3d(tc_stg + (size_t)st * kTmaStageBytes, &P.tmap, 0, urow + k * 8, tile * 16,
+                      &mbar[st]);
+        };
+        if (tid == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          for (int j = 0; j < NST && j < J; ++j) issue(j, tma_jobs + j);
+        }
+        const int g8 = lane >> 2, t4 = lane & 3;
+        const int chA = (g8 & 1) * 4 + (g8 >> 1);  // this lane's 16-byte chunk in each block
+        // the utterance's column maxima over all T frames (step-1 pass)
+        const float* msh = P.mshift + ((size_t)1 * P.U + u) * P.mshift_stride;
+        constexpr float kL2e = 1.44269504088896341f;
+        float acc[4][2][4];  // [m-tile e][n-tile h][fragment]
+        // this lane's parents: n-tile h, fragment pair -> 8h + 2t + {0, 1}
+        for (int j = 0; j < J; ++j) {
+          const unsigned g = tma_jobs + j;
+          const int st = (int)(g % (unsigned)NST);
+          const int tile = j / nch, k = j - tile * nch;
+          const int col0 = tile * 512 + warp * 64 + chA * 4;  // block 2w; block 2w+1 is +32
+          if (k == 0) {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+#pragma unroll
+              for (int h = 0; h < 2; ++h)
+#pragma unroll
+                for (int f = 0; f < 4; ++f) acc[e][h][f] = 0.f;
+          }
+          // the shifts of the own columns (L1-resident; reloaded per chunk
+          // rather than held in registers across the tile)
+          const float4 ma = *reinterpret_cast<const float4*>(msh + col0);
+          const float4 mb = *reinterpret_cast<const float4*>(msh + col0 + 32);
+          const float mlc[8] = {ma.x * kL2e, ma.y * kL2e, ma.z * kL2e, ma.w * kL2e,
+                                mb.x * kL2e, mb.y * kL2e, mb.z * kL2e, mb.w * kL2e};
+          mbar_wait(&mbar[st], (g / (unsigned)NST) & 1u);
+          const float* blk =
+              reinterpret_cast<const float*>(tc_stg + (size_t)st * kTmaStageBytes) + warp * 512;
+          float pa[2][8];  // [row pair rr][own column]: exp(L - m) as tf32
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int r = t4 + 4 * rr;
+            const int fr = 8 * k + r;  // frame s + fr
+            const int ph = r * 32 + (((chA ^ r) & 7) << 2);
+            const float4 xa = *reinterpret_cast<const float4*>(blk + ph);
+            const float4 xb = *reinterpret_cast<const float4*>(blk + 256 + ph);
+            const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+            const bool valid = fr < W;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              pa[rr][q] = valid ? tf32_rna(ex2_ftz(fmaf(xv[q], kL2e, -mlc[q]))) : 0.f;
+          }
+          // B fragments: factors of parents 8h + g at rows t, t+4 of the chunk
+          unsigned bf[2][2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int rr = 0; rr < 2; ++rr) {
+              const int row = 8 * k + t4 + 4 * rr, par = 8 * h + g8;
+              bf[h][rr] = (par < BMAX && row < W)
+                              ? __float_as_uint(PhiF[(size_t)row * BMAX + par])
+                              : 0u;
+            }
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const unsigned a0 = __float_as_uint(pa[0][e]), a1 = __float_as_uint(pa[0][4 + e]);
+            const unsigned a2 = __float_as_uint(pa[1][e]), a3 = __float_as_uint(pa[1][4 + e]);
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              asm volatile(
+                  "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, "
+                  "{%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                  : "+f"(acc[e][h][0]), "+f"(acc[e][h][1]), "+f"(acc[e][h][2]),
+                    "+f"(acc[e][h][3])
+                  : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bf[h][0]), "r"(bf[h][1]));
+          }
+          // stage release per warp (as the CUDA-core variant)
+          __syncwarp();
+          if (lane == 0) {
+            const int done = atomicAdd(&cons[st], 1);
+            if (done == (int)(g / (unsigned)NST) * kNWarp + kNWarp - 1 && j + NST < J) {
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              issue(j + NST, g + NST);
+            }
+          }
+          if (k == nch - 1) {  // tile epilogue: keys of own columns
+            // two passes like emit_keys: bounds (l1/l2, column minima) first,
+            // then the raw-list emission against the warp's running bound
+            float kmax = -INFINITY;
+            for (int pass = 0; pass < 2; ++pass) {
+              float th = 0.f;
+              if (pass == 1) {
+                th = warp_bound(tile < 3 || (tile & 3) == 0);
+                if (!(kmax >= th)) break;
+              }
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {  // own column q: block half q/4, element q%4
+                const int e = q & 3, hb = q >> 2;
+                const int c = col0 + hb * 32 + e;
+                const bool cin = c < C;
+                const float m = cin ? msh[c] : gf;
+                const float rs =
+                    (row_same >= 0 && cin) ? P.sc_rowsf[(size_t)row_same * V + c] : 0.f;
+                float cmin = INFINITY;
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                  for (int f1 = 0; f1 < 2; ++f1) {
+                    const int qp = 8 * h + 2 * t4 + f1;  // parent of fragment 2*hb + f1
+                    if (!cin || qp >= nb || qp >= BMAX) continue;
+                    if (c == sh.b_last[cur][qp]) {  // the repeat column is scored exactly
+                      cmin = -INFINITY;
+                      continue;
+                    }
+                    const float Sq = acc[e][h][2 * hb + f1];
+                    const float r =
+                        row_same >= 0 ? rs : P.sc_rowsf[(size_t)sh.b_row[cur][qp] * V + c];
+                    const bool under = lam_pos && !(Sq >= 7.888609052210118e-31f);  // 2^-100
+                    const float lg = under ? -68.62157f : lg2_ftz(Sq) * 0.693147180559945309f;
+                    const float kbq = sh.kb[qp];
+                    const float key = lam_pos ? kbq + klamf * (m + lg) + r : kbq + r;
+                    const float hh = hw + fabsf(key) * 2.4e-7f;
+                    float klo = under ? -INFINITY : key - hh, kub_v = key + hh;
+                    bool und = under;
+                    if (r == -INFINITY || (lam_pos && (sh.mzero[qp] != 0 || m == kgf))) {
+                      klo = kub_v = kZeroKey;
+                      und = false;
+                    }
+                    if (pass == 0) {
+                      kmax = fmaxf(kmax, kub_v);
+                      cmin = fminf(cmin, klo);
+                      if (klo > l2) {
+                        if (klo > l1) {
+                          l2 = l1;
+                          l1 = klo;
+                        } else {
+                          l2 = klo;
+                        }
+                      }
+                    } else if (kub_v >= th) {
+                      const int idx = atomicAdd(&sh.n_raw, 1);
+                      if (idx < kRawCap)
+                        rawl[idx] = make_uint2(__float_as_uint(kub_v),
+                                               (und ? 0x80000000u : 0u) | ((unsigned)qp << 24) |
+                                                   (unsigned)c);
+                    }
+                  }
+                if (pass == 0 && nb >= B) {
+                  // a column's bound needs all B parents: min over the 4 lanes
+                  // sharing it (each holds 4 of the 16 parent slots)
+                  cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, 1));
+                  cmin = fminf(cmin, __shfl_xor_sync(0xffffffffu, cmin, 2));
+                  if (cin) lcol = fmaxf(lcol, cmin);
+                }
+              }
+            }
           }
         }
         tma_jobs += J;
@@ -2079,14 +2269,14 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
 }
 
 // ------------------------------------------------------------ launchers
-// The four kernel modes compile as separate translation units (Makefile:
-// decode_kernel.cu with -DDK_MODE=0..3); each defines its mode's launcher
+// The kernel modes compile as separate translation units (Makefile:
+// decode_kernel.cu with -DDK_MODE=0..4); each defines its mode's launcher
 // over the beam instantiations, and mode 0's unit also holds the dispatch.
 size_t decode_smem_bytes(const KParams& p);
 int bmax_for(int B);
 
 static int mode_of(const KParams& p) {
-  return p.use_tc ? 3 : p.use_tma ? 2 : (p.kub_smem ? 0 : 1);
+  return p.use_tc == 2 ? 4 : p.use_tc == 1 ? 3 : p.use_tma ? 2 : (p.kub_smem ? 0 : 1);
 }
 
 template <int BMAX, int kMode>
@@ -2158,12 +2348,14 @@ cudaError_t launch_mode0(int, const KParams&, cudaStream_t);
 cudaError_t launch_mode1(int, const KParams&, cudaStream_t);
 cudaError_t launch_mode2(int, const KParams&, cudaStream_t);
 cudaError_t launch_mode3(int, const KParams&, cudaStream_t);
+cudaError_t launch_mode4(int, const KParams&, cudaStream_t);
 size_t static_mode0(int);
 size_t static_mode1(int);
 size_t static_mode2(int);
 size_t static_mode3(int);
+size_t static_mode4(int);
 
-#if DK_MODE == 3  // the tensor-core bulk holds at most 16 parents
+#if DK_MODE >= 3  // the tensor-core bulks hold at most 16 parents
 #define BL_WIDE_CASES(M)
 #define BL_WIDE_STATIC(M)
 #else
@@ -2183,8 +2375,10 @@ BL_MODE_FNS(1)
 BL_MODE_FNS(2)
 #elif DK_MODE == 3
 BL_MODE_FNS(3)
+#elif DK_MODE == 4
+BL_MODE_FNS(4)
 #else
-#error "compile decode_kernel.cu with -DDK_MODE=0..3"
+#error "compile decode_kernel.cu with -DDK_MODE=0..4"
 #endif
 
 #if DK_MODE == 0
@@ -2223,6 +2417,7 @@ size_t decode_smem_bytes(const KParams& p) {
 size_t decode_static_smem(const KParams& p) {
   const int b = bmax_for(p.B);
   switch (mode_of(p)) {
+    case 4: return b <= 16 ? static_mode4(b) : 0;
     case 3: return b <= 16 ? static_mode3(b) : 0;
     case 2: return static_mode2(b);
     case 1: return static_mode1(b);
@@ -2234,6 +2429,7 @@ cudaError_t launch_decode(const KParams& p, cudaStream_t st) {
   const int b = bmax_for(p.B);
   if (b == 0) return cudaErrorInvalidValue;
   switch (mode_of(p)) {
+    case 4: return b <= 16 ? launch_mode4(b, p, st) : cudaErrorInvalidValue;
     case 3: return b <= 16 ? launch_mode3(b, p, st) : cudaErrorInvalidValue;
     case 2: return launch_mode2(b, p, st);
     case 1: return launch_mode1(b, p, st);
