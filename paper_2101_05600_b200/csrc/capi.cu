@@ -508,7 +508,13 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     gtotal += (size_t)T * V;
   }
   const int Tp = (Tmax + 2) & ~1;
-  const int caps = std::min(2 * B + 16, bl::kNT);
+  // contender slots: 3B+16 (BL_CAPS_MULT=k gives kB+16, for sweeps). 2B+16
+  // overflowed into the exact fallback on ~0.7% of beam-20 steps (flat
+  // posteriors): 3B+16 cuts beam 20 at 10 s x 512 from 528 to 330 ms; 4B+16
+  // is slower again (more chain warps, less staging room)
+  static const int caps_mult =
+      std::getenv("BL_CAPS_MULT") ? std::atoi(std::getenv("BL_CAPS_MULT")) : 3;
+  const int caps = std::min(std::max(2, caps_mult) * B + 16, bl::kNT);
   const int nbest = std::max(1, d->nbest);
   const int rs = bl::res_stride(S, nbest);
   const int U = n;

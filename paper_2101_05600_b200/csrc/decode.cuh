@@ -66,7 +66,7 @@ struct KParams {
   int Tmax;        // max T over the batch
   int Tp;          // stride of one gamma array (>= Tmax + 1)
   int S;           // max max_steps over the batch
-  int caps;        // contender states per area (2B + 16)
+  int caps;        // contender states per area (3B + 16)
   // DecoderConfig
   double lambda;
   double eos_dend;

@@ -166,6 +166,19 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       "r"(parity)
       : "memory");
 }
+// wait with a suspend-time hint: a warp waiting for its stage's data sleeps
+// in the barrier unit instead of re-issuing try_wait (the spin loop was ~8%
+// of the streaming loop's instructions; the other CTA on the SM gets the
+// issue slots)
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 // bounded wait (tensor-core variant): a barrier that never completes reports
 // where and traps instead of hanging the device
 __device__ __noinline__ void mbar_wait_dbg(unsigned long long* bar, unsigned parity, int tag,
@@ -1405,10 +1418,14 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         float m0 = gf, m1 = gf, r0s = 0.f, r1s = 0.f;
         const int colb = ((2 * tid) >= kTmaBoxCols ? kTmaRows * kTmaBoxCols : 0) +
                          ((2 * tid) & (kTmaBoxCols - 1));
+        // job counters kept incrementally (a runtime division per job and
+        // thread was ~10% of this loop's instructions): stage, its use round
+        // (mbarrier parity, release count), tile and chunk
+        int st = (int)(tma_jobs % (unsigned)NST);
+        unsigned rnd = tma_jobs / (unsigned)NST;
+        int tile = 0, k = 0;
         for (int j = 0; j < J; ++j) {
           const unsigned g = tma_jobs + j;
-          const int st = (int)(g % (unsigned)NST);
-          const int tile = j / nch, k = j - tile * nch;
           const int c0 = tile * 2 * kNT + 2 * tid;
           const bool active = c0 < C, two = c0 + 1 < C;
           if (k == 0) {
@@ -1418,7 +1435,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             r0s = (row_same >= 0 && active) ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
             r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
           }
-          mbar_wait(&mbar[st], (g / (unsigned)NST) & 1u);
+          mbar_wait_sleep(&mbar[st], rnd & 1u);
           if (active) {
             const float* sb = stages + (size_t)st * (kTmaStageBytes / 4) + colb;
             const int nrow = min(kTmaRows, W - k * kTmaRows);
@@ -1462,7 +1479,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           __syncwarp();
           if (lane == 0) {
             const int done = atomicAdd(&cons[st], 1);
-            if (done == (int)(g / (unsigned)NST) * kNWarp + kNWarp - 1 && j + NST < J) {
+            if (done == (int)rnd * kNWarp + kNWarp - 1 && j + NST < J) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
               issue(j + NST, g + NST);
             }
@@ -1474,6 +1491,14 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             const float th = warp_bound(tile < 3 || (tile & 3) == 0);
             if (active && kmax >= th)
               emit_keys(c0, c0 + 1, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, true, th, kmax);
+          }
+          if (++st == NST) {
+            st = 0;
+            ++rnd;
+          }
+          if (++k == nch) {
+            k = 0;
+            ++tile;
           }
         }
         tma_jobs += J;
