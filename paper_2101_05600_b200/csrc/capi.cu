@@ -412,12 +412,28 @@ int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
                       static_cast<const int*>(d->nb_live.p) + p.u0, d->cfg.ctc_weight, st));
       p.sc_rows = bl::dec_att(d->net);
       p.sc_rowsf = bl::dec_attf(d->net);
+      p.net_lse = bl::dec_lse(d->net);
+      p.net_logits = p.net_lse ? bl::dec_logits(d->net) : nullptr;
       launches += bl::dec_launches_per_step(d->net);
       if (d->record) {
-        rec_rows.emplace_back((size_t)p.U * B * V);
-        CK(cudaMemcpyAsync(rec_rows.back().data(), p.sc_rows, sizeof(double) * rec_rows.back().size(),
-                           cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
+        const size_t rows = (size_t)p.U * B;
+        rec_rows.emplace_back(rows * V);
+        if (p.net_lse) {  // the rows the search used: (double)logit - lse
+          std::vector<float> lg(rows * V);
+          std::vector<double> ls(rows);
+          CK(cudaMemcpyAsync(lg.data(), p.net_logits, sizeof(float) * lg.size(),
+                             cudaMemcpyDeviceToHost, st));
+          CK(cudaMemcpyAsync(ls.data(), p.net_lse, sizeof(double) * rows, cudaMemcpyDeviceToHost,
+                             st));
+          CK(cudaStreamSynchronize(st));
+          for (size_t r = 0; r < rows; ++r)
+            for (int c = 0; c < V; ++c)
+              rec_rows.back()[r * V + c] = (double)lg[r * V + c] - ls[r];
+        } else {
+          CK(cudaMemcpyAsync(rec_rows.back().data(), p.sc_rows,
+                             sizeof(double) * rec_rows.back().size(), cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+        }
       }
     }
     CK(bl::launch_decode(p, st));
@@ -514,7 +530,12 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   // is slower again (more chain warps, less staging room)
   static const int caps_mult =
       std::getenv("BL_CAPS_MULT") ? std::atoi(std::getenv("BL_CAPS_MULT")) : 3;
-  const int caps = std::min(std::max(2, caps_mult) * B + 16, bl::kNT);
+  // The P6 chains take (caps + 15) / 16 warps; the walk (P8) that overlaps
+  // them needs one thread per selected item (<= B + bmax), so the chain warps
+  // leave at least ceil((B + bmax) / 32) warps to it.
+  const int bmax0 = bl::bmax_for(B);
+  const int chain_warps = bl::kNWarp - (B + bmax0 + 31) / 32;
+  const int caps = std::min({std::max(2, caps_mult) * B + 16, bl::kNT, 16 * chain_warps});
   const int nbest = std::max(1, d->nbest);
   const int rs = bl::res_stride(S, nbest);
   const int U = n;

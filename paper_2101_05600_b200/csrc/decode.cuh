@@ -84,6 +84,10 @@ struct KParams {
   const int* sc_row;     // row of entry k
   const double* sc_rows; // [rows][V]; row 0 = uniform fallback
   const float* sc_rowsf;  // [rows][V]: (float)((1-lambda)*row), -inf where row is log-zero
+  // network scorer with the fused log-softmax: rows are logits [rows][V]
+  // (fp32) minus net_lse[row] (fp64); sc_rows / sc_rowsf unused then
+  const float* net_logits;
+  const double* net_lse;
   // workspace (per-utterance slices)
   double* gam;     // [U][2][caps][2][Tp]
   double* Ftab;    // [U][Tp][C]   eos tail tables (need_tail only)

@@ -88,6 +88,23 @@ __device__ __forceinline__ double gread(const double* a, int i, int vlo, int cov
   return (i < vlo || i > cov) ? kLogZero : a[i];
 }
 
+// scorer rows: the table (Uniform / Table / Loop rows), or for the network
+// scorer the output GEMM's fp32 logits and the row's fp64 log-normaliser:
+// att = (double)logit - lse, attf = (float)((1 - lambda) att) -- the values
+// materialised rows would hold. The fp32 attf rows (every key reads one) are
+// materialised by the log-softmax kernel unless it is fused into the GEMM.
+__device__ __forceinline__ double att_at(const KParams& P, int row, int c) {
+  if (P.net_lse) return (double)P.net_logits[(size_t)row * P.V + c] - P.net_lse[row];
+  return P.sc_rows[(size_t)row * P.V + c];
+}
+__device__ __forceinline__ float attf_at(const KParams& P, int row, int c) {
+  if (P.net_lse && !P.sc_rowsf) {
+    const double v = (double)P.net_logits[(size_t)row * P.V + c] - P.net_lse[row];
+    return P.lambda >= 1.0 ? 0.f : (float)((P.lambda <= 0.0 ? 1.0 : 1.0 - P.lambda) * v);
+  }
+  return P.sc_rowsf[(size_t)row * P.V + c];
+}
+
 __device__ __forceinline__ float ex2_ftz(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -824,9 +841,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           const double fl = last >= 0 ? Ft[(size_t)cov * C + last] : Gt[cov];
           ee = log_add(log_mul(gnp[cov], fl), log_mul(gbp[cov], Gt[cov]), tb);
         }
-        const double* row = P.sc_rows + (size_t)sh.b_row[cur][j] * V;
         Item it;
-        it.score = mix_joint(lam, ee, __dadd_rn(sh.b_att[cur][j], row[C]));
+        it.score = mix_joint(lam, ee, __dadd_rn(sh.b_att[cur][j], att_at(P, sh.b_row[cur][j], C)));
         it.parent = j;
         it.token = C;
         it.tau = it.taut = 0;
@@ -1006,7 +1022,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
               bool under = false;
               if (c != last) {
                 const float r = row_same >= 0 ? (cc ? r1s : r0s)
-                                              : P.sc_rowsf[(size_t)sh.b_row[cur][q] * V + c];
+                                              : attf_at(P, sh.b_row[cur][q], c);
                 // same arithmetic as kbq + lamf * (m + __logf(Sq)) + r for a
                 // normal Sq; below 2^-100 only the certified upper bound
                 // with log(Sq) <= log(2^-99) is kept
@@ -1200,8 +1216,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
               S1[q] = make_float2(v1[2 * q], v1[2 * q + 1]);
             }
             const float ma = msh[ca], mb = msh[cb];
-            const float ra = (row_same >= 0 && acta) ? P.sc_rowsf[(size_t)row_same * V + ca] : 0.f;
-            const float rb = (row_same >= 0 && actb) ? P.sc_rowsf[(size_t)row_same * V + cb] : 0.f;
+            const float ra = (row_same >= 0 && acta) ? attf_at(P, row_same, ca) : 0.f;
+            const float rb = (row_same >= 0 && actb) ? attf_at(P, row_same, cb) : 0.f;
             float kmax = -INFINITY;
             if (acta) emit_keys(ca, cb, actb, S0, S1, ma, actb ? mb : gf, ra, rb, false, 0.f, kmax);
             const float th = warp_bound(tile < 3 || (tile & 3) == 0);
@@ -1334,7 +1350,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
                 const bool cin = c < C;
                 const float m = cin ? msh[c] : gf;
                 const float rs =
-                    (row_same >= 0 && cin) ? P.sc_rowsf[(size_t)row_same * V + c] : 0.f;
+                    (row_same >= 0 && cin) ? attf_at(P, row_same, c) : 0.f;
                 float cmin = INFINITY;
 #pragma unroll
                 for (int h = 0; h < 2; ++h)
@@ -1348,7 +1364,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
                     }
                     const float Sq = acc[e][h][2 * hb + f1];
                     const float r =
-                        row_same >= 0 ? rs : P.sc_rowsf[(size_t)sh.b_row[cur][qp] * V + c];
+                        row_same >= 0 ? rs : attf_at(P, sh.b_row[cur][qp], c);
                     const bool under = lam_pos && !(Sq >= 7.888609052210118e-31f);  // 2^-100
                     const float lg = under ? -68.62157f : lg2_ftz(Sq) * 0.693147180559945309f;
                     const float kbq = sh.kb[qp];
@@ -1432,8 +1448,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
 #pragma unroll
             for (int q = 0; q < kP; ++q) S0[q] = S1[q] = make_float2(0.f, 0.f);
             m0 = m1 = gf;
-            r0s = (row_same >= 0 && active) ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
-            r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
+            r0s = (row_same >= 0 && active) ? attf_at(P, row_same, c0) : 0.f;
+            r1s = (row_same >= 0 && two) ? attf_at(P, row_same, c0 + 1) : 0.f;
           }
           mbar_wait_sleep(&mbar[st], rnd & 1u);
           if (active) {
@@ -1516,8 +1532,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         for (int q = 0; q < kP; ++q) S0[q] = S1[q] = make_float2(0.f, 0.f);
         if (act) {
         const long long tq1 = clock64();
-        r0s = row_same >= 0 ? P.sc_rowsf[(size_t)row_same * V + c0] : 0.f;
-        r1s = (row_same >= 0 && two) ? P.sc_rowsf[(size_t)row_same * V + c0 + 1] : 0.f;
+        r0s = row_same >= 0 ? attf_at(P, row_same, c0) : 0.f;
+        r1s = (row_same >= 0 && two) ? attf_at(P, row_same, c0 + 1) : 0.f;
         const float* col = grid + (size_t)(s - 1) * V + c0;
         // columns c0 and c0+1 are both inside the row (c0 + 1 <= C = V-1,
         // the blank), so the pair is always loaded (the odd column of an odd
@@ -1851,7 +1867,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
               P, sh, u, cur, j, c, s, e, grid, phi + (size_t)j * P.Tmax, gnc, gbc, &tau, &taut,
               tb);
           const double att = __dadd_rn(sh.b_att[cur][j],
-                                       P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+                                       att_at(P, sh.b_row[cur][j], c));
           items[q].score = mix_joint(lam, psi, att);
           items[q].tau = tau;
           items[q].taut = taut;
@@ -1879,7 +1895,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             }
             const double psi = M == -HUGE_VAL ? kLogZero : M + log_pos(S, tb);
             const double att = __dadd_rn(sh.b_att[cur][j],
-                                         P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+                                         att_at(P, sh.b_row[cur][j], c));
             items[q].score = mix_joint(lam, psi, att);
           }
         }
@@ -1931,7 +1947,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           sc = items[caps + j].score;
         } else {
           const double att = __dadd_rn(sh.b_att[cur][j],
-                                       P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+                                       att_at(P, sh.b_row[cur][j], c));
           const double psi = lam <= 0.0 ? kLogZero
                                         : psi_only<BMAX>(P, sh, u, cur, j, c, s, e, grid,
                                                          phi + (size_t)j * P.Tmax, tb);
@@ -2032,7 +2048,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           sh.b_taut[nxt][k] = x.taut;
           sh.b_last[nxt][k] = c;
           sh.b_att[nxt][k] = __dadd_rn(sh.b_att[cur][j],
-                                       P.sc_rows[(size_t)sh.b_row[cur][j] * V + c]);
+                                       att_at(P, sh.b_row[cur][j], c));
           sh.b_joint[nxt][k] = x.score;
           sh.b_row[nxt][k] = P.net_rows ? u * B + k : lookup_row(P, hist_c, l, l - 1, j, c);
           sh.child_q[k] = x.slot;

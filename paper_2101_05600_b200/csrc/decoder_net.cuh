@@ -27,14 +27,19 @@ const DecSpec& dec_spec(const DecoderNet* n);
 cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16* memory, int T2,
                         cudaStream_t st);
 // Step l (1-based): reads the hypotheses' tokens / ancestry from the search
-// history (hist [U][hstride] with hstride = (S_search+1)*B), writes
-// att [U*B][V] (fp64 log-probs) and attf [U*B][V] = (float)((1-lambda)*att).
+// history (hist [U][hstride] with hstride = (S_search+1)*B), writes the
+// output logits [U*B][V] (fp32), attf [U*B][V] = (float)((1-lambda)*att)
+// and lse [U*B] (fp64), with att = (double)logit - lse (the fp64 rows
+// themselves only with BL_LOG_SOFTMAX set; with BL_FUSED_LOG_SOFTMAX the
+// output GEMM's epilogue computes lse and attf is not written).
 // nb_live [U]: live hypotheses entering step l (written by the search kernel;
 // ignored at l = 1, where every utterance has the empty prefix only).
 cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, const int* nb_live,
                      double lambda, cudaStream_t st);
-const double* dec_att(const DecoderNet* n);
-const float* dec_attf(const DecoderNet* n);
+const double* dec_att(const DecoderNet* n);   // nullptr unless BL_LOG_SOFTMAX
+const float* dec_attf(const DecoderNet* n);   // nullptr when fused into the GEMM
+const float* dec_logits(const DecoderNet* n);
+const double* dec_lse(const DecoderNet* n);   // nullptr with BL_LOG_SOFTMAX
 int dec_launches_per_step(const DecoderNet* n);
 
 }  // namespace bl

@@ -11,6 +11,10 @@ enum GemmEpilogue : int {
   kRelu = 1,      // out = max(acc + bias, 0)
   kResidual = 2,  // out_f32 += acc + bias   (in place residual stream)
   kScalePe = 3,   // out = (acc + bias) * scale + pe[row % pe_rows][col]
+  kLsePart = 4,   // out = acc + bias, plus per (row, 128-column slot) the
+                  // partial log-softmax {max (as double), sum exp(x - max)
+                  // (fp64)} in lse_part[row][lse_stride] (a tile writes its
+                  // first slot; the caller zeroes the buffer)
 };
 
 // C[M,N] = A[M,K] . B[N,K]^T; A, B bf16 K-major (row strides lda/ldb in
@@ -29,6 +33,8 @@ struct GemmDesc {
   float scale = 1.f;
   const float* pe = nullptr;
   int pe_rows = 1;
+  double* lse_part = nullptr;  // kLsePart: [M][lse_stride][2]
+  int lse_stride = 0;
 };
 
 cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t st);

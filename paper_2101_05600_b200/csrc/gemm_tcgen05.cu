@@ -97,6 +97,8 @@ struct GemmArgs {
   float scale;
   const float* pe;
   int pe_rows;
+  double* lse_part;  // kLsePart
+  int lse_stride;
   // implicit conv2 (kConv): A tiles are 4D TMA boxes over the channel-last
   // conv1 output; a tile covers `tpt` output frames x F2 bins = `rows` rows
   int S, T2, F2, tpt, tps, ktin, rows;
@@ -209,6 +211,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int rbase = m0 + q * 32, row = rbase + lane;
       const bool row_ok = row < g.M;
+      float lm = -INFINITY;  // kLsePart: this row's running max over the tile
+      double ls = 0.0;       //           and sum of exp(x - lm)
       int qrows = 32, cy = 0, cz = 0;
       if (kConv) {
         const int mt = tile / tiles_n;
@@ -271,6 +275,19 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (col0 + j < g.N) x[j] = x[j] * sc + src[j];
           }
         }
+        if (g.mode == kLsePart) {  // fused log-softmax: partial max and sum of exp
+          float cm = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < g.N) cm = fmaxf(cm, x[j]);
+          if (cm > lm) {
+            ls *= exp((double)lm - (double)cm);
+            lm = cm;
+          }
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j < g.N) ls += (double)expf(x[j] - lm);
+        }
         unsigned char* sb = stg + (nchunk & 1) * kStgBytes;
         if (lane == 0) bulk_wait_read<1>();  // the store that last used sb has read it
         __syncwarp();
@@ -300,6 +317,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           bulk_commit();
         }
         (void)kCW32;
+      }
+      if (g.mode == kLsePart && row_ok && ls > 0.0) {
+        double* pp = g.lse_part + ((size_t)row * g.lse_stride + n0 / 128) * 2;
+        pp[0] = (double)lm;
+        pp[1] = ls;
       }
       tc_fence_before();
       __syncwarp();
@@ -384,6 +406,7 @@ GemmArgs args_of(const GemmDesc& d) {
   GemmArgs g{};
   g.M = d.M; g.N = d.N; g.K = d.K; g.mode = d.mode; g.bias = d.bias; g.out_f32 = d.out_f32;
   g.out_bf16 = d.out_bf16; g.ldo = d.ldo; g.scale = d.scale; g.pe = d.pe; g.pe_rows = d.pe_rows;
+  g.lse_part = d.lse_part; g.lse_stride = d.lse_stride;
   return g;
 }
 
@@ -395,6 +418,8 @@ cudaError_t gemm_bf16(const GemmDesc& d, cudaStream_t st) {
   if ((d.out_bf16 != nullptr) == (d.out_f32 != nullptr)) return cudaErrorInvalidValue;
   if (d.out_bf16 ? (d.ldo % 8) : (d.ldo % 4)) return cudaErrorInvalidValue;
   if ((d.mode == kResidual || d.mode == kScalePe) && !d.out_f32) return cudaErrorInvalidValue;
+  if (d.mode == kLsePart && (!d.out_f32 || !d.lse_part || d.lse_stride < (d.N + 127) / 128))
+    return cudaErrorInvalidValue;
   CUtensorMap tA;
   if (!make_map(&tA, d.A, d.M, d.K, d.lda, kBM)) return cudaErrorInvalidValue;
   const GemmArgs g = args_of(d);

@@ -14,4 +14,4 @@ for T, n in ((249, 512), (124, 512)):
         dec.decode_raw(descs, on_device=True)
         t0 = time.perf_counter(); dec.decode_raw(descs, on_device=True); ms = (time.perf_counter() - t0) * 1e3
         st = dec.last_stats
-        print(f"caps_mult={os.environ.get('BL_CAPS_MULT', 2)} T={T} beam={beam} n={n}: {ms:.1f} ms kernel {st['kernel_ms']:.1f} fallback {st['fallback_steps']} contenders/step {st['contenders']/st['steps']:.1f}", flush=True)
+        print(f"caps_mult={os.environ.get('BL_CAPS_MULT', 3)} T={T} beam={beam} n={n}: {ms:.1f} ms kernel {st['kernel_ms']:.1f} fallback {st['fallback_steps']} contenders/step {st['contenders']/st['steps']:.1f}", flush=True)
