@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -363,6 +364,173 @@ __global__ void __launch_bounds__(128)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
+// The same for 256 < T <= 512 (20 s segments: T = 499): K and V are two
+// 256-row TMA boxes each; S = Q K^T is two M=128 N=256 MMAs into TMEM columns
+// [0, 512) (tcgen05 kernels run one CTA per SM, so the whole TMEM is free);
+// the softmax takes its max over all 512 columns, then P goes through shared
+// memory one 256-key half at a time (64 KB, aliasing the consumed Q/K tiles):
+// O = P0 V0, then O += P1 V1 once the first product has read P0. O lives in
+// TMEM columns [0, 64), which only the first half of S occupied.
+constexpr int kAtt2K = 512;
+constexpr int kAtt2Smem = 16384 /*Q*/ + 65536 /*K*/ + 65536 /*V*/ + 1024;
+
+__global__ void __launch_bounds__(128)
+    attention_tc512_kernel(const __grid_constant__ CUtensorMap tQ,
+                           const __grid_constant__ CUtensorMap tKV, int T, int d,
+                           __nv_bfloat16* __restrict__ out) {
+  using namespace tc;
+  extern __shared__ __align__(1024) unsigned char araw[];
+  unsigned char* sm = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(araw) + 1023) & ~(uintptr_t)1023);
+  unsigned char* Qs = sm;
+  unsigned char* Ks = sm + 16384;          // 2 x [256 x 64] bf16
+  unsigned char* Ps = sm;                  // 4 x [128 x 64] bf16 = one half of P
+  unsigned char* Vs = sm + 16384 + 65536;  // 2 x [256 x 64] bf16
+  __shared__ __align__(8) uint64_t bar_ld, bar_mma;
+  __shared__ uint32_t tbase;
+  const int n = blockIdx.x, h = blockIdx.y, qt = blockIdx.z;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int row0 = n * T;
+  if (tid == 0) {
+    mb_init(&bar_ld, 1);
+    mb_init(&bar_mma, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mb_expect_tx(&bar_ld, 16384 + 4 * 32768);
+    tma2d(Qs, &tQ, h * kDk, row0 + qt * kAttQ, &bar_ld);
+    tma2d(Ks, &tKV, d + h * kDk, row0, &bar_ld);
+    tma2d(Ks + 32768, &tKV, d + h * kDk, row0 + 256, &bar_ld);
+    tma2d(Vs, &tKV, 2 * d + h * kDk, row0, &bar_ld);
+    tma2d(Vs + 32768, &tKV, 2 * d + h * kDk, row0 + 256, &bar_ld);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     s32(&tbase)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (tid == 0) {
+    mb_wait(&bar_ld, 0);
+    tc_fence_after();
+    const uint64_t dq = umma_desc(Qs);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      const uint64_t dk = umma_desc(Ks + hh * 32768);
+#pragma unroll
+      for (int k = 0; k < kDk / 16; ++k)
+        umma(tmem + 256 * hh, dq + 2ull * k, dk + 2ull * k, kIdescS, k > 0);
+    }
+    umma_commit(&bar_mma);
+  }
+  __syncwarp();
+  mb_wait(&bar_mma, 0);
+  tc_fence_after();
+  const int r = warp * 32 + lane;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const float c2 = 1.4426950408889634f * rsqrtf((float)kDk);  // log2(e) / sqrt(dk)
+  float m = -INFINITY;
+#pragma unroll 1
+  for (int c0 = 0; c0 < kAtt2K; c0 += 32) {
+    if (c0 >= T) break;
+    uint32_t v[32];
+    tmem_ld32(trow + c0, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (c0 + j < T) m = fmaxf(m, __uint_as_float(v[j]));
+  }
+  float sum = 0.f;
+#pragma unroll 1
+  for (int hh = 0; hh < 2; ++hh) {
+    if (hh == 1) {  // P0 V0 has read the P buffer
+      __syncwarp();
+      mb_wait(&bar_mma, 1);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c1 = 0; c1 < 256; c1 += 32) {
+      const int c0 = hh * 256 + c1;
+      uint32_t v[32];
+      if (c0 < T) tmem_ld32(trow + c0, v);
+      float p[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float e = (c0 + j < T) ? exp2f((__uint_as_float(v[j]) - m) * c2) : 0.f;
+        sum += __bfloat162float(__float2bfloat16_rn(e));
+        p[j] = e;
+      }
+      unsigned char* blk = Ps + (c1 >> 6) * 16384;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 u;
+        __nv_bfloat162 h0 = __floats2bfloat162_rn(p[8 * c], p[8 * c + 1]);
+        __nv_bfloat162 h1 = __floats2bfloat162_rn(p[8 * c + 2], p[8 * c + 3]);
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(p[8 * c + 4], p[8 * c + 5]);
+        __nv_bfloat162 h3 = __floats2bfloat162_rn(p[8 * c + 6], p[8 * c + 7]);
+        u.x = *reinterpret_cast<uint32_t*>(&h0);
+        u.y = *reinterpret_cast<uint32_t*>(&h1);
+        u.z = *reinterpret_cast<uint32_t*>(&h2);
+        u.w = *reinterpret_cast<uint32_t*>(&h3);
+        *reinterpret_cast<uint4*>(blk + sw128(r, ((c1 & 63) >> 3) + c)) = u;
+      }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      const uint64_t dv = umma_desc(Vs + hh * 32768);
+#pragma unroll
+      for (int kk = 0; kk < 256 / 16; ++kk) {
+        const uint64_t dp = umma_desc(Ps + (kk >> 2) * 16384) + 2ull * (kk & 3);
+        umma(tmem, dp, dv + 128ull * kk /* 16 keys = 2048 B */, kIdescO, (hh > 0 || kk > 0));
+      }
+      umma_commit(&bar_mma);
+    }
+  }
+  __syncwarp();
+  mb_wait(&bar_mma, 0);  // third completion (S, P0 V0, P1 V1)
+  tc_fence_after();
+  const float inv = 1.f / sum;
+  const int q = qt * kAttQ + r;
+  uint32_t o[64];
+  {
+    uint32_t v[32];
+    tmem_ld32(trow, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[j] = v[j];
+    tmem_ld32(trow + 32, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) o[32 + j] = v[j];
+  }
+  if (q < T) {
+    uint4* dst = reinterpret_cast<uint4*>(out + ((size_t)row0 + q) * d + h * kDk);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      uint4 u;
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(o[8 * c]) * inv,
+                                                __uint_as_float(o[8 * c + 1]) * inv);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 2]) * inv,
+                                                __uint_as_float(o[8 * c + 3]) * inv);
+      __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 4]) * inv,
+                                                __uint_as_float(o[8 * c + 5]) * inv);
+      __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(o[8 * c + 6]) * inv,
+                                                __uint_as_float(o[8 * c + 7]) * inv);
+      u.x = *reinterpret_cast<uint32_t*>(&h0);
+      u.y = *reinterpret_cast<uint32_t*>(&h1);
+      u.z = *reinterpret_cast<uint32_t*>(&h2);
+      u.w = *reinterpret_cast<uint32_t*>(&h3);
+      dst[c] = u;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
 // in-place log_softmax over rows of width V; one CTA per row
 __global__ void __launch_bounds__(256) log_softmax_kernel(float* __restrict__ x, int V) {
   __shared__ float red[8];
@@ -657,6 +825,10 @@ struct EncoderImpl {
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, kAttSmem)) !=
         cudaSuccess)
       return e;
+    if ((e = cudaFuncSetAttribute(attention_tc512_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, kAtt2Smem)) !=
+        cudaSuccess)
+      return e;
     launches = 0;
     const size_t fb_elems = (size_t)S * T_in * s.idim;
     float* stage[2] = {nullptr, nullptr};
@@ -731,15 +903,19 @@ struct EncoderImpl {
         ln(y.ln1g, y.ln1b);
         if ((e = gemm(M, 3 * d, d, Y, y.wqkv, kPlain, y.bqkv, nullptr, QKV, 3 * d)) != cudaSuccess)
           return e;
-        if (T2 <= kAttK) {
+        if (T2 <= kAtt2K && std::getenv("BL_ENC_ATTN_CUDA") == nullptr) {
           CUtensorMap tQ, tKV;
           if (!make_tmap(&tQ, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, QKV, 3 * d, M, (size_t)6 * d,
                          kDk, kAttQ, CU_TENSOR_MAP_SWIZZLE_128B) ||
               !make_tmap(&tKV, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, QKV, 3 * d, M, (size_t)6 * d,
                          kDk, kAttK, CU_TENSOR_MAP_SWIZZLE_128B))
             return cudaErrorInvalidValue;
-          attention_tc_kernel<<<dim3(ns, s.heads, (T2 + kAttQ - 1) / kAttQ), 128, kAttSmem,
-                                st>>>(tQ, tKV, T2, d, AO);
+          if (T2 <= kAttK)
+            attention_tc_kernel<<<dim3(ns, s.heads, (T2 + kAttQ - 1) / kAttQ), 128, kAttSmem,
+                                  st>>>(tQ, tKV, T2, d, AO);
+          else
+            attention_tc512_kernel<<<dim3(ns, s.heads, (T2 + kAttQ - 1) / kAttQ), 128,
+                                     kAtt2Smem, st>>>(tQ, tKV, T2, d, AO);
         } else {
           attention_kernel<<<dim3(ns, s.heads), kAttnWarps * 32, attn_smem, st>>>(QKV, T2, d,
                                                                                  s.heads, AO);

@@ -123,8 +123,11 @@ def _run_encoder(spec, n, frames, seed):
 @pytest.mark.gpu
 @pytest.mark.parametrize("spec_name,n,frames", [("TINY", 3, 150), ("SMALL", 3, 1000),
                                                  ("LARGE", 1, 1000), ("TINY", 2, 1100),
-                                                 ("SMALL", 2, 2000)])
+                                                 ("SMALL", 2, 2000), ("TINY", 2, 1032),
+                                                 ("LARGE", 1, 2000)])
 def test_encoder_vs_torch(spec_name, n, frames):
+    """T2 <= 256: one-tile tcgen05 attention; 256 < T2 <= 512 (frames 1032 ->
+    257, 1100 -> 274, 2000 -> 499): the two-half tcgen05 attention."""
     from torch_encoder import encoder_forward
     spec = {"TINY": TINY, "SMALL": enc.SMALL, "LARGE": enc.LARGE}[spec_name]
     w, fb, grid, _ = _run_encoder(spec, n, frames, seed=11)
