@@ -9,9 +9,11 @@ import torch  # noqa: E402
 from paper_2101_05600_b200 import encoder as enc  # noqa: E402
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 28800
-for (N, K, mode, name) in [(768, 256, 0, "qkv"), (256, 256, 2, "wo+res"), (256, 256, 0, "q2"),
-                           (2048, 256, 1, "ff1+relu"), (256, 2048, 2, "ff2+res"),
-                           (500, 256, 0, "out")]:
+d = int(sys.argv[2]) if len(sys.argv) > 2 else 256  # 512: the Librispeech-size decoder
+V = 500 if d == 256 else 5000
+for (N, K, mode, name) in [(3 * d, d, 0, "qkv"), (d, d, 2, "wo+res"), (d, d, 0, "q2"),
+                           (2048, d, 1, "ff1+relu"), (d, 2048, 2, "ff2+res"),
+                           (V, d, 0, "out")]:
     A = torch.randn(M, K, device="cuda").bfloat16()
     B = torch.randn(N, K, device="cuda").bfloat16()
     bias = torch.randn(N, device="cuda")
@@ -31,4 +33,14 @@ for (N, K, mode, name) in [(768, 256, 0, "qkv"), (256, 256, 2, "wo+res"), (256, 
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 20
-    print(f"{name:9s} M={M} N={N} K={K}: {ms * 1e3:7.1f} us  {2 * M * N * K / ms / 1e9:7.1f} TFLOP/s")
+    # cuBLAS on the same shape (library reference point, bf16 out)
+    for _ in range(3):
+        torch.matmul(A, B.t())
+    e0.record()
+    for _ in range(20):
+        torch.matmul(A, B.t())
+    e1.record()
+    torch.cuda.synchronize()
+    cb = e0.elapsed_time(e1) / 20
+    print(f"{name:9s} M={M} N={N} K={K}: {ms * 1e3:7.1f} us  {2 * M * N * K / ms / 1e9:7.1f} TFLOP/s"
+          f"   (cuBLAS {cb * 1e3:7.1f} us)")
