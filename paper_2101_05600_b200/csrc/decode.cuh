@@ -42,13 +42,15 @@ struct HistRec {
 };
 
 // TMA streaming of the CTC window slab (large vocabularies): 512-column tiles
-// (two columns per thread) x kTmaRows-row chunks, kTmaStagesMax stages. The
-// tensor-core variant uses the same 16 KB stages as 16 swizzle blocks of
-// 8 rows x 32 columns, and a factor operand of 512 B per 8-row chunk.
-constexpr int kTmaBoxCols = 256;
+// (two columns per thread) x kTmaRows-row chunks, kTmaStagesMax stages; a
+// stage is 8 warp slices of kTmaRows x kTmaBoxCols (each warp streams its own
+// 64 columns). The tensor-core variant uses the same 16 KB stages as 16
+// swizzle blocks of 8 rows x 32 columns, and a factor operand of 512 B per
+// 8-row chunk.
+constexpr int kTmaBoxCols = 64;
 constexpr int kTmaRows = 8;
 constexpr int kTmaStagesMax = 10;
-constexpr int kTmaStageBytes = 2 * kTmaRows * kTmaBoxCols * 4;
+constexpr int kTmaStageBytes = 8 * kTmaRows * kTmaBoxCols * 4;
 
 struct KParams {
   CUtensorMap tmap;  // TMA map over all utterances' grid rows: 2D [sum T][V] (fp32),

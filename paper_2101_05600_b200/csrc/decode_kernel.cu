@@ -196,6 +196,15 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigne
       "r"(parity), "r"(1000000u)
       : "memory");
 }
+__device__ __forceinline__ void mbar_wait_sleep_s(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WS_%=;\n}" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 // bounded wait (tensor-core variant): a barrier that never completes reports
 // where and traps instead of hanging the device
 __device__ __noinline__ void mbar_wait_dbg(unsigned long long* bar, unsigned parity, int tag,
@@ -511,6 +520,13 @@ __device__ double psi_only(const KParams& P, const Shared<BMAX>& sh, int u,
     prof_t = _now;                                     \
   }
 
+#ifndef BL_PROF_WAIT
+#define PROF_SERIAL(t0) \
+  if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - (t0);
+#else
+#define PROF_SERIAL(t0)
+#endif
+
 }  // namespace
 
 // kMode 0: K1 slab by __ldg, every upper key in shared memory (keys mode);
@@ -529,6 +545,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
   __shared__ SpTables tb;
   __shared__ __align__(8) unsigned long long mbar[kTmaStagesMax];
   __shared__ int cons[kTmaStagesMax];  // warps done with each TMA stage (monotonic)
+  // slab streaming (kMode 2): one ring per warp, barrier (stage, warp) at st * kNWarp + warp
+  __shared__ __align__(8) unsigned long long mbarw[kMode == 2 ? kTmaStagesMax * kNWarp : 1];
   __shared__ __align__(8) unsigned long long mmad[kTmaStagesMax];  // tensor cores: stage's MMAs done
   __shared__ unsigned tmem_base;
 
@@ -576,6 +594,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       if (kTc) mbar_init(&mmad[k], 1);
       cons[k] = 0;
     }
+    if (kMode == 2)
+      for (int k = 0; k < P.tma_stages * kNWarp; ++k) mbar_init(&mbarw[k], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (kTc && warp == 0) {  // accumulators: 2 x (4 subtiles x 16 parents) fp32 columns
@@ -682,6 +702,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
     sh.b_row[0][0] = P.net_rows ? u * B : lookup_row(P, hist_c, 0, 0, 0, 0);
   }
   __syncthreads();
+#ifdef BL_PROF_WAIT
+  if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - prof_t;
+#endif
   if (ud.need_tail) {
     // F[k][c]: label c held from frame k to some k' then blank to T
     // (the eos tail of ctc_prefix.cpp:88-104 in closed form).
@@ -770,6 +793,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
     tma_jobs += J;
   }
   __syncthreads();
+#ifdef BL_PROF_WAIT
+  if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 15] += clock64() - prof_t;
+#endif
   }  // fresh start
   PROF_MARK(0);
 
@@ -947,19 +973,32 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       // (terms below 2^-126 of the column max flush to zero: at most
       // W * 2^-126 absolute, covered by the W * 1e-6 key half-width).
       constexpr int kP = BMAX / 2;
-      // lazy rescale: the shift m only moves when a value exceeds it by more
+      // The column shift is kept in log2 units (ms): each term is
+      // 2^(x * L2E - ms) with ONE rounding (FFMA) instead of (x - m) * L2E.
+      // The shift is the same for every term of an epoch, so ms itself
+      // carries no error; the extra error is the rounding of L2E (|x| * 1.3e-8
+      // per term, |x| <= |m| + 190 for every term above the flush) and the
+      // conversion ms * LN2 of the final shift: <= |m| * 8.6e-8 + 2.5e-6 nats,
+      // covered by the lam * (|m| * 1.5e-7 + 1e-5) term of the key half-width.
+      // The start shift gs = round-up(gf * L2E) makes a log-zero entry
+      // (x == gf) give 2^(<= 0), never an overflow.
+      constexpr float kL2E = 1.44269504088896341f, kLn2 = 0.693147180559945309f;
+      const float gs = __fmul_ru(gf, kL2E);
+      auto mnat = [&](float ms) { return ms == gs ? gf : ms * kLn2; };
+      // lazy rescale: the shift only moves when a value exceeds it by more
       // than 8 nats, so every accumulated term is <= e^8
-      auto rescale = [&](float2(&Sx)[kP], float& m, float x) {
-        if (x > m + 8.f) {
-          const float r = __expf(m - x);
+      auto rescale = [&](float2(&Sx)[kP], float& ms, float x) {
+        if (fmaf(x, kL2E, -ms) > 8.f * kL2E) {
+          const float xs = x * kL2E;
+          const float r = ex2_ftz(ms - xs);
           const float2 r2 = make_float2(r, r);
 #pragma unroll
           for (int q = 0; q < kP; ++q) Sx[q] = __fmul2_rn(Sx[q], r2);
-          m = x;
+          ms = xs;
         }
       };
-      auto acc_term = [&](float2(&Sx)[kP], float m, float x, const float* ph) {
-        const float pe = ex2_ftz((x - m) * 1.44269504088896341f);
+      auto acc_term = [&](float2(&Sx)[kP], float ms, float x, const float* ph) {
+        const float pe = ex2_ftz(fmaf(x, kL2E, -ms));
         const float2 p2 = make_float2(pe, pe);
         if constexpr (BMAX % 4 == 0) {  // 16-byte factor rows
 #pragma unroll
@@ -1029,7 +1068,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
                 under = lam_pos && !(Sq >= 7.888609052210118e-31f);  // 2^-100
                 const float lg = under ? -68.62157f : lg2_ftz(Sq) * 0.693147180559945309f;
                 const float key = lam_pos ? kbq + klamf * (m + lg) + r : kbq + r;
-                const float h = hw + fabsf(key) * 2.4e-7f;
+                const float h = hw + fabsf(key) * 2.4e-7f + klamf * fmaf(fabsf(m), 1.5e-7f, 1e-5f);
                 klo = under ? -INFINITY : key - h;
                 kub_v = key + h;
                 // joint exactly kLogZero: att log-zero, or psi log-zero
@@ -1409,51 +1448,76 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         tma_jobs += J;
       } else if constexpr (kTma) {
         // K1 slab streamed by TMA: job j = (512-column tile, kTmaRows-row
-        // chunk); thread 0 keeps tma_stages jobs in flight on mbarriers, all
-        // threads consume each chunk from shared memory.
+        // chunk). Each warp streams its own 64 columns of the tile through its
+        // own ring of tma_stages 2 KB slices (lane 0 issues, one mbarrier per
+        // slice): a warp refills a slice as soon as it has consumed it, so no
+        // warp waits for a slower one (a shared ring is refilled only when
+        // its slowest consumer is done: ~14% of the bulk's time went to
+        // waiting for data that was requested too late).
         const int nch = (W + kTmaRows - 1) / kTmaRows;
         const int ntile = (C + 2 * kNT - 1) / (2 * kNT);
         const int J = ntile * nch;
         const int NST = P.tma_stages;
-        float* stages = reinterpret_cast<float*>(region + pl.stages);
+        constexpr int kSlice = kTmaRows * kTmaBoxCols;  // floats per warp slice
+        static_assert(kTmaBoxCols == 64 && kTmaStageBytes == kNWarp * kSlice * 4,
+                      "one 64-column slice per warp and stage");
+        float* wst = reinterpret_cast<float*>(region + pl.stages) + warp * kSlice;
+        const unsigned wbar = smem_u32(&mbarw[warp]);  // + 8 * kNWarp per stage
         const int urow = ud.row0 + s - 1;
-        auto issue = [&](int j, unsigned g) {
-          const int st = (int)(g % (unsigned)NST);
-          const int tile = j / nch, k = j - tile * nch;
-          float* dst = stages + (size_t)st * (kTmaStageBytes / 4);
-          mbar_expect_tx(&mbar[st], kTmaStageBytes);
-          tma_load_2d(dst, &P.tmap, tile * 2 * kNT, urow + k * kTmaRows, &mbar[st]);
-          tma_load_2d(dst + kTmaRows * kTmaBoxCols, &P.tmap, tile * 2 * kNT + kTmaBoxCols,
-                      urow + k * kTmaRows, &mbar[st]);
+        auto issue_at = [&](int st, int tile, int k) {  // lane 0
+          const unsigned bar = wbar + 8u * kNWarp * st;
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                       "r"(kSlice * 4)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(wst + st * kNWarp * kSlice)),
+              "l"(reinterpret_cast<unsigned long long>(&P.tmap)),
+              "r"(tile * 2 * kNT + warp * kTmaBoxCols), "r"(urow + k * kTmaRows), "r"(bar)
+              : "memory");
         };
-        if (tid == 0) {
+        if (lane == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          for (int j = 0; j < NST && j < J; ++j) issue(j, tma_jobs + j);
+          for (int j = 0; j < NST && j < J; ++j)
+            issue_at((int)((tma_jobs + j) % (unsigned)NST), j / nch, j % nch);
         }
         float2 S0[kP], S1[kP];
-        float m0 = gf, m1 = gf, r0s = 0.f, r1s = 0.f;
-        const int colb = ((2 * tid) >= kTmaBoxCols ? kTmaRows * kTmaBoxCols : 0) +
-                         ((2 * tid) & (kTmaBoxCols - 1));
+        float m0 = gs, m1 = gs, r0s = 0.f, r1s = 0.f;
+        const int colb = 2 * lane;
         // job counters kept incrementally (a runtime division per job and
         // thread was ~10% of this loop's instructions): stage, its use round
-        // (mbarrier parity, release count), tile and chunk
+        // (mbarrier parity), tile and chunk
         int st = (int)(tma_jobs % (unsigned)NST);
         unsigned rnd = tma_jobs / (unsigned)NST;
         int tile = 0, k = 0;
         for (int j = 0; j < J; ++j) {
-          const unsigned g = tma_jobs + j;
           const int c0 = tile * 2 * kNT + 2 * tid;
           const bool active = c0 < C, two = c0 + 1 < C;
           if (k == 0) {
 #pragma unroll
             for (int q = 0; q < kP; ++q) S0[q] = S1[q] = make_float2(0.f, 0.f);
-            m0 = m1 = gf;
+            m0 = m1 = gs;
             r0s = (row_same >= 0 && active) ? attf_at(P, row_same, c0) : 0.f;
             r1s = (row_same >= 0 && two) ? attf_at(P, row_same, c0 + 1) : 0.f;
           }
-          mbar_wait_sleep(&mbar[st], rnd & 1u);
+#ifdef BL_PROF_WAIT  // diagnostic build: warp 0's stage-wait cycles and stalls
+          if (warp == 0) {
+            const long long tw0 = clock64();
+            unsigned ok;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                "selp.u32 %0, 1, 0, p;\n}"
+                : "=r"(ok)
+                : "r"(wbar + 8u * kNWarp * st), "r"(rnd & 1u)
+                : "memory");
+            mbar_wait_sleep_s(wbar + 8u * kNWarp * st, rnd & 1u);
+            tq_frames += clock64() - tw0;
+            tq_keys += ok ? 0 : 1;
+          } else
+#endif
+          mbar_wait_sleep_s(wbar + 8u * kNWarp * st, rnd & 1u);
           if (active) {
-            const float* sb = stages + (size_t)st * (kTmaStageBytes / 4) + colb;
+            const float* sb = wst + st * kNWarp * kSlice + colb;
             const int nrow = min(kTmaRows, W - k * kTmaRows);
             const int f0 = k * kTmaRows;
             constexpr int kRu = 8;  // rows per unrolled group
@@ -1486,27 +1550,29 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
               }
             }
           }
-          // stage release per warp: the warp that finishes it last refills
-          // it (no block barrier; the other warps stream on). Every lane's
-          // reads of the stage were consumed by its FMAs above, and a warp's
-          // shared-memory accesses (these reads, then lane 0's atomic) are
-          // performed in order, so the refill (issued after the last count)
-          // cannot overtake a read.
+          // the warp's slice is consumed (every lane's reads fed its FMAs
+          // above): lane 0 refills it with job j + NST
           __syncwarp();
           if (lane == 0) {
-            const int done = atomicAdd(&cons[st], 1);
-            if (done == (int)rnd * kNWarp + kNWarp - 1 && j + NST < J) {
+            if (j + NST < J) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              issue(j + NST, g + NST);
+              // job j + NST reuses this stage: its (tile, chunk) from this
+              // job's without a division
+              int kk = k + NST, tt = tile;
+              while (kk >= nch) {
+                kk -= nch;
+                ++tt;
+              }
+              issue_at(st, tt, kk);
             }
           }
           if (k == nch - 1) {  // the tile's keys (whole warp: warp_bound)
             float kmax = -INFINITY;
-            if (active)
-              emit_keys(c0, c0 + 1, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, false, 0.f, kmax);
+            const float n0 = mnat(m0), n1 = two ? mnat(m1) : gf;
+            if (active) emit_keys(c0, c0 + 1, two, S0, S1, n0, n1, r0s, r1s, false, 0.f, kmax);
             const float th = warp_bound(tile < 3 || (tile & 3) == 0);
             if (active && kmax >= th)
-              emit_keys(c0, c0 + 1, two, S0, S1, m0, two ? m1 : gf, r0s, r1s, true, th, kmax);
+              emit_keys(c0, c0 + 1, two, S0, S1, n0, n1, r0s, r1s, true, th, kmax);
           }
           if (++st == NST) {
             st = 0;
@@ -1526,7 +1592,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         const bool act = c0 < C;
         float kmax = -INFINITY;
         float2 S0[kP], S1[kP];
-        float m0 = gf, m1 = gf, r0s = 0.f, r1s = 0.f;
+        float m0 = gs, m1 = gs, n0 = gf, n1 = gf, r0s = 0.f, r1s = 0.f;
         const bool two = c0 + 1 < C;
 #pragma unroll
         for (int q = 0; q < kP; ++q) S0[q] = S1[q] = make_float2(0.f, 0.f);
@@ -1588,17 +1654,18 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           acc(S0, m0, a, phr + i * phs);
           acc(S1, m1, b, phr + i * phs);
         }
-        if (!two) m1 = gf;
+        n0 = mnat(m0);
+        n1 = two ? mnat(m1) : gf;
         const long long tq2 = clock64();
         tq_frames += tq2 - tq1;
-        emit_keys(c0, c0 + 1, two, S0, S1, m0, m1, r0s, r1s, false, 0.f, kmax);
+        emit_keys(c0, c0 + 1, two, S0, S1, n0, n1, r0s, r1s, false, 0.f, kmax);
         tq_keys += clock64() - tq2;
         }
         if (!keys_mode) {
           const int it = cb / (2 * kNT);
           const float th = warp_bound(it < 3 || (it & 3) == 0);
           if (act && kmax >= th)
-            emit_keys(c0, c0 + 1, two, S0, S1, m0, m1, r0s, r1s, true, th, kmax);
+            emit_keys(c0, c0 + 1, two, S0, S1, n0, n1, r0s, r1s, true, th, kmax);
         }
       }
       }
@@ -1830,7 +1897,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         }
       }
       __syncthreads();
+#ifndef BL_PROF_WAIT
       if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 15] += clock64() - ts0;
+#endif
       // ---- P6: contenders re-scored exactly. Warps [0, nser): the serial
       // gamma_n'/gamma_b' chains (one thread per contender, reference op
       // order); the other warps: psi by a parallel fp64 log-sum-exp. ----
@@ -1852,7 +1921,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           if (role == 0) items[q].tau = best;
           else items[q].taut = best;
         }
-        if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - tr0;
+        PROF_SERIAL(tr0);
       } else if (warp < nser) {
         // inputs not staged (window too wide for the region): one lane per
         // contender runs the chains and psi from global memory
@@ -1871,7 +1940,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           items[q].score = mix_joint(lam, psi, att);
           items[q].tau = tau;
           items[q].taut = taut;
-          if (P.prof && tid == 0) P.prof[(size_t)u * 16 + 14] += clock64() - tr0;
+          PROF_SERIAL(tr0);
         }
       } else {
         if (warp == kNWarp - 1) eos_items();
