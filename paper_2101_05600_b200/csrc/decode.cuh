@@ -50,6 +50,7 @@ struct HistRec {
 constexpr int kTmaBoxCols = 64;
 constexpr int kTmaRows = 8;
 constexpr int kTmaStagesMax = 10;
+constexpr int kSlabRows = 16;  // rows per slab job of the TMA filter mode (kMode 2)
 constexpr int kTmaStageBytes = 8 * kTmaRows * kTmaBoxCols * 4;
 
 struct KParams {

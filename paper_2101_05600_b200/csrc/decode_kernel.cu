@@ -1447,34 +1447,46 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         }
         tma_jobs += J;
       } else if constexpr (kTma) {
-        // K1 slab streamed by TMA: job j = (512-column tile, kTmaRows-row
+        // K1 slab streamed by TMA: job j = (512-column tile, kSlabRows-row
         // chunk). Each warp streams its own 64 columns of the tile through its
-        // own ring of tma_stages 2 KB slices (lane 0 issues, one mbarrier per
-        // slice): a warp refills a slice as soon as it has consumed it, so no
-        // warp waits for a slower one (a shared ring is refilled only when
-        // its slowest consumer is done: ~14% of the bulk's time went to
-        // waiting for data that was requested too late).
-        const int nch = (W + kTmaRows - 1) / kTmaRows;
+        // own ring of slots (lane 0 issues one or two 8-row boxes per job,
+        // one mbarrier per slot): a warp refills a slot as soon as it has
+        // consumed it, so no warp waits for a slower one (a shared ring is
+        // refilled only when its slowest consumer is done: ~14% of the bulk's
+        // time went to waiting for data requested too late). 16-row jobs
+        // halve the per-job overhead (wait, refill, counters) per row.
+        const int nch = (W + kSlabRows - 1) / kSlabRows;
         const int ntile = (C + 2 * kNT - 1) / (2 * kNT);
         const int J = ntile * nch;
-        const int NST = P.tma_stages;
-        constexpr int kSlice = kTmaRows * kTmaBoxCols;  // floats per warp slice
-        static_assert(kTmaBoxCols == 64 && kTmaStageBytes == kNWarp * kSlice * 4,
-                      "one 64-column slice per warp and stage");
+        constexpr int kBox = kTmaRows * kTmaBoxCols;    // floats per 8-row box
+        constexpr int kSlice = kSlabRows * kTmaBoxCols;  // floats per warp slot
+        static_assert(kTmaBoxCols == 64 && kSlabRows == 2 * kTmaRows,
+                      "a warp slot is two 8-row boxes of 64 columns");
+        // slots per warp: the stage area (tma_stages x 16 KB) split over the warps
+        const int NST = max(1, P.tma_stages * kTmaStageBytes / (kNWarp * kSlice * 4));
         float* wst = reinterpret_cast<float*>(region + pl.stages) + warp * kSlice;
-        const unsigned wbar = smem_u32(&mbarw[warp]);  // + 8 * kNWarp per stage
+        const unsigned wbar = smem_u32(&mbarw[warp]);  // + 8 * kNWarp per slot
         const int urow = ud.row0 + s - 1;
         auto issue_at = [&](int st, int tile, int k) {  // lane 0
           const unsigned bar = wbar + 8u * kNWarp * st;
+          const unsigned dst = smem_u32(wst + st * kNWarp * kSlice);
+          const int two_box = W - k * kSlabRows > kTmaRows;  // the window's rows only
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                       "r"(kSlice * 4)
+                       "r"((two_box ? 2 : 1) * kBox * 4)
                        : "memory");
+          const int x = tile * 2 * kNT + warp * kTmaBoxCols, y = urow + k * kSlabRows;
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-              " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(wst + st * kNWarp * kSlice)),
-              "l"(reinterpret_cast<unsigned long long>(&P.tmap)),
-              "r"(tile * 2 * kNT + warp * kTmaBoxCols), "r"(urow + k * kTmaRows), "r"(bar)
+              " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+              "l"(reinterpret_cast<unsigned long long>(&P.tmap)), "r"(x), "r"(y), "r"(bar)
               : "memory");
+          if (two_box)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst + kBox * 4),
+                "l"(reinterpret_cast<unsigned long long>(&P.tmap)), "r"(x), "r"(y + kTmaRows),
+                "r"(bar)
+                : "memory");
         };
         if (lane == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1485,7 +1497,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         float m0 = gs, m1 = gs, r0s = 0.f, r1s = 0.f;
         const int colb = 2 * lane;
         // job counters kept incrementally (a runtime division per job and
-        // thread was ~10% of this loop's instructions): stage, its use round
+        // thread was ~10% of this loop's instructions): slot, its use round
         // (mbarrier parity), tile and chunk
         int st = (int)(tma_jobs % (unsigned)NST);
         unsigned rnd = tma_jobs / (unsigned)NST;
@@ -1500,7 +1512,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             r0s = (row_same >= 0 && active) ? attf_at(P, row_same, c0) : 0.f;
             r1s = (row_same >= 0 && two) ? attf_at(P, row_same, c0 + 1) : 0.f;
           }
-#ifdef BL_PROF_WAIT  // diagnostic build: warp 0's stage-wait cycles and stalls
+#ifdef BL_PROF_WAIT  // diagnostic build: warp 0's slot-wait cycles and stalls
           if (warp == 0) {
             const long long tw0 = clock64();
             unsigned ok;
@@ -1518,45 +1530,43 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           mbar_wait_sleep_s(wbar + 8u * kNWarp * st, rnd & 1u);
           if (active) {
             const float* sb = wst + st * kNWarp * kSlice + colb;
-            const int nrow = min(kTmaRows, W - k * kTmaRows);
-            const int f0 = k * kTmaRows;
+            const int nrow = min(kSlabRows, W - k * kSlabRows);
+            const float* ph0 = phr + k * kSlabRows * phs;
             constexpr int kRu = 8;  // rows per unrolled group
-            if (nrow == kTmaRows) {  // full chunk: rows unrolled so their loads and exps overlap
+            int i0 = 0;
+            // full 8-row groups: rows unrolled so their loads and exps overlap
+            for (; i0 + kRu <= nrow; i0 += kRu) {
+              float2 v[kRu];
 #pragma unroll
-              for (int i0 = 0; i0 < kTmaRows; i0 += kRu) {
-                float2 v[kRu];
+              for (int k2 = 0; k2 < kRu; ++k2)
+                v[k2] = *reinterpret_cast<const float2*>(sb + (i0 + k2) * kTmaBoxCols);
+              float xma = v[0].x, xmb = v[0].y;
 #pragma unroll
-                for (int k2 = 0; k2 < kRu; ++k2)
-                  v[k2] = *reinterpret_cast<const float2*>(sb + (i0 + k2) * kTmaBoxCols);
-                float xma = v[0].x, xmb = v[0].y;
-#pragma unroll
-                for (int k2 = 1; k2 < kRu; ++k2) {
-                  xma = fmaxf(xma, v[k2].x);
-                  xmb = fmaxf(xmb, v[k2].y);
-                }
-                rescale(S0, m0, xma);  // one test per column per group
-                rescale(S1, m1, xmb);
-#pragma unroll
-                for (int k2 = 0; k2 < kRu; ++k2) {
-                  acc_term(S0, m0, v[k2].x, phr + (f0 + i0 + k2) * phs);
-                  acc_term(S1, m1, v[k2].y, phr + (f0 + i0 + k2) * phs);
-                }
+              for (int k2 = 1; k2 < kRu; ++k2) {
+                xma = fmaxf(xma, v[k2].x);
+                xmb = fmaxf(xmb, v[k2].y);
               }
-            } else {
-              for (int i = 0; i < nrow; ++i) {
-                const float2 v = *reinterpret_cast<const float2*>(sb + i * kTmaBoxCols);
-                acc(S0, m0, v.x, phr + (f0 + i) * phs);
-                acc(S1, m1, v.y, phr + (f0 + i) * phs);
+              rescale(S0, m0, xma);  // one test per column per group
+              rescale(S1, m1, xmb);
+#pragma unroll
+              for (int k2 = 0; k2 < kRu; ++k2) {
+                acc_term(S0, m0, v[k2].x, ph0 + (i0 + k2) * phs);
+                acc_term(S1, m1, v[k2].y, ph0 + (i0 + k2) * phs);
               }
             }
+            for (; i0 < nrow; ++i0) {  // the window's last rows
+              const float2 v = *reinterpret_cast<const float2*>(sb + i0 * kTmaBoxCols);
+              acc(S0, m0, v.x, ph0 + i0 * phs);
+              acc(S1, m1, v.y, ph0 + i0 * phs);
+            }
           }
-          // the warp's slice is consumed (every lane's reads fed its FMAs
+          // the warp's slot is consumed (every lane's reads fed its FMAs
           // above): lane 0 refills it with job j + NST
           __syncwarp();
           if (lane == 0) {
             if (j + NST < J) {
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              // job j + NST reuses this stage: its (tile, chunk) from this
+              // job j + NST reuses this slot: its (tile, chunk) from this
               // job's without a division
               int kk = k + NST, tt = tile;
               while (kk >= nch) {
