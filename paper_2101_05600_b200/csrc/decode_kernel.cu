@@ -987,14 +987,27 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       auto mnat = [&](float ms) { return ms == gs ? gf : ms * kLn2; };
       // lazy rescale: the shift only moves when a value exceeds it by more
       // than 8 nats, so every accumulated term is <= e^8
-      auto rescale = [&](float2(&Sx)[kP], float& ms, float x) {
-        if (fmaf(x, kL2E, -ms) > 8.f * kL2E) {
-          const float xs = x * kL2E;
-          const float r = ex2_ftz(ms - xs);
-          const float2 r2 = make_float2(r, r);
+      auto rescale_do = [&](float2(&Sx)[kP], float& ms, float x) {
+        const float xs = x * kL2E;
+        const float r = ex2_ftz(ms - xs);
+        const float2 r2 = make_float2(r, r);
 #pragma unroll
-          for (int q = 0; q < kP; ++q) Sx[q] = __fmul2_rn(Sx[q], r2);
-          ms = xs;
+        for (int q = 0; q < kP; ++q) Sx[q] = __fmul2_rn(Sx[q], r2);
+        ms = xs;
+      };
+      auto needs_rescale = [&](float ms, float x) { return fmaf(x, kL2E, -ms) > 8.f * kL2E; };
+      auto rescale = [&](float2(&Sx)[kP], float& ms, float x) {
+        if (needs_rescale(ms, x)) rescale_do(Sx, ms, x);
+      };
+      // both columns of a group, behind one warp-uniform branch: rescales
+      // are rare after a tile's first group, and the predicated form issues
+      // its ~16 instructions on every group
+      auto rescale2 = [&](float2(&Sa)[kP], float& ma, float xa, float2(&Sb)[kP], float& mb,
+                          float xb) {
+        const bool na = needs_rescale(ma, xa), nb2 = needs_rescale(mb, xb);
+        if (__any_sync(__activemask(), na || nb2)) {
+          if (na) rescale_do(Sa, ma, xa);
+          if (nb2) rescale_do(Sb, mb, xb);
         }
       };
       auto acc_term = [&](float2(&Sx)[kP], float ms, float x, const float* ph) {
@@ -1546,8 +1559,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
                 xma = fmaxf(xma, v[k2].x);
                 xmb = fmaxf(xmb, v[k2].y);
               }
-              rescale(S0, m0, xma);  // one test per column per group
-              rescale(S1, m1, xmb);
+              rescale2(S0, m0, xma, S1, m1, xmb);  // one test per column per group
 #pragma unroll
               for (int k2 = 0; k2 < kRu; ++k2) {
                 acc_term(S0, m0, v[k2].x, ph0 + (i0 + k2) * phs);
@@ -1556,8 +1568,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
             }
             for (; i0 < nrow; ++i0) {  // the window's last rows
               const float2 v = *reinterpret_cast<const float2*>(sb + i0 * kTmaBoxCols);
-              acc(S0, m0, v.x, ph0 + i0 * phs);
-              acc(S1, m1, v.y, ph0 + i0 * phs);
+              rescale2(S0, m0, v.x, S1, m1, v.y);
+              acc_term(S0, m0, v.x, ph0 + i0 * phs);
+              acc_term(S1, m1, v.y, ph0 + i0 * phs);
             }
           }
           // the warp's slot is consumed (every lane's reads fed its FMAs
