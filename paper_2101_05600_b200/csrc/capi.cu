@@ -620,6 +620,8 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     while (use_tma && use_tc != 1 && U > 148 && tma_stages > 3 &&
            need(tma_stages) + 6 * 1024 > 113 * 1024)
       --tma_stages;
+    if (const char* e = std::getenv("BL_TMA_STAGES"))  // sweep override (16 KB units)
+      if (use_tma && use_tc != 1) tma_stages = std::max(2, std::min(bl::kTmaStagesMax, atoi(e)));
   }
   // shared-memory plan: the aliased region (P3-P5 keys, P6 staging) is sized
   // so the whole plan fits 3 CTAs/SM (~71 KB) when the fixed parts allow it;
