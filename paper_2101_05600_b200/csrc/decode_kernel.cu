@@ -1509,6 +1509,24 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         float2 S0[kP], S1[kP];
         float m0 = gs, m1 = gs, r0s = 0.f, r1s = 0.f;
         const int colb = 2 * lane;
+        // Column early-out (one row per step: row_same >= 0): every key of
+        // column c is kb_q + lam * (m + lg S_q) + r with the same m and r, so
+        // kbmax + lam * (m + lg max_q S_q) + r bounds them all (+ the largest
+        // half-width, + 1e-3 for rounding); a column whose bound is below the
+        // block's running bound cannot reach theta0 (nor raise a bound) and
+        // skips both key passes. P4 takes theta0 >= the running bound, so
+        // theta0, the list and the contenders are those of the full scan.
+        float kbmax = -INFINITY;
+        for (int q = 0; q < nb; ++q) kbmax = fmaxf(kbmax, sh.kb[q]);
+        auto col_bound = [&](const float2(&Sx)[kP], float mn) {
+          float smax = 0.f;
+#pragma unroll
+          for (int q = 0; q < kP; ++q)
+            if (2 * q < nb) smax = fmaxf(smax, 2 * q + 1 < nb ? fmaxf(Sx[q].x, Sx[q].y) : Sx[q].x);
+          const float lg = smax >= 7.888609052210118e-31f ? lg2_ftz(smax) * kLn2 : -68.62157f;
+          const float un = lam_pos ? kbmax + klamf * (mn + lg) : kbmax;
+          return un + fabsf(un) * 2.4e-7f + hw + klamf * fmaf(fabsf(mn), 1.5e-7f, 1e-5f) + 1e-3f;
+        };
         // job counters kept incrementally (a runtime division per job and
         // thread was ~10% of this loop's instructions): slot, its use round
         // (mbarrier parity), tile and chunk
@@ -1592,9 +1610,15 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           if (k == nch - 1) {  // the tile's keys (whole warp: warp_bound)
             float kmax = -INFINITY;
             const float n0 = mnat(m0), n1 = two ? mnat(m1) : gf;
-            if (active) emit_keys(c0, c0 + 1, two, S0, S1, n0, n1, r0s, r1s, false, 0.f, kmax);
+            bool keys = active;
+            if (keys && row_same >= 0) {
+              const float thr = ord2f(*reinterpret_cast<volatile int*>(&sh.th_run));
+              keys = !(col_bound(S0, n0) + r0s < thr &&
+                       (!two || col_bound(S1, n1) + r1s < thr));
+            }
+            if (keys) emit_keys(c0, c0 + 1, two, S0, S1, n0, n1, r0s, r1s, false, 0.f, kmax);
             const float th = warp_bound(tile < 3 || (tile & 3) == 0);
-            if (active && kmax >= th)
+            if (keys && kmax >= th)
               emit_keys(c0, c0 + 1, two, S0, S1, n0, n1, r0s, r1s, true, th, kmax);
           }
           if (++st == NST) {
@@ -1728,7 +1752,10 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           th = mx;
         }
         if (lane == 0) {
-          sh.theta = th;
+          // the running bound of the filter mode is a valid theta0 too (B
+          // candidates reach it); the larger one lists fewer keys, with the
+          // same theta and contenders
+          sh.theta = keys_mode ? th : fmaxf(th, ord2f(sh.th_run));
           sh.theta2 = -INFINITY;  // stays when fewer than B keys are listed
           sh.n_list = 0;
         }
