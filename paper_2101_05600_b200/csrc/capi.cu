@@ -601,25 +601,27 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   }
   // tcgen05 kernels run one CTA per SM (the runtime's occupancy for any
   // kernel using tcgen05.alloc): the tensor-core variant takes the deepest ring
-  int tma_stages = use_tma ? (use_tc == 1 ? bl::kTmaStagesMax : U <= 148 ? 6 : 4) : 0;
+  int tma_stages = use_tma ? (use_tc == 1 ? bl::kTmaStagesMax : 6) : 0;
   {
-    // long utterances: fewer TMA stages (down to 2), then the non-TMA path,
-    // before the plan is rejected (12 KB left for static shared memory);
-    // large calls (two CTAs per SM wanted): fewer stages until two fit
+    // Slab mode: 16 KB stages split into per-warp slots of 16 rows (two per
+    // warp from 4 stages up; fewer stages give 8-row slots, which carry 3/4 or
+    // less of the bytes in flight and run up to 1.4x slower,
+    // scripts/c3_leg.py N 499). Large calls take 4 stages when two CTAs per
+    // SM then fit (their serial phases overlap), else 6 at one CTA per SM.
+    // Long utterances: fewer stages (down to 2), then the non-TMA path,
+    // before the plan is rejected (12 KB left for static shared memory).
     const size_t lim = (227 - 12) * 1024;
     const size_t fixed0 = bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0).total;
     auto need = [&](int st) {
       return fixed0 + bl::smem_plan(Tmax, B, bmax, C, caps, S, 0, 0, st, use_tc).region_need;
     };
+    if (use_tma && use_tc != 1 && U > 148 && need(4) + 6 * 1024 <= 113 * 1024) tma_stages = 4;
     while (use_tma && tma_stages > 2 && need(tma_stages) > lim) --tma_stages;
     if (use_tma && need(tma_stages) > lim) {
       use_tma = false;
       use_tc = 0;
       tma_stages = 0;
     }
-    while (use_tma && use_tc != 1 && U > 148 && tma_stages > 3 &&
-           need(tma_stages) + 6 * 1024 > 113 * 1024)
-      --tma_stages;
     if (const char* e = std::getenv("BL_TMA_STAGES"))  // sweep override (16 KB units)
       if (use_tma && use_tc != 1) tma_stages = std::max(2, std::min(bl::kTmaStagesMax, atoi(e)));
   }

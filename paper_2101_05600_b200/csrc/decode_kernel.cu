@@ -197,6 +197,16 @@ __device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigne
       : "memory");
 }
 __device__ __forceinline__ void mbar_wait_sleep_s(unsigned bar, unsigned parity) {
+#ifdef BL_WAIT_SPIN
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WS_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WS_%=:\n\t"
@@ -1468,26 +1478,29 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         // refilled only when its slowest consumer is done: ~14% of the bulk's
         // time went to waiting for data requested too late). 16-row jobs
         // halve the per-job overhead (wait, refill, counters) per row.
-        const int nch = (W + kSlabRows - 1) / kSlabRows;
+        constexpr int kBox = kTmaRows * kTmaBoxCols;  // floats per 8-row box
+        static_assert(kTmaBoxCols == 64 && kSlabRows == 2 * kTmaRows,
+                      "a warp slot is one or two 8-row boxes of 64 columns");
+        // slots per warp: the stage area (tma_stages x 16 KB) split over the
+        // warps, 16-row slots when that leaves two per warp, else 8-row ones
+        const int wfl = P.tma_stages * kTmaStageBytes / (kNWarp * 4);  // floats per warp
+        const int srows = wfl >= 2 * kSlabRows * kTmaBoxCols ? kSlabRows : kTmaRows;
+        const int kSlice = srows * kTmaBoxCols;  // floats per warp slot
+        const int NST = max(1, wfl / kSlice);
+        const int nch = (W + srows - 1) / srows;
         const int ntile = (C + 2 * kNT - 1) / (2 * kNT);
         const int J = ntile * nch;
-        constexpr int kBox = kTmaRows * kTmaBoxCols;    // floats per 8-row box
-        constexpr int kSlice = kSlabRows * kTmaBoxCols;  // floats per warp slot
-        static_assert(kTmaBoxCols == 64 && kSlabRows == 2 * kTmaRows,
-                      "a warp slot is two 8-row boxes of 64 columns");
-        // slots per warp: the stage area (tma_stages x 16 KB) split over the warps
-        const int NST = max(1, P.tma_stages * kTmaStageBytes / (kNWarp * kSlice * 4));
         float* wst = reinterpret_cast<float*>(region + pl.stages) + warp * kSlice;
         const unsigned wbar = smem_u32(&mbarw[warp]);  // + 8 * kNWarp per slot
         const int urow = ud.row0 + s - 1;
         auto issue_at = [&](int st, int tile, int k) {  // lane 0
           const unsigned bar = wbar + 8u * kNWarp * st;
           const unsigned dst = smem_u32(wst + st * kNWarp * kSlice);
-          const int two_box = W - k * kSlabRows > kTmaRows;  // the window's rows only
+          const int two_box = srows > kTmaRows && W - k * srows > kTmaRows;  // window rows only
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
                        "r"((two_box ? 2 : 1) * kBox * 4)
                        : "memory");
-          const int x = tile * 2 * kNT + warp * kTmaBoxCols, y = urow + k * kSlabRows;
+          const int x = tile * 2 * kNT + warp * kTmaBoxCols, y = urow + k * srows;
           asm volatile(
               "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
               " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
@@ -1561,8 +1574,8 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           mbar_wait_sleep_s(wbar + 8u * kNWarp * st, rnd & 1u);
           if (active) {
             const float* sb = wst + st * kNWarp * kSlice + colb;
-            const int nrow = min(kSlabRows, W - k * kSlabRows);
-            const float* ph0 = phr + k * kSlabRows * phs;
+            const int nrow = min(srows, W - k * srows);
+            const float* ph0 = phr + k * srows * phs;
             constexpr int kRu = 8;  // rows per unrolled group
             int i0 = 0;
             // full 8-row groups: rows unrolled so their loads and exps overlap
@@ -1596,7 +1609,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           __syncwarp();
           if (lane == 0) {
             if (j + NST < J) {
+#ifndef BL_NO_REFILL_FENCE
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
               // job j + NST reuses this slot: its (tile, chunk) from this
               // job's without a division
               int kk = k + NST, tt = tile;

@@ -6,13 +6,16 @@ import paper_2101_05600_b200 as bl
 names = ["init+Ftab", "P1 window/eos", "P2 phi/PhiF", "P3 bulk(+P4a)", "P4 theta", "P5 collect", "P6 contenders", "P7 rank (fb)", "fallback", "P8 walk (fb)", "P6-P9 overlap", "finalize", "t0:P3 frames", "t0:P3 keys", "t0:P6 serial", "t0:P6 staging"]
 rng = np.random.default_rng(1)
 CFGS = [(500, 10, 20, 64)]
-if len(sys.argv) > 1:  # V B M2 U  (M2 < 0: no margin)
+TENC = 249
+if len(sys.argv) > 1:  # V B M2 U [T_enc]  (M2 < 0: no margin)
     CFGS = [tuple(int(x) for x in sys.argv[1:5])]
+    if len(sys.argv) > 5:
+        TENC = int(sys.argv[5])
 for (V, B, M2, U) in CFGS:
     M2 = bl.NO_MARGIN if M2 < 0 else M2
     G = []
     for i in range(U):
-        p = rng.exponential(size=(249, V)); G.append(np.log(p / p.sum(1, keepdims=True)).astype(np.float32))
+        p = rng.exponential(size=(TENC, V)); G.append(np.log(p / p.sum(1, keepdims=True)).astype(np.float32))
     utts = [bl.Utterance(f"b{i}", bl.PosteriorGrid(g)) for i, g in enumerate(G)]
     dec = bl.Decoder(bl.UniformScorer(V - 1), bl.DecoderConfig(beam_width=B, margin_m2=M2))
     for rep in range(2):
