@@ -187,26 +187,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // in the barrier unit instead of re-issuing try_wait (the spin loop was ~8%
 // of the streaming loop's instructions; the other CTA on the SM gets the
 // issue slots)
-__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
-      "@!p bra WS_%=;\n}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000u)
-      : "memory");
-}
 __device__ __forceinline__ void mbar_wait_sleep_s(unsigned bar, unsigned parity) {
-#ifdef BL_WAIT_SPIN
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WS_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WS_%=;\n}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-  return;
-#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WS_%=:\n\t"
@@ -1609,9 +1590,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           __syncwarp();
           if (lane == 0) {
             if (j + NST < J) {
-#ifndef BL_NO_REFILL_FENCE
               asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
               // job j + NST reuses this slot: its (tile, chunk) from this
               // job's without a division
               int kk = k + NST, tt = tile;
