@@ -92,16 +92,13 @@ __device__ __forceinline__ double gread(const double* a, int i, int vlo, int cov
 // scorer the output GEMM's fp32 logits and the row's fp64 log-normaliser:
 // att = (double)logit - lse, attf = (float)((1 - lambda) att) -- the values
 // materialised rows would hold. The fp32 attf rows (every key reads one) are
-// materialised by the log-softmax kernel unless it is fused into the GEMM.
+// always materialised (by the log-softmax kernel, or after the fused GEMM
+// epilogue's normaliser): a branch here cost the vocab-500 kernel 4%.
 __device__ __forceinline__ double att_at(const KParams& P, int row, int c) {
   if (P.net_lse) return (double)P.net_logits[(size_t)row * P.V + c] - P.net_lse[row];
   return P.sc_rows[(size_t)row * P.V + c];
 }
 __device__ __forceinline__ float attf_at(const KParams& P, int row, int c) {
-  if (P.net_lse && !P.sc_rowsf) {
-    const double v = (double)P.net_logits[(size_t)row * P.V + c] - P.net_lse[row];
-    return P.lambda >= 1.0 ? 0.f : (float)((P.lambda <= 0.0 ? 1.0 : 1.0 - P.lambda) * v);
-  }
   return P.sc_rowsf[(size_t)row * P.V + c];
 }
 

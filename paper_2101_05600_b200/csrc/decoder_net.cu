@@ -814,6 +814,17 @@ __global__ void dec_lse_kernel(const double* __restrict__ part, int stride, int 
   lse[r] = m + log(sum);
 }
 
+// fused mode: the fp32 (1 - lambda) att rows from the logits and the fp64
+// normaliser (the search's certified keys read these rows)
+__global__ void dec_attf_kernel(const float* __restrict__ logits, const double* __restrict__ lse,
+                                int V, double lambda, float* __restrict__ attf) {
+  const size_t r = blockIdx.x;
+  const double l = lse[r];
+  const double sc = lambda <= 0.0 ? 1.0 : 1.0 - lambda;
+  for (int c = threadIdx.x; c < V; c += blockDim.x)
+    attf[r * V + c] = lambda >= 1.0 ? 0.f : (float)(sc * ((double)logits[r * V + c] - l));
+}
+
 // Row normalisation modes. Default: one warp per row writes the fp32 attf
 // row (every certified key reads one) and the fp64 log-normaliser; the search
 // derives the few fp64 att values it needs as (double)logit - lse, so the
@@ -1044,7 +1055,7 @@ const float* dec_attf(const DecoderNet* n) { return n->attf; }
 const float* dec_logits(const DecoderNet* n) { return n->logits; }
 const double* dec_lse(const DecoderNet* n) { return n->lse; }
 int dec_launches_per_step(const DecoderNet* n) {
-  return 6 + 11 * n->s.layers + (n->lse_part ? 1 : 0);
+  return 6 + 11 * n->s.layers + (n->lse_part ? 2 : 0);
 }
 
 cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16* memory, int T2,
@@ -1056,8 +1067,8 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
   const size_t need = b_kvc + b_kv2 + al(M * d * 4) + 3 * al(M * d * 2) + al(M * 3 * d * 2) +
                       al(M * s.dff * 2) + al(M * s.vocab * 4) +
                       (fused_log_softmax() ? al(M * ((s.vocab + 127) / 128) * 16) + al(M * 8)
-                                           : al(M * s.vocab * 4) + al(M * s.vocab * 8) +
-                                                 al(M * 8)) +
+                                           : al(M * s.vocab * 8) + al(M * 8)) +
+                      al(M * s.vocab * 4) +
                       2 * al(M * S * 4) + 2 * al(M * 4);
   cudaError_t e;
   if (need > n->ws_bytes) {
@@ -1086,12 +1097,12 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
   n->attf = nullptr;
   n->att = nullptr;
   n->lse_stride = 0;
+  n->attf = reinterpret_cast<float*>(take(M * s.vocab * 4));
   if (fused_log_softmax()) {
     n->lse_stride = (s.vocab + 127) / 128;
     n->lse_part = reinterpret_cast<double*>(take(M * n->lse_stride * 16));
     n->lse = reinterpret_cast<double*>(take(M * 8));
   } else {
-    n->attf = reinterpret_cast<float*>(take(M * s.vocab * 4));
     if (rows_log_softmax()) n->att = reinterpret_cast<double*>(take(M * s.vocab * 8));
     else n->lse = reinterpret_cast<double*>(take(M * 8));
   }
@@ -1194,6 +1205,7 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
     g.lse_part = n->lse_part; g.lse_stride = n->lse_stride;
     if ((e = gemm_bf16(g, st)) != cudaSuccess) return e;
     dec_lse_kernel<<<(M + 127) / 128, 128, 0, st>>>(n->lse_part, n->lse_stride, M, n->lse);
+    dec_attf_kernel<<<M, 256, 0, st>>>(n->logits, n->lse, s.vocab, lambda, n->attf);
     return cudaGetLastError();
   }
   if ((e = n->gemm(M, s.vocab, d, n->Y, n->wout, kPlain, n->bout, n->logits, nullptr, s.vocab,

@@ -12,6 +12,9 @@
   (a miss = the reference asked for a prefix the device never scored).
 """
 import ctypes as C
+import os
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -126,6 +129,20 @@ def test_transformer_search_vs_reference_replay(ref, espec, dspec, n, frames, be
         assert g.tokens == r.tokens and g.label_times == r.label_times, (g.id, g.tokens, r.tokens)
         assert g.steps_taken == r.steps and g.eos_trigger == r.eos_trigger
         assert abs(g.joint_logp - r.joint_logp) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_fused_log_softmax_mode_vs_reference_replay():
+    """BL_FUSED_LOG_SOFTMAX=1 (normaliser partials in the output GEMM's
+    epilogue, attf rows materialised after it): the replay parity above, in a
+    fresh process (the mode is read once per process)."""
+    env = dict(os.environ, BL_FUSED_LOG_SOFTMAX="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "-p", "no:cacheprovider",
+                        __file__ + "::test_transformer_search_vs_reference_replay"],
+                       env=env, cwd=os.path.dirname(os.path.dirname(__file__)),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 
 @pytest.mark.gpu
