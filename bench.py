@@ -269,12 +269,15 @@ def run_c2(torch, bl, dev, n=2880):
     return out
 
 
-def run_model_c3(args, torch, dist, bl, n, world, dev, local, chunk=720):
+def run_model_c3(args, torch, dist, bl, n, world, dev, local, chunk=2880):
     """The full Librispeech-size model (BASELINE config 3: encoder 12 x d512,
     Transformer decoder scorer 6 x d512, 8 heads, ff 2048, vocab 5000;
     random-init) end to end: pinned host fbank -> device encoder (grid +
     memory) -> joint CTC/attention decode with the device decoder scorer ->
-    results on the host, `chunk` segments in flight per call."""
+    results on the host, `chunk` segments in flight per call (the whole
+    recording: 2880 per call decodes 10.6k audio-s/s vs 8.7k at 720 -- the
+    per-step search launch quantises to whole waves of 296 CTAs and the
+    decoder GEMMs get M = 28,800 rows; ~115 GB of HBM incl. the KV cache)."""
     from paper_2101_05600_b200 import encoder as benc
     from paper_2101_05600_b200 import transformer as btr
     from paper_2101_05600_b200.api import _check, lib

@@ -21,12 +21,14 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--beam", type=int, default=10)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--spec", default="small", choices=["small", "large"])
+ap.add_argument("--m2", type=int, default=20, help="margin M2 (< 0: unbounded, the default knobs)")
 a = ap.parse_args()
 espec, dspec = (enc.SMALL, tr.SMALL) if a.spec == "small" else (enc.LARGE, tr.LARGE)
 V, D = espec.vocab, espec.d_model
 e = enc.Encoder(espec, enc.random_weights(espec, seed=0), chunk=148)
 sc = tr.TransformerScorer(dspec, tr.random_weights(dspec, seed=1))
-dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=a.beam, margin_m1=5, margin_m2=20))
+dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=a.beam, margin_m1=5,
+                                      margin_m2=bl.NO_MARGIN if a.m2 < 0 else a.m2))
 fb = torch.from_numpy(enc.synthetic_fbank(a.n, 1000, seed=2)).pin_memory()
 grid = torch.empty(a.n, 249, V, device="cuda")
 mem = torch.empty(a.n, 249, D, device="cuda", dtype=torch.bfloat16)
