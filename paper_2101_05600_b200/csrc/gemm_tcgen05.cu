@@ -1,7 +1,8 @@
 // gemm_tcgen05.cu — bf16 GEMM on the sm_100a 5th-generation tensor cores for
 // the encoder (SURVEY §8 a'1): C[M,N] = A[M,K] · B[N,K]^T, fp32 accumulation
 // in tensor memory, fused epilogue (bias, ReLU, residual, scale + positional
-// table), bf16 and/or fp32 output.
+// table), bf16 and/or fp32 output. The residual epilogue (x += acc + bias)
+// never reads x: each chunk goes out as a TMA reduce-add (fp32 add in L2).
 //
 // Persistent, warp-specialised kernel, one CTA per SM, 192 threads:
 //   warp 0 (one lane) : TMA producer — cp.async.bulk.tensor.2d (SWIZZLE_128B)
@@ -257,11 +258,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (g.mode == kRelu) {
 #pragma unroll
           for (int j = 0; j < 64; ++j) x[j] = fmaxf(x[j], 0.f);
-        } else if (g.mode == kResidual || g.mode == kScalePe) {
-          const float* src = g.mode == kResidual
-                                 ? g.out_f32 + (size_t)row * g.ldo + col0
-                                 : g.pe + (size_t)(row % g.pe_rows) * g.N + col0;
-          const float sc = g.mode == kResidual ? 1.f : g.scale;
+        } else if (g.mode == kScalePe) {
+          // (kResidual needs no read: the chunk is added to the residual
+          // stream in global memory by a TMA reduce-add below)
+          const float* src = g.pe + (size_t)(row % g.pe_rows) * g.N + col0;
+          const float sc = g.scale;
           if (row_ok && full_cols && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) {  // 32 columns (fp32 output)
@@ -312,6 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
           if (kConv)
             tma_store3d(qrows == 32 ? &tOb : &tOr, sb, col0, cy, cz);
+          else if (g.mode == kResidual)
+            tma_reduce_add2d(tO, sb, col0, rbase);
           else
             tma_store2d(tO, sb, col0, rbase);
           bulk_commit();

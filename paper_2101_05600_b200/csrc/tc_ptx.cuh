@@ -99,6 +99,16 @@ __device__ __forceinline__ void tma_store2d(const CUtensorMap* m, const void* sr
       "r"(s32(src)), "r"(x), "r"(y)
       : "memory");
 }
+// element-wise fp32 add of the shared tile into global memory (the L2 does
+// the read-modify-write): a residual update without reading the residual
+__device__ __forceinline__ void tma_reduce_add2d(const CUtensorMap* m, const void* src, int x,
+                                                 int y) {
+  asm volatile(
+      "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], "
+      "[%1];" ::"l"(reinterpret_cast<uint64_t>(m)),
+      "r"(s32(src)), "r"(x), "r"(y)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }

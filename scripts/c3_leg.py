@@ -18,7 +18,9 @@ if len(sys.argv) > 2:
 beam = int(sys.argv[3]) if len(sys.argv) > 3 else bench.BEAM
 dev = torch.device("cuda", 0)
 g = bench.segment_grids(torch, 0, n, dev, 100000)
-dec = bl.Decoder(bl.UniformScorer(bench.VOCAB - 1), bl.DecoderConfig(beam_width=beam))
+# C3_STEP=1: step-granular search (one launch per step, state saved in HBM)
+dec = bl.Decoder(bl.UniformScorer(bench.VOCAB - 1), bl.DecoderConfig(beam_width=beam),
+                 step_mode=os.environ.get("C3_STEP") == "1")
 stride = bench.T_ENC * bench.VOCAB * 4
 descs = [(f"c3_{i}", bench.T_ENC, bench.VOCAB, g.data_ptr() + i * stride) for i in range(n)]
 torch.cuda.synchronize()
