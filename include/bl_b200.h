@@ -165,6 +165,12 @@ int bl_results_stats(const bl_results* r, double* kernel_ms, uint64_t* k1_bytes,
 /* Instrumentation: keys the on-chip filter kept during the prefix-score
  * bulk (large vocabularies), summed over utterance-steps. */
 int bl_results_filter_keys(const bl_results* r, uint64_t* raw_keys);
+/* Instrumentation: wide steps (beams of 13+), i.e. steps whose contender
+ * count exceeded the chain slots (3B+16) while the theta0 list stayed
+ * complete; they are decided from exact scores of the listed candidates in
+ * the candidate order of batched.cpp:181-186, instead of the full fp64
+ * fallback over all B x (|C|+1) candidates. */
+int bl_results_wide_steps(const bl_results* r, uint64_t* wide_steps);
 /* Bulk export (one call for all utterances): row i of tokens/label_times
  * (stride cap >= bl_results_max_tokens) holds n_tokens[i] entries. */
 int bl_results_max_tokens(const bl_results* r);

@@ -106,6 +106,8 @@ def lib() -> C.CDLL:
     L.bl_results_stats.argtypes = [vp, dp, u64p, ip, u64p, u64p]
     L.bl_results_profile.argtypes = [vp, dp]
     L.bl_results_filter_keys.argtypes = [vp, u64p]
+    if hasattr(L, "bl_results_wide_steps"):  # (absent in pre-round-2 A/B builds)
+        L.bl_results_wide_steps.argtypes = [vp, u64p]
     L.bl_results_transfer.argtypes = [vp, u64p, u64p]
     L.bl_results_max_tokens.argtypes = [vp]
     L.bl_results_export.argtypes = [vp, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -696,6 +698,9 @@ class Decoder:
         rk = C.c_uint64()
         L.bl_results_filter_keys(h, C.byref(rk))
         self.last_stats["filter_keys"] = rk.value
+        if hasattr(L, "bl_results_wide_steps"):
+            L.bl_results_wide_steps(h, C.byref(rk))
+            self.last_stats["wide_steps"] = rk.value
         if os.environ.get("BL_PROFILE"):
             prof = (C.c_double * 16)()
             L.bl_results_profile(h, prof)

@@ -285,6 +285,7 @@ struct bl_results {
   int max_tokens = 0;
   uint64_t steps = 0, queries = 0, frames = 0, k1 = 0, fallback = 0, contenders = 0;
   uint64_t raw_keys = 0;  // filter mode: keys that reached the running bound
+  uint64_t wide = 0;      // wide steps (beams of 13+: contenders > caps, complete theta0 list)
   uint64_t h2d = 0, d2h = 0;
   double kernel_ms = 0.0;
   int launches = 0;
@@ -535,7 +536,12 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   // leave at least ceil((B + bmax) / 32) warps to it.
   const int bmax0 = bl::bmax_for(B);
   const int chain_warps = bl::kNWarp - (B + bmax0 + 31) / 32;
-  const int caps = std::min({std::max(2, caps_mult) * B + 16, bl::kNT, 16 * chain_warps});
+  // BL_CAPS: test override (caps >= B: a fallback or wide step's children
+  // take slots 0..B-1); small caps force wide steps at beams of 13+
+  static const int caps_abs = std::getenv("BL_CAPS") ? std::atoi(std::getenv("BL_CAPS")) : 0;
+  const int caps = caps_abs > 0
+                       ? std::min({std::max(B, caps_abs), bl::kNT, 16 * chain_warps})
+                       : std::min({std::max(2, caps_mult) * B + 16, bl::kNT, 16 * chain_warps});
   const int nbest = std::max(1, d->nbest);
   const int rs = bl::res_stride(S, nbest);
   const int U = n;
@@ -636,7 +642,7 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
   size_t region = fixed + need1 <= budget ? budget - fixed : std::max(need0, budget > fixed ? budget - fixed : 0);
   const int kub_smem = (!use_tma && need1 <= region) ? 1 : 0;
   region = (std::max(region, kub_smem ? need1 : need0) + 15) & ~(size_t)15;
-  d->xs.ensure(sizeof(double) * (size_t)U * B * (C + 1));
+  d->xs.ensure(sizeof(double) * (size_t)U * bl::xs_stride(B, C, bmax));
   d->taken.ensure((size_t)U * B * (C + 1));
   d->hist.ensure(sizeof(bl::HistRec) * (size_t)U * (S + 1) * B);
   d->fin.ensure(sizeof(bl::FinEntry) * (size_t)U * B * S);
@@ -977,9 +983,10 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       res->queries += c[1];
       res->frames += c[2];
       res->k1 += c[3];
-      res->fallback += c[4];
+      res->fallback += c[4] & 0xffffffffull;
       res->contenders += c[5];
       res->raw_keys += c[6];
+      res->wide += c[4] >> 32;
     }
     res->max_tokens = S;
     *out = res.release();
@@ -1008,9 +1015,10 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
       res->queries += c[1];
       res->frames += c[2];
       res->k1 += c[3];
-      res->fallback += c[4];
+      res->fallback += c[4] & 0xffffffffull;
       res->contenders += c[5];
       res->raw_keys += c[6];
+      res->wide += c[4] >> 32;
     }
     if (host_timing) {
       auto ms = [](clk::time_point a, clk::time_point b) {
@@ -1049,9 +1057,10 @@ int decode_impl(bl_decoder* d, int n, const bl_utt* utts, int on_device,
     res->queries += c[1];
     res->frames += c[2];
     res->k1 += c[3];
-    res->fallback += c[4];
+    res->fallback += c[4] & 0xffffffffull;
     res->contenders += c[5];
     res->raw_keys += c[6];
+    res->wide += c[4] >> 32;
   }
   *out = res.release();
   return BL_OK;
@@ -1528,6 +1537,10 @@ int bl_results_filter_keys(const bl_results* r, uint64_t* raw_keys) {
   *raw_keys = r->raw_keys;
   return BL_OK;
 }
+int bl_results_wide_steps(const bl_results* r, uint64_t* wide_steps) {
+  *wide_steps = r->wide;
+  return BL_OK;
+}
 int bl_results_max_tokens(const bl_results* r) { return r->max_tokens; }
 
 int bl_results_get(const bl_results* r, int i, const char** id, const int** tokens,
@@ -1828,6 +1841,7 @@ int bl_recognize(bl_encoder* e, bl_decoder* d, const float* fbank, int T, int id
       res->fallback += pp->fallback;
       res->contenders += pp->contenders;
       res->raw_keys += pp->raw_keys;
+      res->wide += pp->wide;
       res->kernel_ms += pp->kernel_ms;
       res->launches += pp->launches + e->launches;
       res->h2d += sizeof(float) * (size_t)m * len * idim;
@@ -2083,6 +2097,7 @@ int bl_group_decode(bl_group* g, int n, const bl_utt* utts, bl_results** out) {
       res->fallback += p->fallback;
       res->contenders += p->contenders;
       res->raw_keys += p->raw_keys;
+      res->wide += p->wide;
       res->h2d += p->h2d;
       res->d2h += p->d2h;
       res->launches += p->launches;

@@ -99,7 +99,7 @@ struct KParams {
                    // 0: keys are filtered on chip against a running bound
                    // while P3 emits them (raw list, kRawCap entries)
   int region_bytes;  // aliased smem region (see smem_plan)
-  double* xs;      // [U][B][C+1]  exact joints (fallback path)
+  double* xs;      // [U][xs_stride(B, C, bmax)]  exact joints (fallback) / wide-step items
   unsigned char* taken;  // [U][B][C+1]
   HistRec* hist;   // [U][S+1][B]
   FinEntry* fin;   // [U][B*S]
@@ -131,6 +131,19 @@ struct KParams {
 // Dynamic shared-memory plan (identical on host and device).
 constexpr int kListCap = 256;  // keys reaching theta0 (P5), 16 B each
 constexpr int kRawCap = 512;   // keys reaching the running bound during P3 (filter mode)
+// Beams of 13+ (BMAX >= 16) on flat posteriors list many more keys: larger
+// lists there (the theta0 list lives in the TMA stage area), and the wide
+// step (decode_kernel.cu P7w) instead of the full fallback when the
+// contenders outnumber the chain slots.
+__host__ __device__ constexpr int list_cap(int bmax) { return bmax >= 16 ? 1024 : kListCap; }
+__host__ __device__ constexpr int raw_cap(int bmax) { return bmax >= 16 ? 2048 : kRawCap; }
+// per-utterance stride (doubles) of KParams::xs: the fallback's B x (|C|+1)
+// joints, or the wide step's items (listed contenders, repeat columns, eos:
+// 24 B each)
+__host__ __device__ inline long long xs_stride(int B, int C, int bmax) {
+  const long long a = (long long)B * (C + 1), b = 3LL * (list_cap(bmax) + 2 * bmax);
+  return bmax >= 16 && b > a ? b : a;  // wide steps only at BMAX >= 16
+}
 
 struct SmemPlan {
   size_t phi, region, items, bbl, total;
@@ -158,7 +171,7 @@ __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, 
   p.ubits = kub_smem ? align16(p.kub + sizeof(float) * (size_t)B * C) : p.kub;
   if (kub_smem) {  // keys mode: every key, its flag, then the theta0 list
     p.clist = align16(p.ubits + sizeof(unsigned) * words);
-    p.raw = p.clist + 16 * (size_t)kListCap;
+    p.raw = p.clist + 16 * (size_t)list_cap(bmax);
     p.stages = p.raw;
     p.region_need = p.raw;
   } else {
@@ -167,7 +180,7 @@ __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, 
     // (cp.async.bulk.tensor dst); the theta0 list is built after P3, so with
     // TMA it takes the stage area, else it follows the raw list
     p.raw = p.kub;
-    const size_t raw_end = p.raw + 8 * (size_t)kRawCap;
+    const size_t raw_end = p.raw + 8 * (size_t)raw_cap(bmax);
     p.stages = ((p.region + raw_end + 127) & ~(size_t)127) - p.region;
     if (tc) p.stages += 1024;  // the kernel aligns the stage ring to 1024 B (swizzle atoms)
     if (tma_stages) {
@@ -175,7 +188,7 @@ __host__ __device__ inline SmemPlan smem_plan(int Tmax, int B, int bmax, int C, 
       p.region_need = p.stages + (size_t)tma_stages * kTmaStageBytes;
     } else {
       p.clist = align16(raw_end);
-      p.region_need = p.clist + 16 * (size_t)kListCap;
+      p.region_need = p.clist + 16 * (size_t)list_cap(bmax);
     }
   }
   p.items = align16(p.region + region_bytes);

@@ -318,6 +318,7 @@ struct Shared {
   float theta, theta2;
   int n_list;
   int th_run, n_raw;  // filter mode: running bound (f2ord) and raw-list size
+  // c_fallback: full fallback steps in the low 32 bits, wide steps in the high 32
   unsigned long long c_queries, c_frames, c_k1, c_fallback, c_cont, c_steps, c_raw;
 };
 
@@ -1092,7 +1093,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
                   }
                 } else if (kub_v >= th) {
                   const int idx = atomicAdd(&sh.n_raw, 1);
-                  if (idx < kRawCap)
+                  if (idx < raw_cap(BMAX))
                     rawl[idx] = make_uint2(__float_as_uint(kub_v),
                                            (under ? 0x80000000u : 0u) | ((unsigned)q << 24) |
                                                (unsigned)c);
@@ -1429,7 +1430,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
                       }
                     } else if (kub_v >= th) {
                       const int idx = atomicAdd(&sh.n_raw, 1);
-                      if (idx < kRawCap)
+                      if (idx < raw_cap(BMAX))
                         rawl[idx] = make_uint2(__float_as_uint(kub_v),
                                                (und ? 0x80000000u : 0u) | ((unsigned)qp << 24) |
                                                    (unsigned)c);
@@ -1761,7 +1762,7 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       auto list_key_qc = [&](int kidx, int q, int c, float ku) {
         if (c != sh.b_last[cur][q]) {
           const int idx = atomicAdd(&sh.n_list, 1);
-          if (idx < kListCap) {
+          if (idx < list_cap(BMAX)) {
             const bool under = (ubits[kidx >> 5] >> (kidx & 31)) & 1u;
             // derived lower bound: never above the key's true lower bound
             clist[idx] = make_float4(
@@ -1798,15 +1799,15 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
         // reach theta0. A raw-list overflow falls back like a list overflow.
         const int nraw = sh.n_raw;
         if (tid == 0) sh.c_raw += nraw;
-        if (nraw > kRawCap) {
-          if (tid == 0) sh.n_list = kListCap + 1;
+        if (nraw > raw_cap(BMAX)) {
+          if (tid == 0) sh.n_list = list_cap(BMAX) + 1;
         } else {
           for (int k = tid; k < nraw; k += kNT) {
             const uint2 e2 = rawl[k];
             const float ku = __uint_as_float(e2.x);
             if (ku >= theta0) {
               const int idx = atomicAdd(&sh.n_list, 1);
-              if (idx < kListCap) {
+              if (idx < list_cap(BMAX)) {
                 // derived lower bound: the one the keys-mode P5 scan lists
                 clist[idx] = make_float4(
                     (e2.y >> 31) ? -INFINITY : ku - 2.000002f * (hw + (fabsf(ku) + hw) * 2.4e-7f),
@@ -1819,9 +1820,9 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       }
       __syncthreads();
       const int nl = sh.n_list;
-      if (nl > kListCap) {
+      if (nl > list_cap(BMAX)) {
         if (tid == 0) sh.n_cont = P.caps + 1;  // overflow: exact fallback
-      } else {
+      } else if constexpr (list_cap(BMAX) <= kNT) {
         if (tid < nl) {
           const float lo = clist[tid].x;
           int rank = 0;
@@ -1831,16 +1832,37 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
           }
           if (rank == B - 1) sh.theta2 = lo;  // unique writer (ranks are distinct)
         }
+      } else {
+        for (int i = tid; i < nl; i += kNT) {
+          const float lo = clist[i].x;
+          int rank = 0;
+          for (int k = 0; k < nl && rank < B; ++k) {
+            const float o = clist[k].x;
+            rank += (o > lo || (o == lo && k < i)) ? 1 : 0;
+          }
+          if (rank == B - 1) sh.theta2 = lo;
+        }
       }
       __syncthreads();
-      if (nl <= kListCap) {
+      if (nl <= list_cap(BMAX)) {
         const float theta = fmaxf(sh.theta2, theta0);
-        if (tid < nl && clist[tid].y >= theta) {
-          const int idx = atomicAdd(&sh.n_cont, 1);
-          if (idx < caps) {
-            items[idx].parent = __float_as_int(clist[tid].z);
-            items[idx].token = __float_as_int(clist[tid].w);
+        if constexpr (list_cap(BMAX) <= kNT) {
+          if (tid < nl && clist[tid].y >= theta) {
+            const int idx = atomicAdd(&sh.n_cont, 1);
+            if (idx < caps) {
+              items[idx].parent = __float_as_int(clist[tid].z);
+              items[idx].token = __float_as_int(clist[tid].w);
+            }
           }
+        } else {
+          for (int i = tid; i < nl; i += kNT)
+            if (clist[i].y >= theta) {
+              const int idx = atomicAdd(&sh.n_cont, 1);
+              if (idx < caps) {
+                items[idx].parent = __float_as_int(clist[i].z);
+                items[idx].token = __float_as_int(clist[i].w);
+              }
+            }
         }
       }
       if (warp == kNWarp - 1 && lane < nb && sh.b_last[cur][lane] >= 0) {
@@ -2043,11 +2065,73 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       group_sync(gw0);
       if (gw0 == 0) PROF_MARK(7);
       }  // decision group
+    } else if (BMAX >= 16 && !P.exact && sh.n_list <= list_cap(BMAX)) {
+      // ---- P7w, wide step (beams of 13+): more contenders than chain slots
+      // (caps), but the theta0 list of P5 is complete. Every candidate the
+      // full fallback could select scores >= the B-th best exact non-eos
+      // score >= theta (B listed candidates certainly reach theta), so it is
+      // a listed key reaching theta, a repeat column or an eos candidate:
+      // their exact fp64 scores (reference operation order, psi_only)
+      // ranked with the fallback's comparator give the fallback's
+      // selection. The children's states follow the walk (fallback tail).
+      if (warp == kNWarp - 1) eos_items();
+      Item* wi = reinterpret_cast<Item*>(P.xs + (size_t)u * xs_stride(B, C, BMAX));
+      const int nl = sh.n_list;
+      const float theta = fmaxf(sh.theta2, sh.theta);
+      if (tid == 0) sh.n_cont = 0;
+      __syncthreads();
+      for (int i = tid; i < nl; i += kNT)
+        if (clist[i].y >= theta) {
+          const int idx = atomicAdd(&sh.n_cont, 1);
+          wi[idx].parent = __float_as_int(clist[i].z);
+          wi[idx].token = __float_as_int(clist[i].w);
+        }
+      if (warp == 0 && lane < nb && sh.b_last[cur][lane] >= 0) {
+        const int idx = atomicAdd(&sh.n_cont, 1);  // repeat column
+        wi[idx].parent = lane;
+        wi[idx].token = sh.b_last[cur][lane];
+      }
+      __syncthreads();
+      const int nw = sh.n_cont;
+      for (int q = tid; q < nw; q += kNT) {
+        const int j = wi[q].parent, c = wi[q].token;
+        const double att = __dadd_rn(sh.b_att[cur][j], att_at(P, sh.b_row[cur][j], c));
+        const double psi = lam <= 0.0 ? kLogZero
+                                      : psi_only<BMAX>(P, sh, u, cur, j, c, s, e, grid,
+                                                       phi + (size_t)j * P.Tmax, tb);
+        wi[q].score = mix_joint(lam, psi, att);
+      }
+      if (tid < nb) wi[nw + tid] = items[caps + tid];  // eos, scored before the first barrier
+      __syncthreads();
+      const int ni = nw + nb;
+      for (int i = tid; i < ni; i += kNT) {
+        const Item me = wi[i];
+        int rank = 0;
+        for (int k = 0; k < ni && rank < B + nb; ++k) {
+          const Item o = wi[k];
+          rank += before(o.score, o.parent, o.token, me.score, me.parent, me.token) ? 1 : 0;
+        }
+        if (rank < B + nb) {
+          SelE x;
+          x.score = me.score;
+          x.parent = me.parent;
+          x.token = me.token;
+          x.slot = -1;
+          x.tau = x.taut = 0;
+          sh.sel[rank] = x;
+        }
+      }
+      if (tid == 0) {
+        sh.nsel = min(ni, B + nb);
+        sh.c_fallback += 1ull << 32;
+      }
+      __syncthreads();
+      PROF_MARK(8);
     } else {
       // ---- fallback: fp64 scores for every candidate + exact selection ----
       if (warp == 0) eos_items();
       __syncthreads();
-      double* xs = P.xs + (size_t)u * B * (C + 1);
+      double* xs = P.xs + (size_t)u * xs_stride(B, C, BMAX);
       unsigned char* taken = P.taken + (size_t)u * B * (C + 1);
       const int total = nb * (C + 1);
       for (int idx = tid; idx < total; idx += kNT) {

@@ -28,5 +28,7 @@ for _ in range(2):
     dec.decode_raw(descs, on_device=True)
 st = dec.last_stats
 gbs = st["k1_bytes"] / (st["kernel_ms"] / 1000.0) / 1e9
-print("c3 %d segments T %d B %d: kernel %.2f ms  %.0f GB/s  frac %.3f  filter_keys/step %.1f" % (
-    n, bench.T_ENC, beam, st["kernel_ms"], gbs, gbs / bench.peaks()[0], st["filter_keys"] / max(1, st["steps"])))
+print("c3 %d segments T %d B %d: kernel %.2f ms  %.0f GB/s  frac %.3f  filter_keys/step %.1f"
+      "  fallback %d wide %s" % (
+    n, bench.T_ENC, beam, st["kernel_ms"], gbs, gbs / bench.peaks()[0],
+    st["filter_keys"] / max(1, st["steps"]), st["fallback_steps"], st.get("wide_steps", "-")))

@@ -11,6 +11,7 @@ columns) ties hundreds of candidates, so the contender set overflows and the
 exact fallback runs on some steps (fallback_steps > 0)."""
 import json
 import os
+import subprocess
 import sys
 
 import numpy as np
@@ -87,3 +88,45 @@ def test_c3_shape_device_resident(c3):
     got = list(dec.decode_raw([(u, g.shape[1], V, g.data_ptr() + i * stride)
                                for i, (u, _) in enumerate(items)], on_device=True))
     _check(got, exp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("beam", [16, 20])
+def test_large_beam_vs_reference(c3, ref, beam):
+    """Beams of 13+ (BMAX >= 16: 1024-entry theta0 list, wide steps) at
+    vocab 5000 on the first 48 frames of four C3 golden grids, fast and
+    step-granular, against the compiled reference. Under BL_CAPS (a fresh
+    process, test_wide_steps_forced) the chain slots shrink to B and nearly
+    every step is decided as a wide step."""
+    import pyoracle as po
+    _, items = c3
+    grids = [np.ascontiguousarray(g[:48]) for _, g in items[:4]]
+    ids = [u for u, _ in items[:4]]
+    want, wc = ref.decode(grids, po.ScorerSpec("uniform", V - 1), po.config(beam_width=beam),
+                          ids=ids)
+    for step in (False, True):
+        dec = bl.Decoder(bl.UniformScorer(V - 1), bl.DecoderConfig(beam_width=beam),
+                         step_mode=step)
+        got = dec.decode([bl.Utterance(u, bl.PosteriorGrid(g)) for u, g in zip(ids, grids)])
+        for g, w in zip(got, want):
+            assert g.tokens == w.tokens and g.label_times == w.label_times, (g.id, step)
+            assert g.steps_taken == w.steps and g.eos_trigger == w.eos_trigger
+            assert abs(g.joint_logp - w.joint_logp) <= TOL
+        if os.environ.get("BL_CAPS"):
+            assert dec.last_stats["wide_steps"] > dec.last_stats["steps"] // 4, dec.last_stats
+
+
+@pytest.mark.gpu
+def test_wide_steps_forced():
+    """BL_CAPS=1 leaves B chain slots: the large-beam parity above and the
+    randomised sweep (beams 16/24/32 among its cases) with nearly every
+    large-beam step decided as a wide step, in a fresh process (the
+    override is read once per process)."""
+    env = dict(os.environ, BL_CAPS="1", BL_FUZZ_CASES="48")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "-p", "no:cacheprovider",
+                        __file__ + "::test_large_beam_vs_reference",
+                        os.path.join(HERE, "test_gpu_fuzz.py")],
+                       env=env, cwd=os.path.dirname(HERE), capture_output=True, text=True,
+                       timeout=1500)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
