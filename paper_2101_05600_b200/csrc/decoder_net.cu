@@ -519,13 +519,26 @@ __global__ void __launch_bounds__(kW * 32, kMinB)
   const __nv_bfloat16* rows = qsrc + ((size_t)u * B + q0) * qs;
   int n = T;  // entries: the memory rows (cross), else the union below
   if constexpr (!kCross) {
-  // this step's K and V into the cache (position l-1, own slot)
-  for (int i = tid; i < nb * 32; i += blockDim.x) {
-    const int k = i >> 5, w = i & 31;
-    const __nv_bfloat16* r = rows + k * d3 + h * kDk;
-    __nv_bfloat16* dst = kv + (((size_t)u * S + l - 1) * B + k) * d2 + h * kDk;
-    reinterpret_cast<uint32_t*>(dst)[w] = reinterpret_cast<const uint32_t*>(r + d)[w];
-    reinterpret_cast<uint32_t*>(dst + d)[w] = reinterpret_cast<const uint32_t*>(r + 2 * d)[w];
+  // this step's K and V into the cache (position l-1, own slot): 16-byte
+  // chunks (8 per 64-dim head row, K then V), every load of the thread in
+  // flight before its stores (one memory latency, not one per chunk)
+  {
+    constexpr int kPer = (16 * 16 + kW * 32 - 1) / (kW * 32);  // chunks per thread (B <= 16)
+    uint4 v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * kW * 32, k = i >> 4, c = i & 15;  // c < 8: K chunk, else V
+      if (k < nb)
+        v[j] = *reinterpret_cast<const uint4*>(rows + k * d3 + (c < 8 ? d : 2 * d) + h * kDk +
+                                               (c & 7) * 8);
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * kW * 32, k = i >> 4, c = i & 15;
+      if (k < nb)
+        *reinterpret_cast<uint4*>(kv + (((size_t)u * S + l - 1) * B + k) * d2 +
+                                  (c < 8 ? 0 : d) + h * kDk + (c & 7) * 8) = v[j];
+    }
   }
   // union of the live hypotheses' entries, positions in contiguous runs per
   // thread so the block scan keeps position order (deterministic sums)
