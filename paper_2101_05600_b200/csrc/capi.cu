@@ -406,8 +406,34 @@ int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
     CK(cudaMemsetAsync(d->rec_nb.p, 0, sizeof(int) * (size_t)p.U * (p.S + 2), st));
     p.rec_nb = static_cast<int*>(d->rec_nb.p);
   }
+  // From step 2 on, the step (the scorer network's ~6 + 11 L launches and the
+  // search launch) is stream-captured and replayed as ONE graph launch; the
+  // executable graph is updated in place (same topology, new step
+  // arguments) instead of re-instantiated. Record mode and BL_NO_GRAPH run
+  // the launches directly.
+  const bool use_graph = d->net && !d->record && std::getenv("BL_NO_GRAPH") == nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  struct GraphGuard {
+    cudaGraphExec_t* g;
+    ~GraphGuard() {
+      if (*g) cudaGraphExecDestroy(*g);
+    }
+  } gguard{&gexec};
   for (int l = 1; l <= p.S + 1; ++l) {
     p.step_l = l;
+    const bool capture = use_graph && l >= 2 && l <= p.S;
+    if (capture) CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    struct CaptureGuard {  // an error inside the captured region ends the capture
+      cudaStream_t s;
+      ~CaptureGuard() {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive) {
+          cudaGraph_t g = nullptr;
+          if (cudaStreamEndCapture(s, &g) == cudaSuccess && g) cudaGraphDestroy(g);
+          cudaGetLastError();
+        }
+      }
+    } cguard{st};
     if (d->net && l <= p.S) {  // att rows of the beam entering step l
       CK(bl::dec_step(d->net, l, p.hist + (size_t)p.u0 * (p.S + 1) * p.B, (p.S + 1) * p.B,
                       static_cast<const int*>(d->nb_live.p) + p.u0, d->cfg.ctc_weight, st));
@@ -437,7 +463,27 @@ int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
         }
       }
     }
-    CK(bl::launch_decode(p, st));
+    if (capture) {
+      const cudaError_t le = bl::launch_decode(p, st);
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(st, &g);
+      CK(le);
+      CK(ce);
+      cudaGraphExecUpdateResultInfo info;
+      if (!gexec || cudaGraphExecUpdate(gexec, g, &info) != cudaSuccess) {
+        cudaGetLastError();
+        if (gexec) cudaGraphExecDestroy(gexec);
+        gexec = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&gexec, g, 0);
+        cudaGraphDestroy(g);
+        CK(ie);
+      } else {
+        cudaGraphDestroy(g);
+      }
+      CK(cudaGraphLaunch(gexec, st));
+    } else {
+      CK(bl::launch_decode(p, st));
+    }
     ++launches;
     if (l % poll == 0 || l == p.S + 1) {
       CK(cudaMemcpyAsync(d->h_done.p, d->n_done.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
