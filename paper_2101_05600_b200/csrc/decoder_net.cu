@@ -496,49 +496,25 @@ constexpr int kSuKeys = BL_SU_KEYS;  // entries per warp chunk
 #endif
 constexpr int kSuW = BL_SU_WARPS;    // warps per CTA
 constexpr int kSuStages = BL_SU_STAGES;  // staging buffers (2: next stage in flight)
-template <bool kCross, int kKeys, int kW, int kMinB>
-__global__ void __launch_bounds__(kW * 32, kMinB)
-    dec_attn_staged_kernel(int l, const __nv_bfloat16* __restrict__ qsrc, int d, int B,
-                           const int* __restrict__ anc, int S, const int* __restrict__ nb_in,
-                           __nv_bfloat16* __restrict__ kv, int T,
-                           __nv_bfloat16* __restrict__ out) {
-  extern __shared__ __align__(16) unsigned char su_sm[];
-  constexpr int kSt = kW * kKeys;  // entries per stage
-  const int u = blockIdx.x, h = blockIdx.y;
-  const int q0 = kCross ? (int)blockIdx.z * 16 : 0;
+// The union of the live hypotheses' self-attention entries of one
+// utterance at step l: every distinct (position, cache slot) any live
+// hypothesis attends to, tagged with the mask of the hypotheses holding it,
+// in position order (deterministic). Built once per step and utterance and
+// shared by every head and layer of dec_attn_staged_kernel<false>.
+template <int kW>
+__global__ void __launch_bounds__(kW * 32)
+    dec_union_kernel(int l, int B, const int* __restrict__ anc, int S,
+                     const int* __restrict__ nb_in, uint32_t* __restrict__ gent,
+                     int* __restrict__ gent_n) {
+  const int u = blockIdx.x;
   const int nb = l == 1 ? 1 : nb_in[u];
-  if (kCross ? (l > 1 && nb <= q0) : nb <= 0) return;  // finished utterance
-  const int nrow = kCross ? min(16, B - q0) : nb;        // query rows of this CTA
-  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(su_sm);
-  __nv_bfloat16* Vs = Ks + (size_t)kSuStages * kSt * kXKPitch;
-  float* mrg = reinterpret_cast<float*>(su_sm);  // [warps][16*64 + 32] after the last stage
-  uint32_t* ent = reinterpret_cast<uint32_t*>(Vs + (size_t)kSuStages * kSt * kXKPitch);  // [B*S]
-  __shared__ int wsum[kW];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const size_t d2 = 2 * (size_t)d, d3 = 3 * (size_t)d, qs = kCross ? d : d3;
-  const __nv_bfloat16* rows = qsrc + ((size_t)u * B + q0) * qs;
-  int n = T;  // entries: the memory rows (cross), else the union below
-  if constexpr (!kCross) {
-  // this step's K and V into the cache (position l-1, own slot): 16-byte
-  // chunks (8 per 64-dim head row, K then V), every load of the thread in
-  // flight before its stores (one memory latency, not one per chunk)
-  {
-    constexpr int kPer = (16 * 16 + kW * 32 - 1) / (kW * 32);  // chunks per thread (B <= 16)
-    uint4 v[kPer];
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int i = tid + j * kW * 32, k = i >> 4, c = i & 15;  // c < 8: K chunk, else V
-      if (k < nb)
-        v[j] = *reinterpret_cast<const uint4*>(rows + k * d3 + (c < 8 ? d : 2 * d) + h * kDk +
-                                               (c & 7) * 8);
-    }
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      const int i = tid + j * kW * 32, k = i >> 4, c = i & 15;
-      if (k < nb)
-        *reinterpret_cast<uint4*>(kv + (((size_t)u * S + l - 1) * B + k) * d2 +
-                                  (c < 8 ? 0 : d) + h * kDk + (c & 7) * 8) = v[j];
-    }
+  __shared__ int wsum[kW];
+  uint32_t* ent = gent + (size_t)u * (((size_t)B * S + 3) & ~(size_t)3);
+  int n = 0;
+  if (nb <= 0) {
+    if (tid == 0) gent_n[u] = 0;
+    return;
   }
   // union of the live hypotheses' entries, positions in contiguous runs per
   // thread so the block scan keeps position order (deterministic sums)
@@ -587,6 +563,63 @@ __global__ void __launch_bounds__(kW * 32, kMinB)
       for (int k = 0; k < 16; ++k) hm |= (sk[k] == s ? 1u : 0u) << k;
       ent[off++] = (uint32_t)p | ((uint32_t)s << 12) | (hm << 16);
     }
+  }
+  if (tid == 0) gent_n[u] = n;
+}
+
+template <bool kCross, int kKeys, int kW, int kMinB>
+__global__ void __launch_bounds__(kW * 32, kMinB)
+    dec_attn_staged_kernel(int l, const __nv_bfloat16* __restrict__ qsrc, int d, int B,
+                           const int* __restrict__ anc, int S, const int* __restrict__ nb_in,
+                           __nv_bfloat16* __restrict__ kv, int T,
+                           __nv_bfloat16* __restrict__ out,
+                           const uint32_t* __restrict__ gent, const int* __restrict__ gent_n) {
+  extern __shared__ __align__(16) unsigned char su_sm[];
+  constexpr int kSt = kW * kKeys;  // entries per stage
+  const int u = blockIdx.x, h = blockIdx.y;
+  const int q0 = kCross ? (int)blockIdx.z * 16 : 0;
+  const int nb = l == 1 ? 1 : nb_in[u];
+  if (kCross ? (l > 1 && nb <= q0) : nb <= 0) return;  // finished utterance
+  const int nrow = kCross ? min(16, B - q0) : nb;        // query rows of this CTA
+  __nv_bfloat16* Ks = reinterpret_cast<__nv_bfloat16*>(su_sm);
+  __nv_bfloat16* Vs = Ks + (size_t)kSuStages * kSt * kXKPitch;
+  float* mrg = reinterpret_cast<float*>(su_sm);  // [warps][16*64 + 32] after the last stage
+  uint32_t* ent = reinterpret_cast<uint32_t*>(Vs + (size_t)kSuStages * kSt * kXKPitch);  // [B*S]
+  __shared__ int wsum[kW];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t d2 = 2 * (size_t)d, d3 = 3 * (size_t)d, qs = kCross ? d : d3;
+  const __nv_bfloat16* rows = qsrc + ((size_t)u * B + q0) * qs;
+  int n = T;  // entries: the memory rows (cross), else the union below
+  if constexpr (!kCross) {
+  // this step's K and V into the cache (position l-1, own slot): 16-byte
+  // chunks (8 per 64-dim head row, K then V), every load of the thread in
+  // flight before its stores (one memory latency, not one per chunk)
+  {
+    constexpr int kPer = (16 * 16 + kW * 32 - 1) / (kW * 32);  // chunks per thread (B <= 16)
+    uint4 v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * kW * 32, k = i >> 4, c = i & 15;  // c < 8: K chunk, else V
+      if (k < nb)
+        v[j] = *reinterpret_cast<const uint4*>(rows + k * d3 + (c < 8 ? d : 2 * d) + h * kDk +
+                                               (c & 7) * 8);
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int i = tid + j * kW * 32, k = i >> 4, c = i & 15;
+      if (k < nb)
+        *reinterpret_cast<uint4*>(kv + (((size_t)u * S + l - 1) * B + k) * d2 +
+                                  (c < 8 ? 0 : d) + h * kDk + (c & 7) * 8) = v[j];
+    }
+  }
+  // the union of the live hypotheses' entries, built once per step and
+  // utterance by dec_union_kernel (shared by every head and layer)
+  n = gent_n[u];
+  {
+    const uint4* src4 =
+        reinterpret_cast<const uint4*>(gent + (size_t)u * (((size_t)B * S + 3) & ~(size_t)3));
+    uint4* dst4 = reinterpret_cast<uint4*>(ent);
+    for (int i = tid; i < (n + 3) / 4; i += blockDim.x) dst4[i] = src4[i];
   }
   }
   // query fragments: rows lane/4 (+8), dims kc*16 + 2*(lane%4) (+8)
@@ -863,7 +896,9 @@ bool use_warp_log_softmax() {
   return !block;
 }
 
-size_t su_smem(int B, int S) { return stage_smem(kSuKeys, kSuW) + (size_t)B * S * 4; }
+size_t su_smem(int B, int S) {
+  return stage_smem(kSuKeys, kSuW) + (((size_t)B * S + 3) & ~(size_t)3) * 4;
+}
 
 // staged source attention unless BL_CROSS_ATTN=whole (A/B runs)
 bool use_staged_cross_attn() {
@@ -916,6 +951,8 @@ struct DecoderNet {
   double *lse_part = nullptr, *lse = nullptr;  // fused log-softmax (output GEMM epilogue)
   int lse_stride = 0;
   int *anc2[2] = {nullptr, nullptr}, *tok = nullptr, *par = nullptr;
+  uint32_t* gent = nullptr;  // [U][B*S rounded to 4] self-attention union entries
+  int* gent_n = nullptr;     // [U]
 
   ~DecoderNet() {
     if (wbuf) cudaFree(wbuf);
@@ -1068,7 +1105,7 @@ const float* dec_attf(const DecoderNet* n) { return n->attf; }
 const float* dec_logits(const DecoderNet* n) { return n->logits; }
 const double* dec_lse(const DecoderNet* n) { return n->lse; }
 int dec_launches_per_step(const DecoderNet* n) {
-  return 6 + 11 * n->s.layers + (n->lse_part ? 2 : 0);
+  return 6 + 11 * n->s.layers + (n->lse_part ? 2 : 0) + (use_union_self_attn(n->B, n->S) ? 1 : 0);
 }
 
 cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16* memory, int T2,
@@ -1082,7 +1119,8 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
                       (fused_log_softmax() ? al(M * ((s.vocab + 127) / 128) * 16) + al(M * 8)
                                            : al(M * s.vocab * 8) + al(M * 8)) +
                       al(M * s.vocab * 4) +
-                      2 * al(M * S * 4) + 2 * al(M * 4);
+                      2 * al(M * S * 4) + 2 * al(M * 4) +
+                      al((size_t)U * ((B * (size_t)S + 3) & ~(size_t)3) * 4) + al((size_t)U * 4);
   cudaError_t e;
   if (need > n->ws_bytes) {
     if (n->ws) cudaFree(n->ws);
@@ -1122,6 +1160,8 @@ cudaError_t dec_prepare(DecoderNet* n, int U, int B, int S, const __nv_bfloat16*
   n->anc2[0] = reinterpret_cast<int*>(take(M * S * 4));
   n->anc2[1] = reinterpret_cast<int*>(take(M * S * 4));
   n->tok = reinterpret_cast<int*>(take(M * 4));
+  n->gent = reinterpret_cast<uint32_t*>(take((size_t)U * ((B * (size_t)S + 3) & ~(size_t)3) * 4));
+  n->gent_n = reinterpret_cast<int*>(take((size_t)U * 4));
   n->par = reinterpret_cast<int*>(take(M * 4));
   n->U = U; n->B = B; n->S = S; n->T2 = T2;
   if ((e = n->ensure_pe(S + 1)) != cudaSuccess) return e;
@@ -1165,6 +1205,8 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
   const size_t na = (size_t)M * l;
   dec_anc_kernel<<<(unsigned)((na + 255) / 256), 256, 0, st>>>(l, U, B, S, n->par,
                                                                n->anc2[(l - 1) & 1], anc);
+  if (use_union_self_attn(B, S))  // the self-attention entries of step l, once
+    dec_union_kernel<4><<<U, 128, 0, st>>>(l, B, anc, S, nb_live, n->gent, n->gent_n);
   dec_embed_kernel<<<(M * 32 + 255) / 256, 256, 0, st>>>(n->tok, n->emb,
                                                          n->pe + (size_t)(l - 1) * d, d,
                                                          std::sqrt((float)d), n->X, M);
@@ -1178,7 +1220,8 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
       return e;
     if (use_union_self_attn(B, S))
       SELF_ATTN<<<dim3(U, s.heads), kSuW * 32, su_smem(B, S), st>>>(
-          l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, 0, n->AO);
+          l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, 0, n->AO,
+          n->gent, n->gent_n);
     else
       dec_self_attn_kernel<<<dim3(U, s.heads), 32 * B, sa, st>>>(
           l, n->QKV, d, B, anc, S, nb_live, n->kvc + (size_t)li * U * S * B * 2 * d, n->AO);
@@ -1189,7 +1232,8 @@ cudaError_t dec_step(DecoderNet* n, int l, const HistRec* hist, int hstride, con
       return e;
     if (use_staged_cross_attn())
       SRC_ATTN<<<dim3(U, s.heads, (B + 15) / 16), BL_XS_WARPS * 32, xs_smem(), st>>>(
-          l, n->QKV, d, B, nullptr, 0, nb_live, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, n->AO);
+          l, n->QKV, d, B, nullptr, 0, nb_live, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, n->AO,
+          nullptr, nullptr);
     else
       dec_cross_attn_mma_kernel<<<dim3(U, s.heads, (B + 15) / 16), kXW * 32, xm, st>>>(
           l, nb_live, n->QKV, n->kv2 + (size_t)li * U * T2 * 2 * d, T2, d, B, n->AO);
