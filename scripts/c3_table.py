@@ -20,13 +20,15 @@ g = bench.segment_grids(torch, 0, n, dev, 100000)
 row = list(np.full(V, -np.log(V)))
 stride = bench.T_ENC * V * 4
 descs = [(f"t{i}", bench.T_ENC, V, g.data_ptr() + i * stride) for i in range(n)]
-for kind in ("uniform", "table"):
+rng = np.random.default_rng(5)
+noisy = [list(np.log(r / r.sum())) for r in rng.exponential(size=(V - 1, V))]
+for kind in ("uniform", "table", "table_noisy"):
     for step in (False, True):
         if kind == "uniform":
             sc = bl.UniformScorer(V - 1)
         else:
             sc = bl.TableScorer(V - 1, 2)
-            sc._entries = {(t,): row for t in range(V - 1)}
+            sc._entries = {(t,): (row if kind == "table" else noisy[t]) for t in range(V - 1)}
             sc._rebuild()
         dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=bench.BEAM), step_mode=step)
         torch.cuda.synchronize()
