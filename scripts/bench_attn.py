@@ -22,10 +22,11 @@ ap.add_argument("--beam", type=int, default=10)
 ap.add_argument("--profile", action="store_true")
 ap.add_argument("--spec", default="small", choices=["small", "large"])
 ap.add_argument("--m2", type=int, default=20, help="margin M2 (< 0: unbounded, the default knobs)")
+ap.add_argument("--chunk", type=int, default=148, help="encoder segments per chunk")
 a = ap.parse_args()
 espec, dspec = (enc.SMALL, tr.SMALL) if a.spec == "small" else (enc.LARGE, tr.LARGE)
 V, D = espec.vocab, espec.d_model
-e = enc.Encoder(espec, enc.random_weights(espec, seed=0), chunk=148)
+e = enc.Encoder(espec, enc.random_weights(espec, seed=0), chunk=a.chunk)
 sc = tr.TransformerScorer(dspec, tr.random_weights(dspec, seed=1))
 dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=a.beam, margin_m1=5,
                                       margin_m2=bl.NO_MARGIN if a.m2 < 0 else a.m2))
