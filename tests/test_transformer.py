@@ -132,11 +132,17 @@ def test_transformer_search_vs_reference_replay(ref, espec, dspec, n, frames, be
 
 
 @pytest.mark.gpu
-def test_fused_log_softmax_mode_vs_reference_replay():
-    """BL_FUSED_LOG_SOFTMAX=1 (normaliser partials in the output GEMM's
-    epilogue, attf rows materialised after it): the replay parity above, in a
-    fresh process (the mode is read once per process)."""
-    env = dict(os.environ, BL_FUSED_LOG_SOFTMAX="1")
+@pytest.mark.parametrize("var,val", [("BL_FUSED_LOG_SOFTMAX", "1"), ("BL_NO_GRAPH", "1"),
+                                     ("BL_LOG_SOFTMAX", "rows")])
+def test_scorer_modes_vs_reference_replay(var, val):
+    """The replay parity above in a fresh process (each switch is read once
+    per process) for the alternative scorer-step paths: BL_FUSED_LOG_SOFTMAX
+    (normaliser partials in the output GEMM's epilogue, attf rows
+    materialised after it), BL_NO_GRAPH (the step's kernels launched
+    directly instead of one CUDA graph per step), BL_LOG_SOFTMAX=rows (fp64
+    att rows materialised by the warp normaliser and read by the search,
+    instead of the staged normaliser's fp32 rows + fp64 log-normaliser)."""
+    env = dict(os.environ, **{var: val})
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                         "-p", "no:cacheprovider",
                         __file__ + "::test_transformer_search_vs_reference_replay"],
