@@ -197,8 +197,10 @@ def golden_parity(bl, dev):
 
 def run_reference(args, rank, world):
     """The reference arm: oracle/_ref (the unmodified reference compiled here)
-    decoding 10 s vocab-5000 segments of the same workload, one segment per
-    step (about half a minute of all-core CPU work each), so the timed
+    decoding 10 s vocab-5000 segments of the same workload, ceil(2 threads /
+    beam) segments per step (the reference fans its utterance x hypothesis
+    scoring tasks out over OpenMP, batched.cpp:143-157: one segment is only
+    10 tasks), about half a minute of all-core CPU work each, so the timed
     region is capped (--ref-budget seconds) and the steps actually run are
     reported."""
     if rank != 0:
@@ -215,14 +217,16 @@ def run_reference(args, rank, world):
     vals, walls = [], []
     t_start = time.perf_counter()
     kind = cores = None
+    per = max(1, min(4, math.ceil(2 * threads / BEAM)))
     for k in range(args.steps):
         if k > 0 and time.perf_counter() - t_start > args.ref_budget:
             break
-        _, kind, cores, wall = ref_decode([grid(100000 + k, T_ENC)], [f"seg{k}"], threads)
-        vals.append(SEG_AUDIO_S / wall)
+        _, kind, cores, wall = ref_decode([grid(100000 + per * k + j, T_ENC) for j in range(per)],
+                                          [f"seg{per * k + j}" for j in range(per)], threads)
+        vals.append(per * SEG_AUDIO_S / wall)
         walls.append(wall)
-    value = len(walls) * SEG_AUDIO_S / sum(walls)
-    sample = (f"1 x 10 s segment per step (T_enc 249, vocab 5000, beam 10, M2 unbounded, "
+    value = len(walls) * per * SEG_AUDIO_S / sum(walls)
+    sample = (f"{per} x 10 s segments per step (T_enc 249, vocab 5000, beam 10, M2 unbounded, "
               f"flat posteriors), {len(walls)} steps run of {args.steps} requested "
               f"(timed region capped at {args.ref_budget:.0f} s), {threads} threads")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "audio-s/s",
@@ -230,7 +234,7 @@ def run_reference(args, rank, world):
             "warmup": args.warmup, "ms_per_step": 1000 * statistics.mean(walls),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
-            "config": workload_config(len(walls), len(walls), 1, False),
+            "config": workload_config(per * len(walls), per * len(walls), 1, False),
             "cpu_baseline": {"value": value, "unit": "audio-s/s", "cores": cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": "audio-s/s", "h2d_bytes_per_step": 0,
@@ -361,7 +365,7 @@ def main():
     ap.add_argument("--segments", type=int, default=0,
                     help="segments of the recording (default: all 2880)")
     ap.add_argument("--sample", type=int, default=0,
-                    help="CPU-baseline segments (default: ceil(cores / 16), at most 2)")
+                    help="CPU-baseline segments (default: ceil(2 cores / beam), at most 4)")
     ap.add_argument("--ref-budget", type=float, default=150.0,
                     help="reference arm: cap on the timed region in seconds")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -482,7 +486,8 @@ def main():
         parity["mismatches"] += gb
         if not args.no_cpu_baseline and world == 1:
             cores = os.cpu_count() or 1
-            k = args.sample or max(1, min(2, math.ceil(cores / 16)))
+            # >= two OpenMP tasks (utterance x hypothesis) per host thread
+            k = args.sample or max(1, min(4, math.ceil(2 * cores / BEAM)))
             src = host if host is not None else grids
             sample = [np.ascontiguousarray(src[i].cpu().numpy()) for i in range(k)]
             want, kind, used, wall = ref_decode(sample, ids[:k], cores)
