@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(256) conv1_kernel(const float* __restrict__ fb
 
 // LayerNorm over d (biased variance, eps 1e-12), one warp per row, VPL = d/32.
 template <int VPL>
-__global__ void layernorm_kernel(const float* __restrict__ X, int rows, const float* __restrict__ g,
+__global__ void layernorm_scalar_kernel(const float* __restrict__ X, int rows, const float* __restrict__ g,
                                  const float* __restrict__ b, __nv_bfloat16* __restrict__ Y) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
@@ -127,6 +127,56 @@ __global__ void layernorm_kernel(const float* __restrict__ X, int rows, const fl
   for (int i = 0; i < VPL; ++i) {
     const int k = i * 32 + lane;
     y[k] = __float2bfloat16_rn(v[i] * rs * g[k] + b[k]);
+  }
+}
+
+// LayerNorm over d (biased variance, eps 1e-12), one warp per row, VPL = d/32:
+// lane i owns the 4-float groups i, i+32, ... (16-byte loads, 8-byte bf16
+// stores, gamma/beta as float4).
+template <int VPL>
+__global__ void layernorm_kernel(const float* __restrict__ X, int rows, const float* __restrict__ g,
+                                 const float* __restrict__ b, __nv_bfloat16* __restrict__ Y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  constexpr int d = VPL * 32, G = VPL / 4;  // float4 groups per lane (VPL % 4 == 0)
+  const float4* x = reinterpret_cast<const float4*>(X + (size_t)warp * d);
+  float4 v[G];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    v[i] = x[i * 32 + lane];
+    s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mean = s / d;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    v[i].x -= mean; v[i].y -= mean; v[i].z -= mean; v[i].w -= mean;
+    q = fmaf(v[i].x, v[i].x, q);
+    q = fmaf(v[i].y, v[i].y, q);
+    q = fmaf(v[i].z, v[i].z, q);
+    q = fmaf(v[i].w, v[i].w, q);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rs = rsqrtf(q / d + 1e-12f);
+  uint2* y = reinterpret_cast<uint2*>(Y + (size_t)warp * d);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+#pragma unroll
+  for (int i = 0; i < G; ++i) {
+    const int k = i * 32 + lane;
+    const float4 gg = __ldg(g4 + k), bb = __ldg(b4 + k);
+    const __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x * rs * gg.x + bb.x,
+                                                     v[i].y * rs * gg.y + bb.y);
+    const __nv_bfloat162 hi = __floats2bfloat162_rn(v[i].z * rs * gg.z + bb.z,
+                                                     v[i].w * rs * gg.w + bb.w);
+    uint2 o;
+    o.x = *reinterpret_cast<const uint32_t*>(&lo);
+    o.y = *reinterpret_cast<const uint32_t*>(&hi);
+    y[k] = o;
   }
 }
 
@@ -560,7 +610,10 @@ __global__ void __launch_bounds__(256) log_softmax_kernel(float* __restrict__ x,
 template <int VPL>
 void ln_launch(const float* X, int rows, const float* g, const float* b, __nv_bfloat16* Y,
                cudaStream_t st) {
-  layernorm_kernel<VPL><<<(rows + 7) / 8, 256, 0, st>>>(X, rows, g, b, Y);
+  if constexpr (VPL % 4 == 0)
+    layernorm_kernel<VPL><<<(rows + 7) / 8, 256, 0, st>>>(X, rows, g, b, Y);
+  else
+    layernorm_scalar_kernel<VPL><<<(rows + 7) / 8, 256, 0, st>>>(X, rows, g, b, Y);
 }
 
 void launch_layernorm(int d, const float* X, int rows, const float* g, const float* b,
