@@ -273,7 +273,7 @@ def run_c2(torch, bl, dev, n=2880):
     return out
 
 
-def run_model_c3(args, torch, dist, bl, n, world, dev, local, chunk=2880):
+def run_model(args, torch, dist, bl, n, world, dev, local, chunk=2880, which="c3"):
     """The full Librispeech-size model (BASELINE config 3: encoder 12 x d512,
     Transformer decoder scorer 6 x d512, 8 heads, ff 2048, vocab 5000;
     random-init) end to end: pinned host fbank -> device encoder (grid +
@@ -281,24 +281,28 @@ def run_model_c3(args, torch, dist, bl, n, world, dev, local, chunk=2880):
     results on the host, `chunk` segments in flight per call (the whole
     recording: 2880 per call decodes 10.6k audio-s/s vs 8.7k at 720 -- the
     per-step search launch quantises to whole waves of 296 CTAs and the
-    decoder GEMMs get M = 28,800 rows; ~115 GB of HBM incl. the KV cache)."""
+    decoder GEMMs get M = 28,800 rows; ~115 GB of HBM incl. the KV cache).
+    which="c2": BASELINE config 1/2's model (encoder 6 x d256, decoder 3 x
+    d256, 4 heads, vocab 500) at config 2's knobs (M2 = 20)."""
     from paper_2101_05600_b200 import encoder as benc
     from paper_2101_05600_b200 import transformer as btr
     from paper_2101_05600_b200.api import _check, lib
     import ctypes as C
-    espec, dspec = benc.LARGE, btr.LARGE
+    espec, dspec = (benc.LARGE, btr.LARGE) if which == "c3" else (benc.SMALL, btr.SMALL)
+    V = espec.vocab
     enc = benc.Encoder(espec, benc.random_weights(espec, seed=0), device=local, chunk=148)
     sc = btr.TransformerScorer(dspec, btr.random_weights(dspec, seed=1), device=local)
-    dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=BEAM), device=local)
+    dec = bl.Decoder(sc, bl.DecoderConfig(beam_width=BEAM, margin_m2=NO_MARGIN if which == "c3"
+                                          else 20), device=local)
     fb = torch.from_numpy(benc.synthetic_fbank(n, 1000, espec.idim, seed=17 + local))
     fb = fb.pin_memory()
     m = min(chunk, n)
-    grid = torch.empty((m, T_ENC, VOCAB), dtype=torch.float32, device=dev)
+    grid = torch.empty((m, T_ENC, V), dtype=torch.float32, device=dev)
     mem = torch.empty((m, T_ENC, espec.d_model), dtype=torch.bfloat16, device=dev)
     st = torch.cuda.Stream(device=dev)
     enc.set_stream(st.cuda_stream)
     dec.set_stream(st.cuda_stream)
-    stride = T_ENC * VOCAB * 4
+    stride = T_ENC * V * 4
     e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
     t_enc = []
 
@@ -306,7 +310,7 @@ def run_model_c3(args, torch, dist, bl, n, world, dev, local, chunk=2880):
         res_all, enc_ms = [], 0.0
         for c0 in range(0, n, m):
             k = min(m, n - c0)
-            descs = [(f"m{c0 + i}", T_ENC, VOCAB, grid.data_ptr() + i * stride) for i in range(k)]
+            descs = [(f"m{c0 + i}", T_ENC, V, grid.data_ptr() + i * stride) for i in range(k)]
             e0.record(st)
             _check(lib().bl_encoder_forward_mem(
                 enc._h, k, 1000, C.c_void_p(fb.data_ptr() + c0 * 1000 * espec.idim * 4), 0,
@@ -344,11 +348,14 @@ def run_model_c3(args, torch, dist, bl, n, world, dev, local, chunk=2880):
            "decode_steps_max": max(r.steps_taken for r in res),
            "mean_hyp_tokens": statistics.mean(lens),
            "h2d_bytes_per_step": n * 1000 * espec.idim * 4,
-           "model": "encoder 12 x d512 (8 heads, ff 2048) + Transformer decoder scorer 6 x d512 "
-                    "(8 heads, ff 2048), vocab 5000, random-init, synthetic 80-dim fbank; the "
-                    "near-uniform random decoder keeps hypotheses ~T long (worst case for the "
-                    "per-step decoder); device-timed, fbank in pinned host memory -> results "
-                    "on the host"}
+           "model": ("encoder 12 x d512 (8 heads, ff 2048) + Transformer decoder scorer 6 x "
+                     "d512 (8 heads, ff 2048), vocab 5000, DecoderConfig defaults (M2 unbounded)"
+                     if which == "c3" else
+                     "encoder 6 x d256 (4 heads, ff 2048) + Transformer decoder scorer 3 x d256 "
+                     "(4 heads, ff 2048), vocab 500, M2 = 20 (BASELINE config 2's knobs)") +
+                    ", random-init, synthetic 80-dim fbank; the near-uniform random decoder keeps "
+                    "hypotheses ~T long (worst case for the per-step decoder); device-timed, "
+                    "fbank in pinned host memory -> results on the host"}
     del dec, sc, enc, grid, mem
     torch.cuda.empty_cache()
     return out
@@ -502,13 +509,15 @@ def main():
     del host
     torch.cuda.empty_cache()
 
-    c2 = model = None
+    c2 = model = model_c2 = None
     if not args.no_legs:
         if rank == 0 and world == 1:
             c2 = run_c2(torch, bl, dev)
         del dec
         torch.cuda.empty_cache()
-        model = run_model_c3(args, torch, dist, bl, n, world, dev, local)
+        model = run_model(args, torch, dist, bl, n, world, dev, local)
+        torch.cuda.empty_cache()
+        model_c2 = run_model(args, torch, dist, bl, n, world, dev, local, which="c2")
 
     peak, peak_kind = peaks()
     kernel_ms = statistics.mean(kms)
@@ -534,7 +543,7 @@ def main():
                          ("steps", "scorer_queries", "ctc_frames_evaluated", "contenders",
                           "fallback_steps")},
             "c2_vocab500": c2,
-            "model_c3": model}
+            "model_c3": model, "model_c2": model_c2}
     if cpu_line:
         line["cpu_baseline"] = cpu_line
     if rank == 0:
