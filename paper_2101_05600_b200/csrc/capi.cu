@@ -411,7 +411,13 @@ int step_loop(bl_decoder* d, bl::KParams p, cudaStream_t st) {
   // executable graph is updated in place (same topology, new step
   // arguments) instead of re-instantiated. Record mode and BL_NO_GRAPH run
   // the launches directly.
-  const bool use_graph = d->net && !d->record && std::getenv("BL_NO_GRAPH") == nullptr;
+  cudaStreamCaptureStatus cs0 = cudaStreamCaptureStatusNone;
+  const bool capturable = st != cudaStreamLegacy && st != cudaStreamPerThread &&
+                          cudaStreamIsCapturing(st, &cs0) == cudaSuccess &&
+                          cs0 == cudaStreamCaptureStatusNone;
+  cudaGetLastError();
+  const bool use_graph =
+      d->net && !d->record && capturable && std::getenv("BL_NO_GRAPH") == nullptr;
   cudaGraphExec_t gexec = nullptr;
   struct GraphGuard {
     cudaGraphExec_t* g;
