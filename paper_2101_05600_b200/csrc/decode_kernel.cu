@@ -1777,9 +1777,25 @@ __global__ void __launch_bounds__(kNT, (BMAX <= 12 && kMode == 0 ? 3 : 2))
       };
       const int nkeys = nb * C;
       if (keys_mode && C >= kNT) {
-        // (q, c) of kidx kept incrementally (stride kNT <= C: at most one wrap)
-        int q = 0, c = tid;
-        for (int kidx = tid; kidx < nkeys; kidx += kNT) {
+        // (q, c) of kidx kept incrementally (stride kNT <= C: at most one wrap);
+        // four keys loaded before any test (the listing's shared-memory
+        // atomics otherwise order every load after the previous test)
+        int q = 0, c = tid, kidx = tid;
+        for (; kidx + 3 * kNT < nkeys; kidx += 4 * kNT) {
+          float ku[4];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) ku[r] = kub[kidx + r * kNT];
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            if (ku[r] >= theta0) list_key_qc(kidx + r * kNT, q, c, ku[r]);
+            c += kNT;
+            if (c >= C) {
+              c -= C;
+              ++q;
+            }
+          }
+        }
+        for (; kidx < nkeys; kidx += kNT) {
           const float ku = kub[kidx];
           if (ku >= theta0) list_key_qc(kidx, q, c, ku);
           c += kNT;
